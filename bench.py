@@ -1,0 +1,338 @@
+"""NFSGLFT benchmark: nodes/sec of forward + adjoint at BASELINE config 3.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 3] [--m M]
+
+A step is one forward (coefficients -> values at all M nodes) plus one adjoint
+(values -> coefficients) on a fixed plan: BASELINE.json's headline metric
+"NFSGLFT nodes/sec fwd+adj at B=64" on config 3 (B=64, M=1e7 nodes uniform in
+the radius-16 ball, complex128).  Inputs are the seeded synthetic inputs of
+SURVEY 8(d) (no public dataset exists for this path).
+
+N > 1 (torchrun, one rank per GPU): weak scaling, each rank owns its own
+M-node shard drawn from the same distribution; rho is the all-reduce max; the
+adjoint's exchange step is an NCCL all-reduce of the coefficient vector.
+
+--impl reference times the CPU reference path (the oracle port of the
+reference algorithm, oracle/; the reference is pure Python and cannot travel)
+on the host cores, extrapolated from bounded node samples.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 loop, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--m", type=int, default=None, help="override the node count per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-sample", type=int, default=4000)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference(work, rho, sample, rank_threads=0):
+    """The reference algorithm on the host (oracle port): fwd+adj on two
+    rho-pinned node samples, extrapolated T(M) = T_fixed + M t_node."""
+    from oracle import sgl_oracle as o
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    threads = o.oracle_threads() if rank_threads == 0 else rank_threads
+    workers = os.cpu_count() or 1
+    times = {}
+    for s in (max(1, sample // 20), sample):
+        idx = np.linspace(0, work.M - 1, s).astype(np.int64)
+        pts = work.points[idx]
+        vals = work.values[idx]
+        t0 = time.perf_counter()
+        p = o.oracle_plan(work.B, pts, rho=rho)
+        t1 = time.perf_counter()
+        o.oracle_forward(p, work.coeffs, threads=threads, workers=workers)
+        o.oracle_adjoint(p, vals, threads=threads, workers=workers)
+        t2 = time.perf_counter()
+        times[s] = (t2 - t1, t1 - t0)
+    (s0, (a0, _)), (s1, (a1, plan_s)) = sorted(times.items())
+    t_node = max((a1 - a0) / (s1 - s0), 1e-12)
+    t_fixed = max(a0 - s0 * t_node, 0.0)
+    T = t_fixed + work.M * t_node
+    return {"value": work.M / T, "unit": "nodes/s", "cores": int(threads),
+            "kind": "port",
+            "sample": (f"oracle fwd+adj at {s0} and {s1} rho-pinned nodes of the config; "
+                       f"T(M) = {t_fixed:.2f} s + M * {t_node * 1e6:.1f} us extrapolated to M={work.M}; "
+                       f"gridding on {threads} OpenMP threads, scipy.fft on {workers} workers"),
+            "t_fixed_s": t_fixed, "t_node_us": t_node * 1e6, "plan_s_at_sample": plan_s}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_1809_10786_b200 import workloads
+    w = workloads.config(args.config, M=args.m)
+    steps = max(1, min(args.steps, 3))
+    vals = []
+    base = None
+    for i in range(steps + min(args.warmup, 1)):
+        r = cpu_reference(w, w.rho, args.cpu_sample)
+        if i >= min(args.warmup, 1):
+            vals.append(r["value"])
+            base = r
+    v = statistics.median(vals)
+    line = {"metric": "NFSGLFT nodes/sec fwd+adj at B=64", "impl": "reference", "value": v, "unit": "nodes/s",
+            "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": 1e3 * w.M / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic (seeded PCG64, SURVEY 8(d))",
+            "config": {"workload": w.name, "B": w.B, "M": w.M, "q": 16, "sigma": 2},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": ("the reference is a pure-Python package; this arm times the oracle port of its algorithm "
+                     "(oracle/, C gridding with OpenMP + numpy/scipy) on the host, capped at 3 timed steps")}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_10786_b200 as sgl
+    from paper_1809_10786_b200 import _native, workloads
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workloads.config(args.config, M=args.m, seed=rank)
+    # rho: the global maximum radius over all ranks' shards
+    rho_t = torch.tensor([w.rho], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(rho_t, op=dist.ReduceOp.MAX)
+    rho = float(rho_t.item())
+
+    coeffs_h = w.coeffs if w.coeffs.ndim == 1 else w.coeffs[0]
+    pts_d = torch.as_tensor(w.points, device=dev)
+    c_d = torch.as_tensor(coeffs_h, device=dev)
+    v_d = torch.as_tensor(w.values, device=dev)
+    t0 = time.perf_counter()
+    p = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=False)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(pl):
+        f = sgl.forward(pl, c_d)
+        a = sgl.adjoint(pl, v_d)
+        if world > 1:
+            dist.all_reduce(torch.view_as_real(a))
+        return f, a
+
+    # per-kernel timings (CUDA events inside the library, on the launching stream)
+    for _ in range(2):
+        step(pprof)
+    torch.cuda.synchronize()
+    fw, ad = [], []
+    for _ in range(3):
+        step(pprof)
+        torch.cuda.synchronize()
+        fw.append(pprof.stage_ms("forward"))
+        ad.append(pprof.stage_ms("adjoint"))
+    stages_fwd = {k: statistics.median([d[k] for d in fw]) for k in fw[0]}
+    stages_adj = {k: statistics.median([d[k] for d in ad]) for k in ad[0]}
+    stats = pprof.stats
+    pprof.close()
+
+    for _ in range(args.warmup):
+        step(p)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(p)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * w.M / (ms / 1e3)
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        c_h = torch.empty(coeffs_h.shape, dtype=torch.complex128, pin_memory=True).numpy()
+        c_h[:] = coeffs_h
+        v_h = torch.empty(w.values.shape, dtype=torch.complex128, pin_memory=True).numpy()
+        v_h[:] = w.values
+        fo = torch.empty((w.M,), dtype=torch.complex128, pin_memory=True).numpy()
+        ao = torch.empty((p.count,), dtype=torch.complex128, pin_memory=True).numpy()
+        L = _native.lib()
+
+        def e2e_step():
+            _native.check(L.sgl_forward(p._handle, c_h.ctypes.data, 1, fo.ctypes.data, None))
+            _native.check(L.sgl_adjoint(p._handle, v_h.ctypes.data, ao.ctypes.data, None))
+            if world > 1:
+                t = torch.from_numpy(ao).to(dev)
+                dist.all_reduce(torch.view_as_real(t))
+                ao[:] = t.cpu().numpy()
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        e_t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+        e_ms = float(e_t.item())
+        e2e = {"value": world * w.M / (e_ms / 1e3), "unit": "nodes/s",
+               "h2d_bytes_per_step": int(c_h.nbytes + v_h.nbytes),
+               "d2h_bytes_per_step": int(fo.nbytes + ao.nbytes), "ms_per_step": e_ms}
+
+    # roofline of the dominant kernel (FP64 tensor pipe; algorithmic FLOPs)
+    q = 16
+    flop_per_node = 4.0 * (2 * q) ** 3     # 2 real FMAs per nonzero tap, (2q)^3 taps
+    kern = {
+        "gather": {"ms": stages_fwd["window"], "flop": w.M * flop_per_node},
+        "scatter": {"ms": stages_adj["window"], "flop": w.M * flop_per_node},
+    }
+    for k in kern.values():
+        k["tflops"] = k["flop"] / (k["ms"] * 1e-3) / 1e12
+        k["frac"] = k["tflops"] / FP64_PEAK_TFLOPS
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": kern[dom]["frac"], "traffic": traffic,
+            "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
+            "algorithmic": f"{flop_per_node:.0f} FLOP/node x {w.M} nodes per launch"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            r = cpu_reference(w, rho, args.cpu_sample)
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "nodes/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "NFSGLFT nodes/sec fwd+adj at B=64", "value": value, "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded PCG64 inputs of SURVEY 8(d); no public dataset)",
+            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": q, "sigma": 2,
+                       "grid": list(p.nfft.grid_shape), "rho": rho,
+                       "l2": "inputs larger than L2 (grid 1.07 GB, node arrays 0.28 GB per rank)",
+                       "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": 6 * args.steps,
+            "gpu_launches_note": "per step: radial_fwd, sph_fwd, gather_tiled, scatter_tiled, sph_adj, radial_adj "
+                                 "(+ 2 cuFFT executions and 2 memsets, library calls)",
+            "kernels": {k: {"ms": v["ms"], "tflops": v["tflops"], "frac": v["frac"]} for k, v in kern.items()},
+            "stages_ms": {"forward": stages_fwd, "adjoint": stages_adj},
+            "plan": {"seconds": plan_s, **stats},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,125 @@
+/*
+ * sgl_b200.h -- C ABI of the B200-native NFSGLFT (forward + adjoint).
+ *
+ * Drop-in boundary for the hot path of the reference `sglnufft` package
+ * (arXiv 1809.10786).  Plain pointers and sizes only; no torch types.
+ * Each entry point replaces one reference interface (paths relative to the
+ * reference's pkg/src/sglnufft/):
+ *
+ *   sgl_plan_create   <- transform.plan            (transform.py:320-382)
+ *                        + nfft.nfft_plan          (nfft.py:147-207)
+ *   sgl_forward       <- transform.forward         (transform.py:385-395)
+ *                        (batched: K coefficient vectors on one plan)
+ *   sgl_adjoint       <- transform.adjoint         (transform.py:398-429)
+ *   sgl_plan_destroy  <- (garbage collection of SglPlan)
+ *   sgl_last_error    <- the ValueError message text raised by the above
+ *   sgl_plan_get_info <- SglPlan / NfftPlan fields (transform.py:292-317,
+ *                        nfft.py:101-120)
+ *
+ * Pointers to points / coefficients / values may be host or device
+ * (CUDA) memory; the library detects which.  Host outputs are complete when
+ * the call returns; device outputs are complete in stream order.
+ *
+ * Calls on one plan must be serialised (the plan owns its scratch grid),
+ * unlike the CPU reference's "share across threads" (README.md:66-67).
+ */
+#ifndef SGL_B200_H
+#define SGL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sgl_plan sgl_plan;
+
+typedef struct {
+    double re, im;
+} sgl_cdouble;
+
+/* return codes; SGL_EINVAL corresponds to the reference's ValueError */
+enum {
+    SGL_OK = 0,
+    SGL_EINVAL = 1,
+    SGL_ECUDA = 2,
+    SGL_ENOMEM = 3,
+    SGL_EUNSUPPORTED = 4
+};
+
+/* plan flags */
+enum {
+    SGL_FLAG_COMPACT_K1 = 1u << 0,        /* compact_k1=True (transform.py:350)     */
+    SGL_FLAG_EXACT_LAST_STAGE = 1u << 1,  /* exact_last_stage=True: rejected        */
+    SGL_FLAG_GENERIC_GRIDDING = 1u << 2,  /* force the per-node window kernels      */
+    SGL_FLAG_PROFILE = 1u << 3            /* record per-stage CUDA-event timings    */
+};
+
+typedef struct {
+    int32_t B;
+    int64_t M;
+    double rho;
+    int32_t sigma;
+    int32_t q;
+    int32_t n_axis[3];
+    int32_t grid[3];
+    int32_t sigma_axes[3];
+    double sigma_eff[3];
+    double lam[3];
+    int64_t coeff_count;
+    int64_t n_tiles;          /* window tiles built by the plan (0 if generic) */
+    int64_t tile_nodes;       /* nodes covered by tiles                        */
+    int64_t tile_dmma;        /* DMMA m8n8k4 issued per gather pass            */
+    int32_t generic;          /* 1 if the per-node window kernels are used     */
+    double plan_ms;           /* device time of plan construction              */
+} sgl_plan_info;
+
+/* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */
+enum {
+    SGL_STAGE_H2D = 0,
+    SGL_STAGE_BASAL = 1,      /* radial + spherical stage (fwd) / their adjoints */
+    SGL_STAGE_FFT = 2,        /* zero + cuFFT (+ place / crop fused in basal)    */
+    SGL_STAGE_WINDOW = 3,     /* gather (fwd) / scatter (adj)                    */
+    SGL_STAGE_D2H = 4,
+    SGL_STAGE_COUNT = 5
+};
+
+/* Create a plan for M points given as (r, theta, phi) rows (M x 3, C order,
+ * float64).  rho <= 0 selects max r (choose_rho, transform.py:39-43).
+ * stream may be NULL (legacy default stream). */
+int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, int32_t q,
+                    double rho, uint32_t flags, void *stream, sgl_plan **out);
+
+/* Forward: coeffs is K x coeff_count(B) complex128 (mu order), values is
+ * K x M complex128 in the caller's point order. */
+int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdouble *values,
+                void *stream);
+
+/* Adjoint: values is M complex128, coeffs receives coeff_count(B). */
+int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, void *stream);
+
+void sgl_plan_destroy(sgl_plan *plan);
+
+int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info);
+
+/* per-stage device milliseconds of the last forward / adjoint call
+ * (dir 0 = forward, 1 = adjoint); needs SGL_FLAG_PROFILE */
+int sgl_plan_stage_ms(const sgl_plan *plan, int32_t dir, float *ms, int32_t n);
+
+/* Message of the most recent failing call on this thread ("" if none). */
+const char *sgl_last_error(void);
+
+/* Select the CUDA device for subsequent plan creation on this thread
+ * (plans remember their device). */
+int sgl_set_device(int32_t device);
+
+/* Number of visible CUDA devices (0 when none; never fails). */
+int sgl_device_count(int32_t *n);
+
+/* Library version string. */
+const char *sgl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGL_B200_H */

@@ -1,0 +1,394 @@
+// C ABI of the B200 NFSGLFT (include/sgl_b200.h).
+//
+// Mirrors the reference surface transform.plan / forward / adjoint
+// (transform.py:320-429) with the same argument meaning and the same
+// ValueError conditions, reported as SGL_EINVAL + sgl_last_error().
+#include <cufft.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "sgl_internal.cuh"
+
+namespace sgl {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+namespace {
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int fft_check(cufftResult r, const char *what) {
+    if (r != CUFFT_SUCCESS) {
+        set_error(std::string("cuFFT error ") + std::to_string((int)r) + " in " + what);
+        return SGL_ECUDA;
+    }
+    return SGL_OK;
+}
+
+void free_plan(Plan *p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->tiles, p->Kl, p->Km,
+                    p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
+                    p->coef_buf, p->val_buf};
+    for (void *b : bufs)
+        if (b) cudaFree(b);
+    if (p->fft_ready) cufftDestroy(p->fft);
+    for (auto &t : p->timers)
+        if (t.ready)
+            for (auto &e : t.ev) cudaEventDestroy(e);
+    cudaSetDevice(cur);
+    delete p;
+}
+
+struct StageRec {
+    // events recorded in call order; slot i..i+1 is charged to stage_of[i]
+    Plan &p;
+    int dir;
+    cudaStream_t st;
+    bool on;
+    int n = 0;
+    int stage_of[SGL_STAGE_COUNT + 1];
+    StageRec(Plan &pl, int d, cudaStream_t s) : p(pl), dir(d), st(s), on(pl.profile) {
+        for (float &x : p.stage_ms[dir]) x = 0.f;
+    }
+    void mark(int stage) {
+        if (!on || n > SGL_STAGE_COUNT) return;
+        stage_of[n] = stage;
+        cudaEventRecord(p.timers[dir].ev[n], st);
+        ++n;
+    }
+    void flush() {   // accumulate and restart (one forward vector / one adjoint)
+        if (!on || n < 2) {
+            n = 0;
+            return;
+        }
+        cudaEventSynchronize(p.timers[dir].ev[n - 1]);
+        for (int i = 0; i + 1 < n; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.timers[dir].ev[i], p.timers[dir].ev[i + 1]);
+            p.stage_ms[dir][stage_of[i]] += ms;
+        }
+        n = 0;
+    }
+};
+
+}  // namespace
+}  // namespace sgl
+
+using namespace sgl;
+
+extern "C" {
+
+const char *sgl_last_error(void) { return g_err.c_str(); }
+
+int sgl_set_device(int32_t device) {
+    SGL_CUDA_CHECK(cudaSetDevice(device));
+    return SGL_OK;
+}
+
+int sgl_device_count(int32_t *n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    if (n) *n = c;
+    return SGL_OK;
+}
+
+const char *sgl_version(void) { return "sgl-b200 0.1.0 (sm_100a, FP64 DMMA gridding)"; }
+
+int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, int32_t q, double rho,
+                    uint32_t flags, void *stream, sgl_plan **out) {
+    g_err.clear();
+    if (!out) {
+        set_error("output plan pointer is NULL");
+        return SGL_EINVAL;
+    }
+    *out = nullptr;
+    if (B < 1) {
+        set_error("bandwidth must be >= 1");
+        return SGL_EINVAL;
+    }
+    if (M < 0 || (M > 0 && !points)) {
+        set_error("points must be (M, 3) spherical coordinates");
+        return SGL_EINVAL;
+    }
+    if (M > (int64_t)INT32_MAX) {
+        set_error("more than 2^31-1 points per plan: shard the node set");
+        return SGL_EUNSUPPORTED;
+    }
+    if (flags & SGL_FLAG_EXACT_LAST_STAGE) {
+        set_error("exact_last_stage=True is not provided by the B200 backend");
+        return SGL_EUNSUPPORTED;
+    }
+    if (q < 1) {
+        set_error("cutoff parameter q must be >= 1");
+        return SGL_EINVAL;
+    }
+    if (sigma < 2) {
+        set_error("oversampling factor must be an integer >= 2");
+        return SGL_EINVAL;
+    }
+    if ((int64_t)q >= 4LL * sigma * B) {
+        set_error("cutoff q = " + std::to_string(q) + " must be below 4*sigma*B = " + std::to_string(4LL * sigma * B));
+        return SGL_EINVAL;
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    Plan *p = new Plan();
+    cudaGetDevice(&p->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    p->B = B;
+    p->M = M;
+    p->rho = rho;
+    p->sigma = sigma;
+    p->q = q;
+    p->compact = flags & SGL_FLAG_COMPACT_K1;
+    p->profile = flags & SGL_FLAG_PROFILE;
+    p->generic = (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
+    p->n_axis[0] = 4 * B;
+    p->n_axis[1] = p->compact ? 2 * B : 4 * B;
+    p->n_axis[2] = 2 * B;
+    p->count = (int64_t)B * (B + 1) * (2 * B + 1) / 6;
+    // sigma escalation (transform.py:357-362) and geometry (nfft.py:174-182)
+    for (int ax = 0; ax < 3; ++ax) {
+        int s = sigma;
+        auto pow2 = [](int64_t v) {
+            int64_t g = 1;
+            while (g < v) g <<= 1;
+            return g;
+        };
+        while (pow2((int64_t)s * p->n_axis[ax]) <= q) s *= 2;
+        p->sig_axes[ax] = s;
+        p->grid[ax] = (int)pow2((int64_t)s * p->n_axis[ax]);
+        p->s_eff[ax] = (double)p->grid[ax] / p->n_axis[ax];
+        p->lam[ax] = p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
+    }
+    p->grid_elems = (size_t)p->grid[0] * p->grid[1] * p->grid[2];
+    WindowParams &wp = p->wp;
+    wp.N0 = p->grid[0];
+    wp.N1 = p->grid[1];
+    wp.N2 = p->grid[2];
+    wp.q = q;
+    double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
+    for (int ax = 0; ax < 3; ++ax) {
+        const double N = p->grid[ax], a = N / kTwoPi, lam = p->lam[ax];
+        *cs[ax] = a / std::sqrt(kTwoPi * lam);                          // nfft.py:137
+        *hs[ax] = ((kTwoPi / N) * (kTwoPi / N)) * (a * a) / (2.0 * lam);  // nfft.py:138
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    int rc = SGL_OK;
+    const double *dpts = points;
+    double *owned = nullptr;
+    if (M > 0 && !is_device_ptr(points)) {
+        if (cudaMalloc(&owned, sizeof(double) * 3 * M) != cudaSuccess ||
+            cudaMemcpyAsync(owned, points, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            set_error("CUDA error while uploading points");
+            rc = SGL_ECUDA;
+        }
+        dpts = owned;
+    }
+    if (rc == SGL_OK) rc = build_nodes(*p, dpts, st);
+    if (owned) {
+        cudaStreamSynchronize(st);
+        cudaFree(owned);
+    }
+    if (rc == SGL_OK) rc = build_basal_tables(*p);
+    if (rc == SGL_OK) {
+        if (cudaMalloc(&p->grid_buf, sizeof(double2) * p->grid_elems) != cudaSuccess ||
+            cudaMalloc(&p->beta, sizeof(double2) * (size_t)B * B * 4 * B) != cudaSuccess ||
+            cudaMalloc(&p->coef_buf, sizeof(double2) * p->count) != cudaSuccess ||
+            cudaMalloc(&p->val_buf, sizeof(double2) * (M ? M : 1)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("out of device memory for the plan's grid / staging buffers");
+            rc = SGL_ENOMEM;
+        }
+    }
+    if (rc == SGL_OK) {
+        rc = fft_check(cufftPlan3d(&p->fft, p->grid[0], p->grid[1], p->grid[2], CUFFT_Z2Z), "cufftPlan3d");
+        if (rc == SGL_OK) p->fft_ready = true;
+    }
+    if (rc == SGL_OK && p->profile) {
+        for (auto &t : p->timers) {
+            for (auto &e : t.ev) cudaEventCreate(&e);
+            t.ready = true;
+        }
+    }
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    auto t1 = std::chrono::steady_clock::now();
+    p->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    (void)ms;
+    if (rc != SGL_OK) {
+        free_plan(p);
+        return rc;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("CUDA error: ") + cudaGetErrorString(e));
+        free_plan(p);
+        return SGL_ECUDA;
+    }
+    *out = reinterpret_cast<sgl_plan *>(p);
+    return SGL_OK;
+}
+
+void sgl_plan_destroy(sgl_plan *plan) { free_plan(reinterpret_cast<Plan *>(plan)); }
+
+int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
+    if (!plan || !info) {
+        set_error("NULL plan or info");
+        return SGL_EINVAL;
+    }
+    const Plan &p = *reinterpret_cast<const Plan *>(plan);
+    info->B = p.B;
+    info->M = p.M;
+    info->rho = p.rho;
+    info->sigma = p.sigma;
+    info->q = p.q;
+    for (int i = 0; i < 3; ++i) {
+        info->n_axis[i] = p.n_axis[i];
+        info->grid[i] = p.grid[i];
+        info->sigma_axes[i] = p.sig_axes[i];
+        info->sigma_eff[i] = p.s_eff[i];
+        info->lam[i] = p.lam[i];
+    }
+    info->coeff_count = p.count;
+    info->n_tiles = p.n_tiles;
+    info->tile_nodes = p.tile_nodes;
+    info->tile_dmma = p.tile_dmma;
+    info->generic = p.generic ? 1 : 0;
+    info->plan_ms = p.plan_ms;
+    return SGL_OK;
+}
+
+int sgl_plan_stage_ms(const sgl_plan *plan, int32_t dir, float *ms, int32_t n) {
+    if (!plan || !ms || dir < 0 || dir > 1) {
+        set_error("bad arguments to sgl_plan_stage_ms");
+        return SGL_EINVAL;
+    }
+    const Plan &p = *reinterpret_cast<const Plan *>(plan);
+    for (int i = 0; i < n && i < SGL_STAGE_COUNT; ++i) ms[i] = p.stage_ms[dir][i];
+    return SGL_OK;
+}
+
+int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdouble *values, void *stream) {
+    g_err.clear();
+    if (!plan) {
+        set_error("NULL plan");
+        return SGL_EINVAL;
+    }
+    Plan &p = *reinterpret_cast<Plan *>(plan);
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    if (K < 1 || !coeffs || (!values && p.M > 0)) {
+        set_error("coefficient length does not match the bandwidth");
+        return SGL_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool cdev = is_device_ptr(coeffs), vdev = values ? is_device_ptr(values) : true;
+    StageRec rec(p, 0, st);
+    for (int64_t k = 0; k < K; ++k) {
+        rec.mark(SGL_STAGE_H2D);
+        const double2 *c = reinterpret_cast<const double2 *>(coeffs) + k * p.count;
+        if (!cdev) {
+            SGL_CUDA_CHECK(cudaMemcpyAsync(p.coef_buf, c, sizeof(double2) * p.count, cudaMemcpyHostToDevice, st));
+            c = p.coef_buf;
+        }
+        rec.mark(SGL_STAGE_BASAL);
+        int rc = launch_basal_forward(p, c, p.grid_buf, st, nullptr);
+        if (rc) return rc;
+        rec.mark(SGL_STAGE_FFT);
+        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+        if (rc) return rc;
+        rc = fft_check(cufftExecZ2Z(p.fft, reinterpret_cast<cufftDoubleComplex *>(p.grid_buf),
+                                    reinterpret_cast<cufftDoubleComplex *>(p.grid_buf), CUFFT_INVERSE),
+                       "cufftExecZ2Z(inverse)");
+        if (rc) return rc;
+        rec.mark(SGL_STAGE_WINDOW);
+        double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : p.val_buf;
+        rc = launch_gather(p, p.grid_buf, v, st);
+        if (rc) return rc;
+        rec.mark(SGL_STAGE_D2H);
+        if (!vdev && p.M > 0)
+            SGL_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<double2 *>(values) + k * p.M, p.val_buf,
+                                           sizeof(double2) * p.M, cudaMemcpyDeviceToHost, st));
+        rec.mark(SGL_STAGE_COUNT);
+        rec.flush();
+    }
+    if (!vdev) SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, void *stream) {
+    g_err.clear();
+    if (!plan) {
+        set_error("NULL plan");
+        return SGL_EINVAL;
+    }
+    Plan &p = *reinterpret_cast<Plan *>(plan);
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    if (!coeffs || (!values && p.M > 0)) {
+        set_error("values length does not match the plan");
+        return SGL_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool vdev = values ? is_device_ptr(values) : true, cdev = is_device_ptr(coeffs);
+    StageRec rec(p, 1, st);
+    rec.mark(SGL_STAGE_H2D);
+    const double2 *v = reinterpret_cast<const double2 *>(values);
+    if (!vdev && p.M > 0) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf, v, sizeof(double2) * p.M, cudaMemcpyHostToDevice, st));
+        v = p.val_buf;
+    }
+    rec.mark(SGL_STAGE_WINDOW);
+    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+    int rc = launch_scatter(p, v, p.grid_buf, st);
+    if (rc) return rc;
+    rec.mark(SGL_STAGE_FFT);
+    rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+    if (rc) return rc;
+    rc = fft_check(cufftExecZ2Z(p.fft, reinterpret_cast<cufftDoubleComplex *>(p.grid_buf),
+                                reinterpret_cast<cufftDoubleComplex *>(p.grid_buf), CUFFT_FORWARD),
+                   "cufftExecZ2Z(forward)");
+    if (rc) return rc;
+    rec.mark(SGL_STAGE_BASAL);
+    double2 *c = cdev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;
+    rc = launch_basal_adjoint(p, p.grid_buf, c, st);
+    if (rc) return rc;
+    rec.mark(SGL_STAGE_D2H);
+    if (!cdev) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs, p.coef_buf, sizeof(double2) * p.count, cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    rec.mark(SGL_STAGE_COUNT);
+    rec.flush();
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+// Gaussian-window gather (forward NFFT interpolation) and scatter (adjoint
+// spreading) on the oversampled grid, FP64, sm_100a.
+//
+// Reference: _gridding.py:53-74 (_gather_kernel), :77-95 (_scatter_kernel)
+// with the wrap padding of :29-50 replaced by modular cell addressing, and
+// the window of nfft.py:123-144:
+//     w_j(delta) = (N_j/2pi)/sqrt(2 pi lam_j) * exp(-delta^2/(2 lam_j)),
+//     delta = u_j - cell, zero where |delta| > q.
+//
+// Tiled kernels (q <= 16): a tile is <= 32 sorted nodes whose window boxes
+// overlap almost entirely.  Per axis-0 slab of the tile's box the contraction
+// over axis 2 is a real GEMM on the FP64 tensor cores (DMMA m8n8k4):
+//     gather : T[(b,re|im), node] = sum_c G[a,b,c] * W2[c,node]
+//     scatter: D[(b,re|im), c]    = sum_node V[(b,re|im),node] * W2[c,node]
+// and the axis-1 / axis-0 weights are applied in the epilogue (gather) or
+// folded into V (scatter).  Gather slabs are staged into shared memory by
+// bulk async copies (cp.async.bulk, mbarrier-completed) in a 3-deep ring;
+// scatter fragments are reduced into the grid with RED.ADD.F64.
+//
+// Generic kernels (any q, or forced): one warp per node, lanes over axis-2
+// taps, exactly the reference loop nest.
+#include <cuda_runtime.h>
+
+#include "sgl_internal.cuh"
+
+namespace sgl {
+namespace {
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+    i %= n;
+    return i < 0 ? i + n : i;
+}
+
+__device__ __forceinline__ double wfun(double u, int cell, double c, double h, int q) {
+    double d = u - (double)cell;
+    return (fabs(d) <= (double)q) ? c * exp(-d * d * h) : 0.0;
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void red_add(double *addr, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// tiled gather
+
+constexpr int GW = 4;                 // warps per CTA: one per 8-node column tile
+constexpr int GT = GW * 32;
+constexpr int NST = 3;                // slab ring depth
+constexpr int SROWS = kBoxMax;        // slab rows (axis 1)
+constexpr int SSTR = kBoxMax + 4;     // max slab row stride in complex (== 4 mod 8)
+constexpr int KSMAX = kBoxMax / 4;    // k-steps over axis 2
+constexpr int W1S = 40;               // gather w1 row stride (doubles)
+
+struct GatherSmem {
+    double2 slab[NST][SROWS * SSTR];
+    double w0[kBox0Max][kTileNodes];
+    double w1[SROWS][W1S];
+    double nu[3][kTileNodes];
+    uint64_t bar[NST];
+    Tile t;
+};
+
+__device__ __forceinline__ void issue_slab(GatherSmem &S, int lane, const Tile &t, int a, int buf, int stride,
+                                           const WindowParams &wp, const double2 *grid) {
+    const int g0 = wrapi(t.o0 + a, wp.N0);
+    if (lane == 0) mbar_expect_tx(&S.bar[buf], (uint32_t)(t.e1 * t.e2 * 16));
+    __syncwarp();
+    const int g2s = wrapi(t.o2, wp.N2);
+    for (int y = lane; y < t.e1; y += 32) {
+        const int g1 = wrapi(t.o1 + y, wp.N1);
+        const double2 *row = grid + ((size_t)g0 * wp.N1 + g1) * wp.N2;
+        double2 *dst = &S.slab[buf][y * stride];
+        int done = 0, g2 = g2s;
+        while (done < t.e2) {
+            int n = min(t.e2 - done, wp.N2 - g2);
+            bulk_g2s(dst + done, row + g2, (uint32_t)(n * 16), &S.bar[buf]);
+            done += n;
+            g2 = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(GT, 2)
+    k_gather_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
+                   const double2 *__restrict__ grid, double2 *__restrict__ out) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    GatherSmem &S = *reinterpret_cast<GatherSmem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    for (int i = tid; i < NST * SROWS * SSTR; i += GT) (&S.slab[0][0])[i] = make_double2(0.0, 0.0);
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&S.bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+
+    uint32_t seq = 0;
+    const int rb = lane >> 3, part = (lane >> 2) & 1, cc = lane & 3;
+    const int kn = warp * 8 + (lane >> 2);     // node of this lane's B fragment
+    const int kcol = warp * 8 + 2 * cc;        // nodes of this lane's accumulators
+
+    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        if (tid == 0) S.t = tiles[ti];
+        __syncthreads();
+        const Tile t = S.t;
+        if (tid < kTileNodes) {
+            const bool ok = tid < t.count;
+            const int64_t s = (int64_t)t.start + tid;
+            // far-away sentinel: all weights of a missing node are exactly zero
+            S.nu[0][tid] = ok ? nodes.u0[s] : -1e9;
+            S.nu[1][tid] = ok ? nodes.u1[s] : -1e9;
+            S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
+        }
+        __syncthreads();
+        const int Mt = (t.e1 + 3) >> 2;
+        const int KS = (t.e2 + 3) >> 2;
+        const int Cw = KS * 4;
+        const int stride = (Cw & 7) ? Cw : Cw + 4;
+        for (int i = tid; i < t.e0 * kTileNodes; i += GT) {
+            const int x = i / kTileNodes, k = i % kTileNodes;
+            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
+        }
+        for (int i = tid; i < Mt * 4 * kTileNodes; i += GT) {
+            const int y = i / kTileNodes, k = i % kTileNodes;
+            S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
+        }
+        double bfr[KSMAX];
+#pragma unroll
+        for (int ks = 0; ks < KSMAX; ++ks)
+            bfr[ks] = (ks < KS) ? wfun(S.nu[2][kn], t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
+        __syncthreads();
+
+        if (warp == 0) {
+            for (int s = 0; s < NST - 1 && s < t.e0; ++s)
+                issue_slab(S, lane, t, s, (int)((seq + s) % NST), stride, wp, grid);
+        }
+        double acc0 = 0.0, acc1 = 0.0;
+        const bool col_live = warp * 8 < t.count;
+        for (int a = 0; a < t.e0; ++a) {
+            if (warp == 0 && a + NST - 1 < t.e0)
+                issue_slab(S, lane, t, a + NST - 1, (int)((seq + a + NST - 1) % NST), stride, wp, grid);
+            const uint32_t q = seq + a;
+            const int buf = (int)(q % NST);
+            mbar_wait(&S.bar[buf], (q / NST) & 1);
+            const double w0a = S.w0[a][kcol], w0b = S.w0[a][kcol + 1];
+            // skip slabs where none of this warp's 8 nodes has weight (uniform)
+            const bool live = col_live && __any_sync(0xffffffffu, (w0a != 0.0) || (w0b != 0.0));
+            if (live) {
+                const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
+                for (int mt = 0; mt < Mt; mt += 3) {
+                    double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                    for (int ks = 0; ks < KSMAX; ++ks) {
+                        if (ks < KS) {
+#pragma unroll
+                            for (int i = 0; i < 3; ++i) {
+                                if (mt + i < Mt) {
+                                    const int b = (mt + i) * 4 + rb;
+                                    const double av = sl[(b * stride + ks * 4 + cc) * 2 + part];
+                                    dmma(d[i], av, bfr[ks]);
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        if (mt + i < Mt) {
+                            const int b = (mt + i) * 4 + rb;
+                            const double2 w1 = *reinterpret_cast<const double2 *>(&S.w1[b][kcol]);
+                            acc0 = fma(w0a * w1.x, d[i][0], acc0);
+                            acc1 = fma(w0b * w1.y, d[i][1], acc1);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        seq += (uint32_t)t.e0;
+
+        // reduce over the 4 row groups (lane bits 3,4); lanes 0-3 re, 4-7 im
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 8);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 8);
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 16);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 16);
+        const double im0 = __shfl_sync(0xffffffffu, acc0, (lane + 4) & 31);
+        const double im1 = __shfl_sync(0xffffffffu, acc1, (lane + 4) & 31);
+        if (lane < 4) {
+            const int k0 = kcol;
+            if (k0 < t.count) out[nodes.perm[t.start + k0]] = make_double2(acc0, im0);
+            if (k0 + 1 < t.count) out[nodes.perm[t.start + k0 + 1]] = make_double2(acc1, im1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tiled scatter
+
+constexpr int SW = 4;                 // warps per CTA; warps own axis-0 slabs
+constexpr int STH = SW * 32;
+constexpr int WS = 36;                // w1/w2 row stride (doubles), conflict-free
+constexpr int CTMAX = kBoxMax / 8;    // 8-column tiles over axis 2
+constexpr int NKS = kTileNodes / 4;   // node k-steps
+
+struct ScatterSmem {
+    double w0[kBox0Max][kTileNodes];
+    double w1[kBoxMax][WS];
+    double w2[kBoxMax][WS];
+    double2 v[kTileNodes];
+    double nu[3][kTileNodes];
+    Tile t;
+};
+
+__global__ void __launch_bounds__(STH, 4)
+    k_scatter_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
+                    const double2 *__restrict__ values, double *__restrict__ grid) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
+
+    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        __syncthreads();   // previous tile's readers are done
+        if (tid == 0) S.t = tiles[ti];
+        __syncthreads();
+        const Tile t = S.t;
+        if (tid < kTileNodes) {
+            const bool ok = tid < t.count;
+            const int64_t s = (int64_t)t.start + tid;
+            S.nu[0][tid] = ok ? nodes.u0[s] : -1e9;
+            S.nu[1][tid] = ok ? nodes.u1[s] : -1e9;
+            S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
+            S.v[tid] = ok ? values[nodes.perm[s]] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        const int Mt = (t.e1 + 3) >> 2;
+        const int CT = (t.e2 + 7) >> 3;
+        for (int i = tid; i < t.e0 * kTileNodes; i += STH) {
+            const int x = i / kTileNodes, k = i % kTileNodes;
+            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
+        }
+        for (int i = tid; i < Mt * 4 * kTileNodes; i += STH) {
+            const int y = i / kTileNodes, k = i % kTileNodes;
+            S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
+        }
+        for (int i = tid; i < CT * 8 * kTileNodes; i += STH) {
+            const int y = i / kTileNodes, k = i % kTileNodes;
+            S.w2[y][k] = wfun(S.nu[2][k], t.o2 + y, wp.c2, wp.h2, wp.q);
+        }
+        __syncthreads();
+        const int nks = (t.count + 3) >> 2;
+        for (int a = warp; a < t.e0; a += SW) {
+            // active node k-steps on this slab (nodes are sorted by lo0)
+            const unsigned mask = __ballot_sync(0xffffffffu, S.w0[a][lane] != 0.0);
+            if (mask == 0u) continue;
+            const int ks0 = (__ffs(mask) - 1) >> 2;
+            const int ks1 = min(nks, ((31 - __clz(mask)) >> 2) + 1);
+            double wv[NKS];
+#pragma unroll
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int n = ks * 4 + kk;
+                const double2 v = S.v[n];
+                wv[ks] = S.w0[a][n] * (part ? v.y : v.x);
+            }
+            const int g0 = wrapi(t.o0 + a, wp.N0);
+            for (int mt = 0; mt < Mt; ++mt) {
+                const int b = mt * 4 + rb;
+                double d[CTMAX][2];
+#pragma unroll
+                for (int ct = 0; ct < CTMAX; ++ct) d[ct][0] = d[ct][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < NKS; ++ks) {
+                    if (ks >= ks0 && ks < ks1) {
+                        const double av = wv[ks] * S.w1[b][ks * 4 + kk];
+#pragma unroll
+                        for (int ct = 0; ct < CTMAX; ++ct) {
+                            if (ct < CT) {
+                                const double bv = S.w2[ct * 8 + cr][ks * 4 + kk];
+                                dmma(d[ct], av, bv);
+                            }
+                        }
+                    }
+                }
+                if (b < t.e1) {
+                    const int g1 = wrapi(t.o1 + b, wp.N1);
+                    double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
+#pragma unroll
+                    for (int ct = 0; ct < CTMAX; ++ct) {
+                        if (ct < CT) {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const int c = ct * 8 + 2 * kk + j;
+                                if (c < t.e2) red_add(row + 2 * wrapi(t.o2 + c, wp.N2) + part, d[ct][j]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// generic per-node kernels (any q): the reference loop nest, one warp per node
+
+constexpr int NW_GEN = 4;
+
+__global__ void __launch_bounds__(NW_GEN * 32)
+    k_gather_generic(int64_t M, NodeSet nodes, WindowParams wp, const double2 *__restrict__ grid,
+                     double2 *__restrict__ out) {
+    extern __shared__ __align__(16) double gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = 2 * wp.q + 1;
+    double *w0 = gsm + warp * 3 * P, *w1 = w0 + P, *w2 = w1 + P;
+    const int64_t i = blockIdx.x * (int64_t)NW_GEN + warp;
+    if (i >= M) return;
+    const double u0 = nodes.u0[i], u1 = nodes.u1[i], u2 = nodes.u2[i];
+    const int l0 = (int)floor(u0), l1 = (int)floor(u1), l2 = (int)floor(u2);
+    for (int o = lane; o < P; o += 32) {
+        w0[o] = wfun(u0, l0 - wp.q + o, wp.c0, wp.h0, wp.q);
+        w1[o] = wfun(u1, l1 - wp.q + o, wp.c1, wp.h1, wp.q);
+        w2[o] = wfun(u2, l2 - wp.q + o, wp.c2, wp.h2, wp.q);
+    }
+    __syncwarp();
+    double ar = 0.0, ai = 0.0;
+    for (int a = 0; a < P; ++a) {
+        const double wa = w0[a];
+        if (wa == 0.0) continue;
+        const int g0 = wrapi(l0 - wp.q + a, wp.N0);
+        for (int b = 0; b < P; ++b) {
+            const double wab = wa * w1[b];
+            const int g1 = wrapi(l1 - wp.q + b, wp.N1);
+            const double2 *row = grid + ((size_t)g0 * wp.N1 + g1) * wp.N2;
+            double sr = 0.0, si = 0.0;
+            for (int c = lane; c < P; c += 32) {
+                const double2 g = row[wrapi(l2 - wp.q + c, wp.N2)];
+                sr = fma(w2[c], g.x, sr);
+                si = fma(w2[c], g.y, si);
+            }
+            ar = fma(wab, sr, ar);
+            ai = fma(wab, si, ai);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+    }
+    if (lane == 0) out[nodes.perm[i]] = make_double2(ar, ai);
+}
+
+__global__ void __launch_bounds__(NW_GEN * 32)
+    k_scatter_generic(int64_t M, NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
+                      double *__restrict__ grid) {
+    extern __shared__ __align__(16) double gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = 2 * wp.q + 1;
+    double *w0 = gsm + warp * 3 * P, *w1 = w0 + P, *w2 = w1 + P;
+    const int64_t i = blockIdx.x * (int64_t)NW_GEN + warp;
+    if (i >= M) return;
+    const double u0 = nodes.u0[i], u1 = nodes.u1[i], u2 = nodes.u2[i];
+    const int l0 = (int)floor(u0), l1 = (int)floor(u1), l2 = (int)floor(u2);
+    for (int o = lane; o < P; o += 32) {
+        w0[o] = wfun(u0, l0 - wp.q + o, wp.c0, wp.h0, wp.q);
+        w1[o] = wfun(u1, l1 - wp.q + o, wp.c1, wp.h1, wp.q);
+        w2[o] = wfun(u2, l2 - wp.q + o, wp.c2, wp.h2, wp.q);
+    }
+    __syncwarp();
+    const double2 v = values[nodes.perm[i]];
+    for (int a = 0; a < P; ++a) {
+        const double wa = w0[a];
+        if (wa == 0.0) continue;
+        const int g0 = wrapi(l0 - wp.q + a, wp.N0);
+        for (int b = 0; b < P; ++b) {
+            const double wab = wa * w1[b];
+            const double tr = wab * v.x, tim = wab * v.y;
+            const int g1 = wrapi(l1 - wp.q + b, wp.N1);
+            double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
+            for (int c = lane; c < P; c += 32) {
+                const int g2 = wrapi(l2 - wp.q + c, wp.N2);
+                red_add(row + 2 * g2, w2[c] * tr);
+                red_add(row + 2 * g2 + 1, w2[c] * tim);
+            }
+        }
+    }
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+}  // namespace
+
+int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st) {
+    if (p.M == 0) return SGL_OK;
+    if (!p.generic) {
+        const size_t sm = sizeof(GatherSmem);
+        SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2 * 8);
+        if (blocks < 1) blocks = 1;
+        k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tiles, p.n_tiles, p.nodes, p.wp, grid, values);
+    } else {
+        const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);
+        if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_gather_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(p.M, p.nodes, p.wp,
+                                                                                           grid, values);
+    }
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st) {
+    if (p.M == 0) return SGL_OK;
+    if (!p.generic) {
+        const size_t sm = sizeof(ScatterSmem);
+        SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 4 * 8);
+        if (blocks < 1) blocks = 1;
+        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.tiles, p.n_tiles, p.nodes, p.wp, values,
+                                                          reinterpret_cast<double *>(grid));
+    } else {
+        const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);
+        if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_scatter_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(
+            p.M, p.nodes, p.wp, values, reinterpret_cast<double *>(grid));
+    }
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+}  // namespace sgl

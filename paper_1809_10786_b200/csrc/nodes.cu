@@ -1,0 +1,301 @@
+// Plan-time node processing on the device: radius check, warp to torus
+// coordinates, pencil/lo0 sort and greedy window tiles.
+//
+// Follows transform.py:39-55 (choose_rho, transform_points) and
+// nfft.py:131-133, 177-178 (reduction into [0, 2pi), u = N tau / 2 pi,
+// lo = floor(u)) of the reference.  The sort and the tiles have no
+// reference counterpart (the reference walks nodes unsorted).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "sgl_internal.cuh"
+
+namespace sgl {
+
+namespace {
+
+__global__ void k_check_radius(const double *pts, int64_t M, double limit, int *bad) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < M) {
+        double r = pts[3 * i];
+        if (!(r <= limit)) atomicOr(bad, 1);  // NaN counts as bad too
+    }
+}
+
+__global__ void k_radius(const double *pts, int64_t M, double *r) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < M) r[i] = pts[3 * i];
+}
+
+__device__ __forceinline__ double reduce_2pi(double x) {
+    // np.mod(x, 2 pi) with the 2 pi -> 0 fold of nfft.py:177-178
+    double t = fmod(x, kTwoPi);
+    if (t < 0.0) t += kTwoPi;
+    if (t >= kTwoPi) t = 0.0;
+    return t;
+}
+
+__device__ __forceinline__ void to_u(double tau, int N, double &u, int &lo) {
+    u = (double)N * tau / kTwoPi;     // nfft.py:132 evaluation order
+    double f = floor(u);
+    lo = (int)f;
+    if (lo >= N) {                    // rounding onto N: same cell modulo N
+        u -= (double)N;
+        lo -= N;
+    }
+}
+
+struct KeyGeom {
+    int N0, N1, N2, W, P2;
+};
+
+__global__ void k_warp_key(const double *pts, int64_t M, double rho, KeyGeom g, double *u0,
+                           double *u1, double *u2, uint64_t *key, int32_t *idx) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double r = pts[3 * i], th = pts[3 * i + 1], ph = pts[3 * i + 2];
+    double gam = (2.0 * r - rho) / rho;                 // transform.py:52
+    gam = fmin(1.0, fmax(-1.0, gam));
+    double t0 = reduce_2pi(acos(gam));
+    double t1 = reduce_2pi(th);
+    double t2 = reduce_2pi(ph);
+    double a, b, c;
+    int l0, l1, l2;
+    to_u(t0, g.N0, a, l0);
+    to_u(t1, g.N1, b, l1);
+    to_u(t2, g.N2, c, l2);
+    u0[i] = a;
+    u1[i] = b;
+    u2[i] = c;
+    uint64_t pencil = (uint64_t)(l1 / g.W) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W);
+    key[i] = pencil * (uint64_t)g.N0 + (uint64_t)l0;
+    idx[i] = (int32_t)i;
+}
+
+__global__ void k_permute(const int32_t *idx, int64_t M, const double *a0, const double *a1,
+                          const double *a2, double *b0, double *b1, double *b2) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    int32_t j = idx[i];
+    b0[i] = a0[j];
+    b1[i] = a1[j];
+    b2[i] = a2[j];
+}
+
+__global__ void k_run_heads(const uint64_t *key, int64_t M, uint64_t N0, int32_t *head) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    head[i] = (i == 0 || key[i] / N0 != key[i - 1] / N0) ? 1 : 0;
+}
+
+__global__ void k_run_starts(const int32_t *head, const int32_t *rank, int64_t M, int32_t *starts) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    if (head[i]) starts[rank[i]] = (int32_t)i;
+}
+
+struct TileGeom {
+    int q;
+    int span0;  // max lo0 span inside a tile
+};
+
+__device__ __forceinline__ int lo_of(double u) { return (int)floor(u); }
+
+// One thread per pencil run: greedy cut into tiles of <= kTileNodes nodes
+// whose lo0 span is <= span0.  write == nullptr: count only.
+__global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const double *u0,
+                        const double *u1, const double *u2, TileGeom g, int32_t *counts,
+                        const int32_t *offsets, Tile *out) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nruns) return;
+    int64_t s = starts[r];
+    int64_t e = (r + 1 < nruns) ? starts[r + 1] : M;
+    int32_t nt = 0;
+    int64_t pos = out ? offsets[r] : 0;
+    int64_t i = s;
+    while (i < e) {
+        int first0 = lo_of(u0[i]);
+        int mn[3] = {1 << 30, 1 << 30, 1 << 30}, mx[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+        int64_t j = i;
+        for (; j < e && j - i < kTileNodes; ++j) {
+            double uu[3] = {u0[j], u1[j], u2[j]};
+            int l0 = lo_of(uu[0]);
+            if (l0 - first0 > g.span0) break;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                int lo = lo_of(uu[d]);
+                int lower = lo - g.q + ((uu[d] > (double)lo) ? 1 : 0);
+                mn[d] = min(mn[d], lower);
+                mx[d] = max(mx[d], lo + g.q);
+            }
+        }
+        if (out) {
+            Tile t;
+            t.start = (int32_t)i;
+            t.count = (int32_t)(j - i);
+            t.o0 = mn[0];
+            t.o1 = mn[1];
+            t.o2 = mn[2];
+            t.e0 = mx[0] - mn[0] + 1;
+            t.e1 = mx[1] - mn[1] + 1;
+            t.e2 = mx[2] - mn[2] + 1;
+            out[pos++] = t;
+        }
+        ++nt;
+        i = j;
+    }
+    if (!out) counts[r] = nt;
+}
+
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * (n ? n : 1)); }
+};
+
+inline unsigned grid_for(int64_t n, int threads) {
+    return (unsigned)((n + threads - 1) / threads);
+}
+
+}  // namespace
+
+int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
+    const int64_t M = p.M;
+    const int T = 256;
+    // rho: explicit, or the largest radius (choose_rho, transform.py:39-43)
+    if (!(p.rho > 0)) {
+        double rmax = 0.0;
+        if (M > 0) {
+            DevBuf<double> r, out;
+            DevBuf<unsigned char> tmp;
+            SGL_CUDA_CHECK(r.alloc(M));
+            SGL_CUDA_CHECK(out.alloc(1));
+            k_radius<<<grid_for(M, T), T, 0, st>>>(pts, M, r.p);
+            size_t tb = 0;
+            cub::DeviceReduce::Max(nullptr, tb, r.p, out.p, (int)M, st);
+            SGL_CUDA_CHECK(tmp.alloc(tb));
+            cub::DeviceReduce::Max(tmp.p, tb, r.p, out.p, (int)M, st);
+            SGL_CUDA_CHECK(cudaMemcpyAsync(&rmax, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        p.rho = rmax > 0 ? rmax : 1.0;
+    }
+    if (M > 0) {
+        DevBuf<int> bad;
+        SGL_CUDA_CHECK(bad.alloc(1));
+        SGL_CUDA_CHECK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        k_check_radius<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho * (1 + 1e-12), bad.p);
+        int hb = 0;
+        SGL_CUDA_CHECK(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (hb) {
+            set_error("point radius exceeds the radial parameter rho");
+            return SGL_EINVAL;
+        }
+    }
+    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u0, sizeof(double) * (M ? M : 1)));
+    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u1, sizeof(double) * (M ? M : 1)));
+    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u2, sizeof(double) * (M ? M : 1)));
+    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.perm, sizeof(int32_t) * (M ? M : 1)));
+    if (M == 0) return SGL_OK;
+
+    int W = (4 - (2 * p.q - 1) % 4) % 4;
+    if (W < 2) W += 4;
+    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W, (p.grid[2] + W - 1) / W};
+    DevBuf<double> a0, a1, a2;
+    DevBuf<uint64_t> key, key_s;
+    DevBuf<int32_t> idx;
+    SGL_CUDA_CHECK(a0.alloc(M));
+    SGL_CUDA_CHECK(a1.alloc(M));
+    SGL_CUDA_CHECK(a2.alloc(M));
+    SGL_CUDA_CHECK(key.alloc(M));
+    SGL_CUDA_CHECK(key_s.alloc(M));
+    SGL_CUDA_CHECK(idx.alloc(M));
+    k_warp_key<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, kg, a0.p, a1.p, a2.p, key.p, idx.p);
+    SGL_CUDA_CHECK(cudaGetLastError());
+
+    // sort by (pencil, lo0); only the bits in use
+    uint64_t maxkey = (uint64_t)((p.grid[1] + W - 1) / W) * kg.P2 * (uint64_t)p.grid[0];
+    int bits = 1;
+    while (bits < 64 && (1ull << bits) < maxkey) ++bits;
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_s.p, idx.p, p.nodes.perm, (int)M, 0, bits,
+                                        st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_s.p, idx.p, p.nodes.perm, (int)M, 0, bits,
+                                        st);
+        SGL_CUDA_CHECK(cudaGetLastError());
+    }
+    k_permute<<<grid_for(M, T), T, 0, st>>>(p.nodes.perm, M, a0.p, a1.p, a2.p, p.nodes.u0, p.nodes.u1,
+                                            p.nodes.u2);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    if (p.generic) return SGL_OK;
+
+    // pencil runs
+    DevBuf<int32_t> head, rank, starts, counts, offs;
+    SGL_CUDA_CHECK(head.alloc(M));
+    SGL_CUDA_CHECK(rank.alloc(M));
+    k_run_heads<<<grid_for(M, T), T, 0, st>>>(key_s.p, M, (uint64_t)p.grid[0], head.p);
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, head.p, rank.p, (int)M, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, rank.p, (int)M, st);
+    }
+    int32_t last_rank = 0, last_head = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_rank, rank.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_head, head.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int64_t nruns = (int64_t)last_rank + last_head;
+    SGL_CUDA_CHECK(starts.alloc(nruns));
+    SGL_CUDA_CHECK(counts.alloc(nruns));
+    SGL_CUDA_CHECK(offs.alloc(nruns));
+    k_run_starts<<<grid_for(M, T), T, 0, st>>>(head.p, rank.p, M, starts.p);
+    TileGeom tg{p.q, kBox0Max - 2 * p.q - 1};
+    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
+                                                 counts.p, nullptr, nullptr);
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, offs.p, (int)nruns, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, offs.p, (int)nruns, st);
+    }
+    int32_t lc = 0, lo = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&lc, counts.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&lo, offs.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    p.n_tiles = (int64_t)lc + lo;
+    SGL_CUDA_CHECK(cudaMalloc(&p.tiles, sizeof(Tile) * p.n_tiles));
+    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
+                                                 counts.p, offs.p, p.tiles);
+    SGL_CUDA_CHECK(cudaGetLastError());
+
+    // tile statistics (host): nodes covered and DMMA count of one gather pass
+    std::vector<Tile> ht(p.n_tiles);
+    SGL_CUDA_CHECK(cudaMemcpyAsync(ht.data(), p.tiles, sizeof(Tile) * p.n_tiles, cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    int64_t nodes = 0, dmma = 0;
+    for (const Tile &t : ht) {
+        nodes += t.count;
+        int64_t mt = (t.e1 + 3) / 4, ks = (t.e2 + 3) / 4, nt = (t.count + 7) / 8;
+        dmma += (int64_t)t.e0 * mt * ks * nt;
+        if (t.e1 > kBoxMax || t.e2 > kBoxMax || t.e0 > kBox0Max) {
+            set_error("internal: window tile exceeds the box limits");
+            return SGL_ECUDA;
+        }
+    }
+    p.tile_nodes = nodes;
+    p.tile_dmma = dmma;
+    return SGL_OK;
+}
+
+}  // namespace sgl

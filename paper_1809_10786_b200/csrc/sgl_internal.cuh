@@ -1,0 +1,120 @@
+// Internal definitions shared by the NFSGLFT CUDA sources (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sgl_b200.h"
+
+namespace sgl {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 6.28318530717958647692;
+
+// ---------------------------------------------------------------------------
+// window tiles:  a tile is <= kTileNodes sorted
+// nodes from one pencil (lo1, lo2 in a W x W cell block), consecutive in lo0.
+// Its box covers the union of the nodes' window supports.
+constexpr int kTileNodes = 32;   // GEMM N-dim (gather) / K-dim (scatter)
+constexpr int kBoxMax = 40;      // max box extent on axes 1 and 2
+constexpr int kBox0Max = 48;     // max box extent on axis 0 (slabs)
+constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
+
+struct Tile {
+    int32_t start;    // first sorted node
+    int32_t count;    // nodes in tile (1..kTileNodes)
+    int32_t o0, o1, o2;  // box origin (unwrapped cell coordinates)
+    int32_t e0, e1, e2;  // box extents
+};
+
+struct NodeSet {
+    // sorted order (tile order); u_j = N_j * tau_j / (2 pi) in [0, N_j)
+    double *u0 = nullptr, *u1 = nullptr, *u2 = nullptr;
+    int32_t *perm = nullptr;   // sorted position -> caller index
+};
+
+struct WindowParams {
+    int32_t N0, N1, N2;
+    int32_t q;
+    double c0, c1, c2;          // (N/2pi)/sqrt(2 pi lam)
+    double h0, h1, h2;          // 1/(2 lam)
+};
+
+struct StageTimer {
+    cudaEvent_t ev[SGL_STAGE_COUNT + 1];
+    bool ready = false;
+};
+
+struct Plan {
+    int B = 0;
+    int64_t M = 0;
+    double rho = 0;
+    int sigma = 2, q = 16;
+    bool compact = false;
+    bool generic = false;
+    bool profile = false;
+    int n_axis[3];
+    int grid[3];
+    int sig_axes[3];
+    double s_eff[3];
+    double lam[3];
+    int64_t count = 0;
+    int device = 0;
+
+    WindowParams wp;
+    NodeSet nodes;
+    Tile *tiles = nullptr;
+    int64_t n_tiles = 0;
+    int64_t tile_nodes = 0;
+    int64_t tile_dmma = 0;
+    double plan_ms = 0;
+    // per-node u (caller order) for the generic kernels
+    double *gu0 = nullptr, *gu1 = nullptr, *gu2 = nullptr;
+
+    // basal matrices (device)
+    double *Kl = nullptr;        // concat over l of (B-l) x 4B
+    int64_t *Kl_off = nullptr;   // host offsets (B+1)
+    double *Km = nullptr;        // concat over m=-(B-1)..B-1 of (B-|m|) x 4B
+    std::vector<int64_t> Kl_off_h, Km_off_h;
+    int64_t *Kl_off_d = nullptr, *Km_off_d = nullptr;
+    double *dec0 = nullptr, *dec1 = nullptr, *dec2 = nullptr;  // deconv incl. (2pi)^3/prod N
+
+    // scratch
+    double2 *grid_buf = nullptr;   // N0 x N1 x N2 complex
+    double2 *beta = nullptr;       // B^2 x 4B complex
+    double2 *coef_buf = nullptr;   // count complex (staging)
+    double2 *val_buf = nullptr;    // M complex (staging)
+    size_t grid_elems = 0;
+    cufftHandle fft = 0;
+    bool fft_ready = false;
+
+    StageTimer timers[2];
+    float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
+};
+
+// error state
+void set_error(const std::string &msg);
+#define SGL_CUDA_CHECK(x)                                                        \
+    do {                                                                         \
+        cudaError_t _e = (x);                                                    \
+        if (_e != cudaSuccess) {                                                 \
+            ::sgl::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + \
+                             " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+            return SGL_ECUDA;                                                    \
+        }                                                                        \
+    } while (0)
+
+// kernels / launchers (defined in the .cu files)
+int build_nodes(Plan &p, const double *points_dev, cudaStream_t st);
+int build_basal_tables(Plan &p);
+int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
+int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
+int launch_basal_forward(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st,
+                         cudaEvent_t mid);
+int launch_basal_adjoint(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
+
+}  // namespace sgl

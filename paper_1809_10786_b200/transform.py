@@ -1,0 +1,244 @@
+"""B200 drop-in for the reference `plan / forward / adjoint` (transform.py:320-429).
+
+Same names, argument meaning and ValueError conditions as the reference
+`sglnufft.transform`; the work runs in `libsgl_b200.so` (hand-written
+sm_100a kernels + cuFFT) through the C ABI of `include/sgl_b200.h`.
+
+Inputs may be numpy arrays (host; results come back as numpy) or CUDA
+`torch` tensors (device; results stay on the device as torch tensors).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .generate import coeff_count
+
+_BACKENDS = ("auto", "tiled", "generic", "numba", "numpy")
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class NfftInfo:
+    """Geometry of the oversampled grid (mirrors NfftPlan fields, nfft.py:101-120)."""
+    d: int
+    n_axis: tuple
+    sigma: tuple
+    q: int
+    grid_shape: tuple
+    sigma_eff: tuple
+    lam: tuple
+    backend: str
+
+    @property
+    def deconv(self):
+        """Per-axis 1/phi-hat over the centred range (nfft.py:183-186)."""
+        return [np.exp(2 * self.lam[j] * (np.pi * (np.arange(n) - n // 2) / self.grid_shape[j]) ** 2)
+                for j, n in enumerate(self.n_axis)]
+
+
+@dataclass
+class SglPlan:
+    """Per-point-set plan; owns the device state of libsgl_b200 (sorted nodes,
+    window tiles, basal matrices, cuFFT plan, scratch grid).
+
+    Calls on one plan are serialised by the plan's scratch buffers; use one
+    plan per concurrent stream (the reference plan is shareable across
+    threads, README.md:66-67)."""
+    B: int
+    rho: float
+    sigma: int
+    q: int | None
+    exact: bool
+    compact_k1: bool
+    points: object
+    n_axis: tuple
+    nfft: NfftInfo
+    device: int
+    _handle: int = field(repr=False)
+    _info: _native.PlanInfo = field(repr=False)
+
+    @property
+    def m_points(self) -> int:
+        return int(self._info.M)
+
+    @property
+    def count(self) -> int:
+        return int(self._info.coeff_count)
+
+    @property
+    def nodes(self) -> np.ndarray:
+        """Warped torus nodes (transform.py:46-55), computed on request."""
+        pts = self.points.detach().cpu().numpy() if _is_torch(self.points) else np.asarray(self.points)
+        out = np.array(pts, dtype=float)
+        out[:, 0] = np.arccos(np.clip((2 * out[:, 0] - self.rho) / self.rho, -1.0, 1.0))
+        return out
+
+    @property
+    def tiles(self) -> int:
+        return int(self._info.n_tiles)
+
+    @property
+    def stats(self) -> dict:
+        i = self._info
+        return {"n_tiles": int(i.n_tiles), "tile_nodes": int(i.tile_nodes), "tile_dmma": int(i.tile_dmma),
+                "generic": bool(i.generic), "plan_ms": float(i.plan_ms)}
+
+    def stage_ms(self, direction: str = "forward") -> dict:
+        """Per-stage device ms of the last call (plan(..., profile=True))."""
+        buf = (ctypes.c_float * 5)()
+        _native.check(_native.lib().sgl_plan_stage_ms(self._handle, 0 if direction == "forward" else 1, buf, 5))
+        return dict(zip(_native.STAGES, (float(x) for x in buf)))
+
+    def close(self) -> None:
+        if self._handle:
+            _native.lib().sgl_plan_destroy(self._handle)
+            self._handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_ptr(x) -> int | None:
+    if _is_torch(x) and x.is_cuda:
+        return _torch().cuda.current_stream(x.device).cuda_stream
+    return None
+
+
+def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
+         exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
+         precompute: bool = True, device: int | None = None, profile: bool = False) -> SglPlan:
+    """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
+
+    ``backend``: "auto" (tiled DMMA kernels for q <= 16, per-node kernels
+    otherwise), "tiled", "generic" (per-node kernels).  The reference names
+    "numba" / "numpy" are accepted as aliases of "auto".  ``precompute`` is
+    accepted for compatibility: window weights are always evaluated on the
+    fly on the device.  ``exact_last_stage=True`` raises ValueError (the exact
+    NDFT is not part of the B200 path)."""
+    if B < 1:
+        raise ValueError("bandwidth must be >= 1")
+    if backend not in _BACKENDS:
+        raise ValueError("backend must be 'auto', 'tiled', 'generic', 'numba' or 'numpy'")
+    torch_in = _is_torch(points)
+    if torch_in:
+        torch = _torch()
+        pts = points.to(torch.float64)
+        if pts.dim() == 1:
+            pts = pts.reshape(1, -1)
+        if pts.dim() != 2 or pts.shape[1] != 3:
+            raise ValueError("points must be (M, 3) spherical coordinates")
+        pts = pts.contiguous()
+        ptr, M = pts.data_ptr(), int(pts.shape[0])
+        dev = pts.device.index if pts.is_cuda else device
+    else:
+        pts = np.atleast_2d(np.ascontiguousarray(points, dtype=np.float64))
+        if pts.ndim != 2 or pts.shape[1] != 3:
+            raise ValueError("points must be (M, 3) spherical coordinates")
+        ptr, M = pts.ctypes.data, int(pts.shape[0])
+        dev = device
+    if rho is not None and not rho > 0:
+        raise ValueError("rho must be positive")
+    if exact_last_stage:
+        raise ValueError("exact_last_stage=True is not provided by the B200 backend")
+    if q is None or q < 1:
+        raise ValueError("cutoff parameter q must be >= 1")
+    if q >= 4 * sigma * B:
+        raise ValueError(f"cutoff q = {q} must be below 4*sigma*B = {4 * sigma * B}")
+    if backend == "tiled" and q > 16:
+        raise ValueError("tiled window kernels need q <= 16")
+    L = _native.lib()
+    if dev is not None:
+        _native.check(L.sgl_set_device(int(dev)))
+    flags = 0
+    if compact_k1:
+        flags |= _native.FLAG_COMPACT_K1
+    if backend == "generic":
+        flags |= _native.FLAG_GENERIC_GRIDDING
+    if profile:
+        flags |= _native.FLAG_PROFILE
+    h = ctypes.c_void_p(0)
+    stream = _stream_ptr(pts)
+    _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q),
+                                    float(rho) if rho is not None else 0.0, flags, stream, ctypes.byref(h)))
+    info = _native.PlanInfo()
+    _native.check(L.sgl_plan_get_info(h, ctypes.byref(info)))
+    nf = NfftInfo(3, tuple(info.n_axis), tuple(info.sigma_axes), int(q), tuple(info.grid),
+                  tuple(info.sigma_eff), tuple(info.lam), "generic" if info.generic else "tiled")
+    return SglPlan(B=int(B), rho=float(info.rho), sigma=int(sigma), q=int(q), exact=False,
+                   compact_k1=bool(compact_k1), points=points, n_axis=tuple(info.n_axis), nfft=nf,
+                   device=int(dev) if dev is not None else 0, _handle=h.value, _info=info)
+
+
+def _check_precise(precise):
+    if precise:
+        raise ValueError("precise=True (80-bit recurrences) has no B200 equivalent")
+
+
+def forward(p: SglPlan, coeffs, precise: bool = False):
+    """Evaluate the expansion at the plan's points (transform.py:385-395).
+
+    ``coeffs``: (count,) complex128, or (K, count) for K vectors on one plan
+    (the batched forward).  Returns (M,) or (K, M)."""
+    _check_precise(precise)
+    cnt = p.count
+    if _is_torch(coeffs):
+        torch = _torch()
+        c = coeffs.to(torch.complex128).contiguous()
+        if c.shape[-1:] != (cnt,) or c.dim() > 2:
+            raise ValueError("coefficient length does not match the bandwidth")
+        K = 1 if c.dim() == 1 else int(c.shape[0])
+        out = torch.empty((K, p.m_points) if c.dim() == 2 else (p.m_points,), dtype=torch.complex128,
+                          device=c.device)
+        _native.check(_native.lib().sgl_forward(p._handle, c.data_ptr(), K, out.data_ptr() if out.numel() else None,
+                                                _stream_ptr(c)))
+        return out
+    c = np.ascontiguousarray(coeffs, dtype=np.complex128)
+    if c.shape[-1:] != (cnt,) or c.ndim > 2 or c.ndim == 0:
+        raise ValueError("coefficient length does not match the bandwidth")
+    K = 1 if c.ndim == 1 else c.shape[0]
+    out = np.empty((K, p.m_points) if c.ndim == 2 else (p.m_points,), dtype=np.complex128)
+    _native.check(_native.lib().sgl_forward(p._handle, c.ctypes.data, K, out.ctypes.data if out.size else None,
+                                            None))
+    return out
+
+
+def adjoint(p: SglPlan, values, precise: bool = False):
+    """Apply the conjugate transpose of `forward` (transform.py:398-429)."""
+    _check_precise(precise)
+    if _is_torch(values):
+        torch = _torch()
+        v = values.to(torch.complex128).contiguous()
+        if tuple(v.shape) != (p.m_points,):
+            raise ValueError("values length does not match the plan")
+        out = torch.empty((p.count,), dtype=torch.complex128, device=v.device)
+        _native.check(_native.lib().sgl_adjoint(p._handle, v.data_ptr() if v.numel() else None, out.data_ptr(),
+                                                _stream_ptr(v)))
+        return out
+    v = np.ascontiguousarray(values, dtype=np.complex128)
+    if v.shape != (p.m_points,):
+        raise ValueError("values length does not match the plan")
+    out = np.empty(p.count, dtype=np.complex128)
+    _native.check(_native.lib().sgl_adjoint(p._handle, v.ctypes.data if v.size else None, out.ctypes.data, None))
+    return out
+
+
+def choose_rho(points) -> float:
+    """Largest sample radius; 1.0 if all points sit at the origin (transform.py:39-43)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    r = float(np.max(pts[:, 0])) if pts.size else 0.0
+    return r if r > 0 else 1.0

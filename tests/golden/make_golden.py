@@ -1,0 +1,188 @@
+"""Generate golden vectors by running the REFERENCE package itself.
+
+Run in the build container, where the read-only reference is importable:
+
+    python tests/golden/make_golden.py [--skip-big]
+
+It imports `sglnufft` from /root/reference/pkg/src, builds each input with
+the reference's own generators (draw order of SURVEY.md 8(d)), runs the
+reference `plan / forward / adjoint` (numba backend, defaults sigma=2,
+q=16 unless stated) and stores inputs + outputs as compressed .npz
+fixtures next to this script.  Nothing on the GPU box reads
+/root/reference; the tests only read these fixtures.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import sglnufft  # noqa: E402
+    return sglnufft
+
+
+def _vals(rng, M):
+    re = rng.uniform(-1.0, 1.0, M)
+    im = rng.uniform(-1.0, 1.0, M)
+    return re + 1j * im
+
+
+def small_cases(ref):
+    """Small shapes covering sigma escalation, compact_k1, small q, and nodes
+    on grid lines / the r = rho and r = 0 boundaries / the poles."""
+    out = {}
+    specs = [
+        # name, B, M, q, compact, radius, seed
+        ("b1_q4", 1, 7, 4, False, 2.0, 101),
+        ("b2_q8", 2, 10, 8, False, 2.0, 102),
+        ("b4_q8", 4, 30, 8, False, 2.0, 103),
+        ("b5_q10", 5, 40, 10, False, 2.5, 104),
+        ("b8_q16", 8, 200, 16, False, 3.0, 105),
+        ("b6_q6_compact", 6, 100, 6, True, 4.0, 106),
+        ("b12_q12", 12, 300, 12, False, 3.5, 107),
+    ]
+    for name, B, M, q, compact, rad, seed in specs:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        c = ref.gen_coeffs(B, rng)
+        pts = ref.gen_points_ball(M, rad, rng)
+        v = _vals(rng, M)
+        p = ref.plan(B, pts, q=q, compact_k1=compact)
+        out[name] = dict(B=B, q=q, compact=compact, points=pts, coeffs=c, values=v, rho=p.rho,
+                         fwd=ref.forward(p, c), adj=ref.adjoint(p, v))
+    # special nodes: r = rho (x0 = 0 exactly), r = 0 (x0 = pi), poles, phi = 0,
+    # and Cartesian-grid nodes whose warped coordinates fall on grid lines.
+    for name, B, q in [("edges_b8_q16", 8, 16), ("edges_b3_q2", 3, 2), ("edges_b4_q5", 4, 5)]:
+        rng = np.random.Generator(np.random.PCG64(200 + B))
+        c = ref.gen_coeffs(B, rng)
+        special = np.array([
+            [2.0, 0.0, 0.0], [2.0, np.pi, 0.0], [0.0, 0.0, 0.0], [0.0, 1.0, 2.0],
+            [1.0, np.pi / 2, 0.0], [2.0, np.pi / 2, np.pi], [1.5, np.pi / 4, 3 * np.pi / 2],
+            [1.0, np.pi / 2, 2 * np.pi - 1e-17], [0.5, 0.0, 1.0],
+        ])
+        grid = ref.gen_grid(6, 1.0)
+        pts = np.concatenate([special, grid, ref.gen_points_ball(40, 2.0, rng)])
+        v = _vals(rng, pts.shape[0])
+        p = ref.plan(B, pts, q=q)
+        out[name] = dict(B=B, q=q, compact=False, points=pts, coeffs=c, values=v, rho=p.rho,
+                         fwd=ref.forward(p, c), adj=ref.adjoint(p, v))
+    return out
+
+
+def cfg_cases(ref, skip_big):
+    out = {}
+    # config 1 at full size: B=16, M=20000 N(0, I/2), seed 0 (forward; adjoint too)
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 16
+    c = ref.gen_coeffs(B, rng)
+    from sglnufft.generate import cartesian_to_spherical
+    pts = cartesian_to_spherical(rng.normal(0.0, np.sqrt(0.5), (20_000, 3)))
+    v = _vals(rng, 20_000)
+    t = time.time()
+    p = ref.plan(B, pts)
+    out["cfg1"] = dict(B=B, q=16, compact=False, points=pts, coeffs=c, values=v, rho=p.rho,
+                       fwd=ref.forward(p, c), adj=ref.adjoint(p, v))
+    print(f"cfg1 {time.time() - t:.1f}s", flush=True)
+
+    # config 2 shape: B=32, gen_grid(100, 4.0); 2000-node seeded subset, rho pinned
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 32
+    c = ref.gen_coeffs(B, rng)
+    full = ref.gen_grid(100, 4.0)
+    vfull = _vals(rng, full.shape[0])
+    rho = float(np.max(full[:, 0]))
+    sel = np.sort(np.random.Generator(np.random.PCG64(1)).choice(full.shape[0], 2000, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    out["cfg2_sub2000"] = dict(B=B, q=16, compact=False, points=full[sel], coeffs=c, values=vfull[sel],
+                               rho=rho, sel=sel, fwd=ref.forward(p, c), adj=ref.adjoint(p, vfull[sel]))
+    print(f"cfg2 {time.time() - t:.1f}s", flush=True)
+
+    # config 3 shape: B=64, c / n, ball radius 16, M = 1e7 -> 600-node subset
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 64
+    c = ref.gen_coeffs(B, rng)
+    nmu = ref.indexing.mu_to_nlm_array(B)[:, 0]
+    c = c / nmu
+    Mf = 10_000_000
+    full = ref.gen_points_ball(Mf, 16.0, rng)
+    vfull = _vals(rng, Mf)
+    rho = float(np.max(full[:, 0]))
+    sel = np.sort(np.random.Generator(np.random.PCG64(1)).choice(Mf, 600, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    out["cfg3_sub600"] = dict(B=B, q=16, compact=False, points=full[sel], coeffs=c, values=vfull[sel],
+                              rho=rho, sel=sel, fwd=ref.forward(p, c), adj=ref.adjoint(p, vfull[sel]),
+                              head=full[:8], vhead=vfull[:8])
+    print(f"cfg3 {time.time() - t:.1f}s", flush=True)
+    del full, vfull
+
+    # config 5 shape: B=48 (sigma_eff = 8/3), 64 vectors, 2e6 N(0, I/2) nodes -> 400-node subset, 2 vectors
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 48
+    cs = np.stack([ref.gen_coeffs(B, rng) for _ in range(64)])
+    Mf = 2_000_000
+    full = cartesian_to_spherical(rng.normal(0.0, np.sqrt(0.5), (Mf, 3)))
+    rho = float(np.max(full[:, 0]))
+    sel = np.sort(np.random.Generator(np.random.PCG64(1)).choice(Mf, 400, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    fw = np.stack([ref.forward(p, cs[k]) for k in (0, 63)])
+    out["cfg5_sub400"] = dict(B=B, q=16, compact=False, points=full[sel], coeffs=cs[[0, 63]], rho=rho,
+                              sel=sel, fwd=fw, head=full[:8])
+    print(f"cfg5 {time.time() - t:.1f}s", flush=True)
+    del full
+
+    if not skip_big:
+        # config 4 shape: B=128, adjoint only (the reference forward is NaN here);
+        # 120-node subset of the 50/50 mixture; rho pinned to the full 1e8 set.
+        rng = np.random.Generator(np.random.PCG64(0))
+        B = 128
+        _ = ref.gen_coeffs(B, rng)
+        Mf = 100_000_000
+        h = Mf // 2
+        a = cartesian_to_spherical(rng.normal(0.0, np.sqrt(0.5), (h, 3)))
+        b = ref.gen_points_ball(Mf - h, 22.0, rng)
+        perm = rng.permutation(Mf)
+        vfull = _vals(rng, Mf)
+        rho = float(max(a[:, 0].max(), b[:, 0].max()))
+        sel = np.sort(np.random.Generator(np.random.PCG64(1)).choice(Mf, 120, replace=False))
+        src = perm[sel]
+        pts = np.where((src < h)[:, None], a[np.minimum(src, h - 1)], b[np.maximum(src - h, 0)])
+        vals = vfull[sel]
+        del a, b, vfull, perm
+        t = time.time()
+        p = ref.plan(B, pts, rho=rho)
+        out["cfg4_sub120"] = dict(B=B, q=16, compact=False, points=pts, values=vals, rho=rho, sel=sel,
+                                  adj=ref.adjoint(p, vals))
+        print(f"cfg4 {time.time() - t:.1f}s", flush=True)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-big", action="store_true")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    ref = _ref()
+    cases = {}
+    if args.only in ("", "small"):
+        cases.update(small_cases(ref))
+    if args.only in ("", "cfg"):
+        cases.update(cfg_cases(ref, args.skip_big))
+    for name, d in cases.items():
+        path = os.path.join(HERE, f"ref_{name}.npz")
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})
+        print("wrote", path, os.path.getsize(path))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Goldens are outputs of the reference package itself (tests/golden/).  The bar
+is rel-linf = max|x - ref| / max|ref| <= 1e-10 (BASELINE north star; the
+reference's own idiom, test_transform.py:223, 303); the measured CPU rounding
+floor is 1e-15 .. 3e-14.
+"""
+import numpy as np
+import pytest
+
+from conftest import SMALL, load_golden
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x), np.asarray(ref)
+    return float(np.max(np.abs(x - ref)) / np.max(np.abs(ref)))
+
+
+@pytest.fixture(scope="module")
+def sgl():
+    import paper_1809_10786_b200 as m
+    from paper_1809_10786_b200 import _native
+    assert _native.device_count() >= 1, "no CUDA device: the -m gpu suite needs a B200"
+    return m
+
+
+def _plan(sgl, g, **kw):
+    return sgl.plan(int(g["B"]), g["points"], q=int(g["q"]), rho=float(g["rho"]),
+                    compact_k1=bool(g["compact"]), **kw)
+
+
+@pytest.mark.parametrize("backend", ["auto", "generic"])
+@pytest.mark.parametrize("name", SMALL + ["cfg1", "cfg2_sub2000", "cfg3_sub600", "cfg5_sub400"])
+def test_forward_adjoint_match_reference(sgl, name, backend):
+    g = load_golden(name)
+    if backend == "generic" and name.startswith("cfg") and name != "cfg1":
+        pytest.skip("generic kernels cross-checked on the small and cfg1 shapes")
+    p = _plan(sgl, g, backend=backend)
+    assert p.rho == float(g["rho"])
+    f = sgl.forward(p, g["coeffs"])
+    assert f.shape == g["fwd"].shape
+    assert rel(f, g["fwd"]) <= TOL, rel(f, g["fwd"])
+    if "adj" in g:
+        a = sgl.adjoint(p, g["values"])
+        assert rel(a, g["adj"]) <= TOL, rel(a, g["adj"])
+
+
+# Config 4 (B = 128, rho = 22) is ill-conditioned in FP64: the adjoint entries
+# span 1 .. 1e95 and rounding is amplified by the radial functions.  Measured
+# spread between FP64 implementations of the SAME sums on this input:
+# reference fast path vs direct summation 2.6e-9, oracle restatement vs
+# reference 5.1e-9, oracle vs direct 4.7e-9.  The bar for this config is
+# therefore the demonstrated FP64 floor x 4.
+TOL_CFG4 = 2e-8
+
+
+def test_config4_adjoint_matches_reference(sgl):
+    # B = 128, rho pinned to the full 1e8-node set; the reference forward is NaN here
+    g = load_golden("cfg4_sub120")
+    p = sgl.plan(128, g["points"], rho=float(g["rho"]))
+    a = sgl.adjoint(p, g["values"])
+    assert np.all(np.isfinite(a))
+    assert rel(a, g["adj"]) <= TOL_CFG4, rel(a, g["adj"])
+    # our forward stays finite where the reference overflows (transform.py:226)
+    f = sgl.forward(p, np.ones(p.count, dtype=complex))
+    assert np.all(np.isfinite(f))
+
+
+@pytest.mark.parametrize("name", ["b8_q16", "b5_q10", "edges_b4_q5", "cfg1"])
+def test_tiled_and_generic_kernels_agree(sgl, name):
+    # the reference's TestBackends pattern (test_nfft.py:213-225)
+    g = load_golden(name)
+    pa, pb = _plan(sgl, g, backend="tiled"), _plan(sgl, g, backend="generic")
+    assert pa.stats["n_tiles"] > 0 and pb.stats["generic"]
+    assert rel(sgl.forward(pa, g["coeffs"]), sgl.forward(pb, g["coeffs"])) <= 1e-12
+    assert rel(sgl.adjoint(pa, g["values"]), sgl.adjoint(pb, g["values"])) <= 1e-12
+
+
+@pytest.mark.parametrize("B,M,q,rad", [(5, 40, 10, 2.5), (8, 500, 16, 3.0), (16, 3000, 16, 4.0), (6, 200, 20, 2.0)])
+def test_pairing(sgl, B, M, q, rad):
+    # <y, F x> == <F^H y, x> (test_transform.py:305-315)
+    rng = np.random.default_rng(32 + B)
+    pts = sgl.gen_points_ball(M, rad, rng)
+    p = sgl.plan(B, pts, q=q)
+    x = sgl.gen_coeffs(B, rng)
+    y = rng.normal(size=M) + 1j * rng.normal(size=M)
+    lhs = np.vdot(y, sgl.forward(p, x))
+    rhs = np.vdot(sgl.adjoint(p, y), x)
+    assert abs(lhs - rhs) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(y)
+
+
+def test_linearity_zero_and_errors(sgl):
+    rng = np.random.default_rng(22)
+    B = 4
+    pts = sgl.gen_points_ball(30, 2.0, rng)
+    p = sgl.plan(B, pts, q=8)
+    x, y = sgl.gen_coeffs(B, rng), sgl.gen_coeffs(B, rng)
+    a, b = 1.3 - 0.2j, -0.7 + 1.1j
+    lhs = sgl.forward(p, a * x + b * y)
+    rhs = a * sgl.forward(p, x) + b * sgl.forward(p, y)
+    assert rel(lhs, rhs) <= 1e-10
+    assert np.all(sgl.adjoint(p, np.zeros(30)) == 0)
+    assert np.all(sgl.forward(p, np.zeros(p.count)) == 0)
+    with pytest.raises(ValueError):
+        sgl.forward(p, np.zeros(p.count + 1))
+    with pytest.raises(ValueError):
+        sgl.adjoint(p, np.zeros(31))
+    with pytest.raises(ValueError):
+        sgl.forward(p, x, precise=True)
+    with pytest.raises(ValueError):
+        sgl.plan(2, np.array([[2.1, 0, 0]]), q=4, rho=1.0)
+
+
+def test_compact_grid_agrees(sgl):
+    g = load_golden("b8_q16")
+    full = _plan(sgl, g)
+    comp = sgl.plan(8, g["points"], compact_k1=True)
+    assert comp.nfft.grid_shape[1] == full.nfft.grid_shape[1] // 2
+    assert rel(sgl.forward(comp, g["coeffs"]), sgl.forward(full, g["coeffs"])) <= 1e-10
+    assert rel(sgl.adjoint(comp, g["values"]), sgl.adjoint(full, g["values"])) <= 1e-10
+
+
+def test_batched_forward_matches_single(sgl):
+    g = load_golden("cfg5_sub400")
+    p = _plan(sgl, g)
+    fb = sgl.forward(p, g["coeffs"])
+    assert fb.shape == (2, 400)
+    for k in range(2):
+        assert rel(fb[k], g["fwd"][k]) <= TOL
+        assert np.array_equal(fb[k], sgl.forward(p, g["coeffs"][k]))
+
+
+def test_torch_device_tensors(sgl):
+    import torch
+    g = load_golden("b12_q12")
+    dev = torch.device("cuda", 0)
+    pts = torch.as_tensor(g["points"], device=dev)
+    p = sgl.plan(12, pts, q=12, rho=float(g["rho"]))
+    f = sgl.forward(p, torch.as_tensor(g["coeffs"], device=dev))
+    assert f.is_cuda and f.dtype == torch.complex128
+    assert rel(f.cpu().numpy(), g["fwd"]) <= TOL
+    a = sgl.adjoint(p, torch.as_tensor(g["values"], device=dev))
+    assert rel(a.cpu().numpy(), g["adj"]) <= TOL
+
+
+def test_empty_and_single_node(sgl):
+    p = sgl.plan(3, np.zeros((0, 3)), q=4)
+    assert sgl.forward(p, np.ones(14)).shape == (0,)
+    assert np.all(sgl.adjoint(p, np.zeros(0)) == 0)
+    g = load_golden("edges_b3_q2")
+    from oracle import sgl_oracle as o
+    pts = g["points"][:1]
+    p1 = sgl.plan(3, pts, q=2, rho=float(g["rho"]))
+    op = o.oracle_plan(3, pts, q=2, rho=float(g["rho"]))
+    assert rel(sgl.forward(p1, g["coeffs"]), o.oracle_forward(op, g["coeffs"])) <= TOL
+
+
+def test_config3_full_size(sgl):
+    """BASELINE config 3 at full M = 1e7: the forward is pointwise, so the
+    golden subset must match entry for entry; the adjoint is linear, so the
+    GPU adjoint over all nodes with values zeroed outside the subset must
+    match the reference adjoint of the subset."""
+    from paper_1809_10786_b200 import workloads
+    g = load_golden("cfg3_sub600")
+    w = workloads.config(3)
+    p = sgl.plan(64, w.points)
+    assert p.rho == float(g["rho"])
+    f = sgl.forward(p, w.coeffs)
+    assert rel(f[g["sel"]], g["fwd"]) <= TOL
+    v = np.zeros(w.M, dtype=complex)
+    v[g["sel"]] = g["values"]
+    a = sgl.adjoint(p, v)
+    assert rel(a, g["adj"]) <= TOL
+    # full-size property: pairing over all 1e7 nodes, relative to the
+    # Cauchy-Schwarz scale |F x| |y| (entries of F x reach 1e53 here)
+    lhs = np.vdot(w.values, f)
+    rhs = np.vdot(sgl.adjoint(p, w.values), w.coeffs)
+    assert abs(lhs - rhs) <= 1e-11 * np.linalg.norm(f) * np.linalg.norm(w.values)
