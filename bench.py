@@ -105,34 +105,40 @@ class ClockSampler:
 
 
 def cpu_reference(work, rho, sample, rank_threads=0):
-    """The reference algorithm on the host (oracle port): fwd+adj on two
-    rho-pinned node samples, extrapolated T(M) = T_fixed + M t_node."""
+    """The reference algorithm on the host (oracle port of the reference path):
+    the per-call fixed stages (basal + FFT, both directions) are timed in
+    full; the window loops are timed on a rho-pinned S-node sample and scaled
+    to M (they are linear in the node count): T(M) = T_fixed + M * t_node."""
     from oracle import sgl_oracle as o
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
     threads = o.oracle_threads() if rank_threads == 0 else rank_threads
     workers = os.cpu_count() or 1
-    times = {}
-    for s in (max(1, sample // 20), sample):
-        idx = np.linspace(0, work.M - 1, s).astype(np.int64)
-        pts = work.points[idx]
-        vals = work.values[idx]
-        t0 = time.perf_counter()
-        p = o.oracle_plan(work.B, pts, rho=rho)
-        t1 = time.perf_counter()
-        o.oracle_forward(p, work.coeffs, threads=threads, workers=workers)
-        o.oracle_adjoint(p, vals, threads=threads, workers=workers)
-        t2 = time.perf_counter()
-        times[s] = (t2 - t1, t1 - t0)
-    (s0, (a0, _)), (s1, (a1, plan_s)) = sorted(times.items())
-    t_node = max((a1 - a0) / (s1 - s0), 1e-12)
-    t_fixed = max(a0 - s0 * t_node, 0.0)
+    idx = np.linspace(0, work.M - 1, min(sample, work.M)).astype(np.int64)
+    p = o.oracle_plan(work.B, work.points[idx], rho=rho)
+    c = work.coeffs if work.coeffs.ndim == 1 else work.coeffs[0]
+    # warm-up (thread pools, first-touch pages), excluded as the reference
+    # excludes its JIT warm-up (experiments.py:240-243)
+    warm = o.oracle_plan(work.B, work.points[idx[:64]], rho=rho)
+    o.oracle_adjoint(warm, work.values[idx[:64]], threads=threads, workers=workers)
+    o.oracle_forward(warm, c, threads=threads, workers=workers)
+    t0 = time.perf_counter()
+    grid = o.spectral_forward(p, o.basal_forward(p, c), workers)
+    t1 = time.perf_counter()
+    o.gather(grid, p.base, p.win, p.q, threads)
+    t2 = time.perf_counter()
+    g2 = o.scatter(p.grid, p.base, p.win, work.values[idx], p.q, threads)
+    t3 = time.perf_counter()
+    o.basal_adjoint(p, o.spectral_adjoint(p, g2, workers))
+    t4 = time.perf_counter()
+    t_fixed = (t1 - t0) + (t4 - t3)
+    t_node = ((t2 - t1) + (t3 - t2)) / len(idx)
     T = t_fixed + work.M * t_node
-    return {"value": work.M / T, "unit": "nodes/s", "cores": int(threads),
-            "kind": "port",
-            "sample": (f"oracle fwd+adj at {s0} and {s1} rho-pinned nodes of the config; "
-                       f"T(M) = {t_fixed:.2f} s + M * {t_node * 1e6:.1f} us extrapolated to M={work.M}; "
-                       f"gridding on {threads} OpenMP threads, scipy.fft on {workers} workers"),
-            "t_fixed_s": t_fixed, "t_node_us": t_node * 1e6, "plan_s_at_sample": plan_s}
+    return {"value": work.M / T, "unit": "nodes/s", "cores": int(threads), "kind": "port",
+            "sample": (f"oracle port of the reference path; basal+FFT (fwd {t1 - t0:.2f} s, adj {t4 - t3:.2f} s) "
+                       f"timed in full, gather+scatter timed on {len(idx)} rho-pinned nodes "
+                       f"({t_node * 1e6:.1f} us/node) and scaled to M={work.M}; window loops on {threads} "
+                       f"OpenMP threads, scipy.fft on {workers} workers"),
+            "t_fixed_s": t_fixed, "t_node_us": t_node * 1e6}
 
 
 def run_reference(args, rank, world):

@@ -7,7 +7,7 @@
 //     w_j(delta) = (N_j/2pi)/sqrt(2 pi lam_j) * exp(-delta^2/(2 lam_j)),
 //     delta = u_j - cell, zero where |delta| > q.
 //
-// Tiled kernels (q <= 16): a tile is <= 32 sorted nodes whose window boxes
+// Tiled kernels (q <= 16): a tile is <= 64 sorted nodes whose window boxes
 // overlap almost entirely.  Per axis-0 slab of the tile's box the contraction
 // over axis 2 is a real GEMM on the FP64 tensor cores (DMMA m8n8k4):
 //     gather : T[(b,re|im), node] = sum_c G[a,b,c] * W2[c,node]
@@ -55,16 +55,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+// Wait for the phase of `parity` to complete.  A watchdog turns a lost
+// phase (a pipeline bug) into a trapped kernel instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try(bar, parity)) {
+        if (++spins == (1u << 24)) __trap();
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -81,28 +92,40 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
 
 // ---------------------------------------------------------------------------
 // tiled gather
+//
+// CTA = 8 consumer warps (one per 8-node M-tile of the 64-node tile) + 1
+// producer warp.  Per box slab a (axis 0), consumer warp w computes
+//     D[node, (b, re|im)] = sum_c W2[c, node] * G[a, b, c]       (DMMA)
+// with the W2 fragments resident in registers and the G fragments read from
+// the shared-memory slab, then applies W1[b, node] and W0[a, node].  The
+// producer streams slabs with cp.async.bulk into a 3-deep ring guarded by
+// full / empty mbarriers, so warps never meet at a CTA barrier inside a tile.
 
-constexpr int GW = 4;                 // warps per CTA: one per 8-node column tile
-constexpr int GT = GW * 32;
+constexpr int GCW = kTileNodes / 8;   // consumer warps
+constexpr int GT = (GCW + 1) * 32;    // + producer warp
 constexpr int NST = 3;                // slab ring depth
 constexpr int SROWS = kBoxMax;        // slab rows (axis 1)
 constexpr int SSTR = kBoxMax + 4;     // max slab row stride in complex (== 4 mod 8)
 constexpr int KSMAX = kBoxMax / 4;    // k-steps over axis 2
-constexpr int W1S = 40;               // gather w1 row stride (doubles)
+constexpr int NTMAX = kBoxMax / 4;    // 4-row (8 re|im column) tiles over axis 1
 
 struct GatherSmem {
     double2 slab[NST][SROWS * SSTR];
     double w0[kBox0Max][kTileNodes];
-    double w1[SROWS][W1S];
     double nu[3][kTileNodes];
-    uint64_t bar[NST];
+    uint64_t full[NST];
+    uint64_t empty[NST];
     Tile t;
 };
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 
 __device__ __forceinline__ void issue_slab(GatherSmem &S, int lane, const Tile &t, int a, int buf, int stride,
                                            const WindowParams &wp, const double2 *grid) {
     const int g0 = wrapi(t.o0 + a, wp.N0);
-    if (lane == 0) mbar_expect_tx(&S.bar[buf], (uint32_t)(t.e1 * t.e2 * 16));
+    if (lane == 0) mbar_expect_tx(&S.full[buf], (uint32_t)(t.e1 * t.e2 * 16));
     __syncwarp();
     const int g2s = wrapi(t.o2, wp.N2);
     for (int y = lane; y < t.e1; y += 32) {
@@ -111,8 +134,8 @@ __device__ __forceinline__ void issue_slab(GatherSmem &S, int lane, const Tile &
         double2 *dst = &S.slab[buf][y * stride];
         int done = 0, g2 = g2s;
         while (done < t.e2) {
-            int n = min(t.e2 - done, wp.N2 - g2);
-            bulk_g2s(dst + done, row + g2, (uint32_t)(n * 16), &S.bar[buf]);
+            const int n = min(t.e2 - done, wp.N2 - g2);
+            bulk_g2s(dst + done, row + g2, (uint32_t)(n * 16), &S.full[buf]);
             done += n;
             g2 = 0;
         }
@@ -125,19 +148,23 @@ __global__ void __launch_bounds__(GT, 2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GatherSmem &S = *reinterpret_cast<GatherSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool producer = warp == GCW;
 
     for (int i = tid; i < NST * SROWS * SSTR; i += GT) (&S.slab[0][0])[i] = make_double2(0.0, 0.0);
     if (tid == 0) {
-        for (int s = 0; s < NST; ++s) mbar_init(&S.bar[s], 1);
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], GCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
 
-    uint32_t seq = 0;
-    const int rb = lane >> 3, part = (lane >> 2) & 1, cc = lane & 3;
-    const int kn = warp * 8 + (lane >> 2);     // node of this lane's B fragment
-    const int kcol = warp * 8 + 2 * cc;        // nodes of this lane's accumulators
+    uint32_t seq = 0;                           // slabs streamed by this CTA so far
+    const int node = warp * 8 + (lane >> 2);    // this lane's node (consumers)
+    const int cc = lane & 3;
+    const int rb = lane >> 3, part = (lane >> 2) & 1;
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         if (tid == 0) S.t = tiles[ti];
@@ -146,98 +173,111 @@ __global__ void __launch_bounds__(GT, 2)
         if (tid < kTileNodes) {
             const bool ok = tid < t.count;
             const int64_t s = (int64_t)t.start + tid;
-            // far-away sentinel: all weights of a missing node are exactly zero
+            // far-away sentinel: every weight of a missing node is exactly zero
             S.nu[0][tid] = ok ? nodes.u0[s] : -1e9;
             S.nu[1][tid] = ok ? nodes.u1[s] : -1e9;
             S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
+        }
+        __syncthreads();
+        for (int i = tid; i < t.e0 * kTileNodes; i += GT) {
+            const int x = i / kTileNodes, k = i % kTileNodes;
+            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
         }
         __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
         const int Cw = KS * 4;
         const int stride = (Cw & 7) ? Cw : Cw + 4;
-        for (int i = tid; i < t.e0 * kTileNodes; i += GT) {
-            const int x = i / kTileNodes, k = i % kTileNodes;
-            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
-        }
-        for (int i = tid; i < Mt * 4 * kTileNodes; i += GT) {
-            const int y = i / kTileNodes, k = i % kTileNodes;
-            S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
-        }
-        double bfr[KSMAX];
-#pragma unroll
-        for (int ks = 0; ks < KSMAX; ++ks)
-            bfr[ks] = (ks < KS) ? wfun(S.nu[2][kn], t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
-        __syncthreads();
 
-        if (warp == 0) {
-            for (int s = 0; s < NST - 1 && s < t.e0; ++s)
-                issue_slab(S, lane, t, s, (int)((seq + s) % NST), stride, wp, grid);
-        }
-        double acc0 = 0.0, acc1 = 0.0;
-        const bool col_live = warp * 8 < t.count;
-        for (int a = 0; a < t.e0; ++a) {
-            if (warp == 0 && a + NST - 1 < t.e0)
-                issue_slab(S, lane, t, a + NST - 1, (int)((seq + a + NST - 1) % NST), stride, wp, grid);
-            const uint32_t q = seq + a;
-            const int buf = (int)(q % NST);
-            mbar_wait(&S.bar[buf], (q / NST) & 1);
-            const double w0a = S.w0[a][kcol], w0b = S.w0[a][kcol + 1];
-            // skip slabs where none of this warp's 8 nodes has weight (uniform)
-            const bool live = col_live && __any_sync(0xffffffffu, (w0a != 0.0) || (w0b != 0.0));
-            if (live) {
-                const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
-                for (int mt = 0; mt < Mt; mt += 3) {
-                    double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        if (producer) {
+            for (int a = 0; a < t.e0; ++a) {
+                const uint32_t q = seq + a;
+                const int buf = (int)(q % NST);
+                const uint32_t use = q / NST;
+                if (use > 0) {
+                    if (lane == 0) mbar_wait(&S.empty[buf], (use - 1) & 1);
+                    __syncwarp();
+                }
+                issue_slab(S, lane, t, a, buf, stride, wp, grid);
+            }
+        } else {
+            double afr[KSMAX], w1r[NTMAX];
+            const double u1 = S.nu[1][node], u2 = S.nu[2][node];
 #pragma unroll
-                    for (int ks = 0; ks < KSMAX; ++ks) {
-                        if (ks < KS) {
+            for (int ks = 0; ks < KSMAX; ++ks)
+                afr[ks] = (ks < KS) ? wfun(u2, t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NTMAX; ++nt)
+                w1r[nt] = (nt < Mt) ? wfun(u1, t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
+            const bool col_live = warp * 8 < t.count;
+            double acc_re = 0.0, acc_im = 0.0;
+            for (int a = 0; a < t.e0; ++a) {
+                const uint32_t q = seq + a;
+                const int buf = (int)(q % NST);
+                const double w0 = S.w0[a][node];
+                // every consumer observes every phase (keeps the ring's parity
+                // bookkeeping exact); the math is skipped where none of this
+                // warp's 8 nodes has weight on the slab (warp-uniform)
+                mbar_wait(&S.full[buf], (q / NST) & 1);
+                if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
+                    const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
+                    double s_re = 0.0, s_im = 0.0;
+#pragma unroll
+                    for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
+                        if (nt0 < Mt) {
+                            double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                            for (int ks = 0; ks < KSMAX; ++ks) {
+                                if (ks < KS) {
+#pragma unroll
+                                    for (int i = 0; i < 3; ++i) {
+                                        if (nt0 + i < NTMAX && nt0 + i < Mt) {
+                                            const int b = (nt0 + i) * 4 + rb;
+                                            const double bv = sl[(b * stride + ks * 4 + cc) * 2 + part];
+                                            dmma(d[i], afr[ks], bv);
+                                        }
+                                    }
+                                }
+                            }
 #pragma unroll
                             for (int i = 0; i < 3; ++i) {
-                                if (mt + i < Mt) {
-                                    const int b = (mt + i) * 4 + rb;
-                                    const double av = sl[(b * stride + ks * 4 + cc) * 2 + part];
-                                    dmma(d[i], av, bfr[ks]);
+                                if (nt0 + i < NTMAX && nt0 + i < Mt) {
+                                    s_re = fma(w1r[nt0 + i], d[i][0], s_re);
+                                    s_im = fma(w1r[nt0 + i], d[i][1], s_im);
                                 }
                             }
                         }
                     }
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        if (mt + i < Mt) {
-                            const int b = (mt + i) * 4 + rb;
-                            const double2 w1 = *reinterpret_cast<const double2 *>(&S.w1[b][kcol]);
-                            acc0 = fma(w0a * w1.x, d[i][0], acc0);
-                            acc1 = fma(w0b * w1.y, d[i][1], acc1);
-                        }
-                    }
+                    acc_re = fma(w0, s_re, acc_re);
+                    acc_im = fma(w0, s_im, acc_im);
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.empty[buf]);
             }
-            __syncthreads();
+            // reduce over the 4 lanes of a node (their rows b differ)
+            acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
+            acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
+            acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
+            acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
+            if (cc == 0 && node < t.count) out[nodes.perm[t.start + node]] = make_double2(acc_re, acc_im);
         }
         seq += (uint32_t)t.e0;
-
-        // reduce over the 4 row groups (lane bits 3,4); lanes 0-3 re, 4-7 im
-        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 8);
-        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 8);
-        acc0 += __shfl_xor_sync(0xffffffffu, acc0, 16);
-        acc1 += __shfl_xor_sync(0xffffffffu, acc1, 16);
-        const double im0 = __shfl_sync(0xffffffffu, acc0, (lane + 4) & 31);
-        const double im1 = __shfl_sync(0xffffffffu, acc1, (lane + 4) & 31);
-        if (lane < 4) {
-            const int k0 = kcol;
-            if (k0 < t.count) out[nodes.perm[t.start + k0]] = make_double2(acc0, im0);
-            if (k0 + 1 < t.count) out[nodes.perm[t.start + k0 + 1]] = make_double2(acc1, im1);
-        }
     }
 }
 
 // ---------------------------------------------------------------------------
 // tiled scatter
+//
+// Work units are (slab a, 4-row M-tile) pairs of the tile's box, dealt
+// round-robin to the CTA's warps.  Per unit
+//     D[(b, re|im), c] = sum_node V[(b, re|im), node] * W2[c, node]   (DMMA)
+// with V = W0[a,node] W1[b,node] v_node formed on the fly, then reduced into
+// the grid with RED.ADD.F64.  Node k-steps with no weight on the slab are
+// skipped (nodes are sorted by lo0 inside a tile).
 
-constexpr int SW = 4;                 // warps per CTA; warps own axis-0 slabs
+constexpr int SW = 8;                 // warps per CTA
 constexpr int STH = SW * 32;
-constexpr int WS = 36;                // w1/w2 row stride (doubles), conflict-free
+constexpr int WS = kTileNodes + 4;    // w1/w2 row stride (doubles): conflict-free
 constexpr int CTMAX = kBoxMax / 8;    // 8-column tiles over axis 2
 constexpr int NKS = kTileNodes / 4;   // node k-steps
 
@@ -250,7 +290,7 @@ struct ScatterSmem {
     Tile t;
 };
 
-__global__ void __launch_bounds__(STH, 4)
+__global__ void __launch_bounds__(STH, 2)
     k_scatter_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
                     const double2 *__restrict__ values, double *__restrict__ grid) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -288,49 +328,46 @@ __global__ void __launch_bounds__(STH, 4)
         }
         __syncthreads();
         const int nks = (t.count + 3) >> 2;
-        for (int a = warp; a < t.e0; a += SW) {
-            // active node k-steps on this slab (nodes are sorted by lo0)
-            const unsigned mask = __ballot_sync(0xffffffffu, S.w0[a][lane] != 0.0);
-            if (mask == 0u) continue;
-            const int ks0 = (__ffs(mask) - 1) >> 2;
-            const int ks1 = min(nks, ((31 - __clz(mask)) >> 2) + 1);
-            double wv[NKS];
+        const int units = t.e0 * Mt;
+        for (int u = warp; u < units; u += SW) {
+            const int a = u / Mt, mt = u - a * Mt;
+            // active node k-steps on this slab (nodes sorted by lo0)
+            const unsigned lo = __ballot_sync(0xffffffffu, S.w0[a][lane] != 0.0);
+            const unsigned hi = __ballot_sync(0xffffffffu, S.w0[a][32 + lane] != 0.0);
+            const unsigned long long mask = ((unsigned long long)hi << 32) | lo;
+            if (mask == 0ull) continue;
+            const int ks0 = (__ffsll((long long)mask) - 1) >> 2;
+            const int ks1 = min(nks, ((63 - __clzll((long long)mask)) >> 2) + 1);
+            const int b = mt * 4 + rb;
+            double d[CTMAX][2];
+#pragma unroll
+            for (int ct = 0; ct < CTMAX; ++ct) d[ct][0] = d[ct][1] = 0.0;
 #pragma unroll
             for (int ks = 0; ks < NKS; ++ks) {
-                const int n = ks * 4 + kk;
-                const double2 v = S.v[n];
-                wv[ks] = S.w0[a][n] * (part ? v.y : v.x);
-            }
-            const int g0 = wrapi(t.o0 + a, wp.N0);
-            for (int mt = 0; mt < Mt; ++mt) {
-                const int b = mt * 4 + rb;
-                double d[CTMAX][2];
-#pragma unroll
-                for (int ct = 0; ct < CTMAX; ++ct) d[ct][0] = d[ct][1] = 0.0;
-#pragma unroll
-                for (int ks = 0; ks < NKS; ++ks) {
-                    if (ks >= ks0 && ks < ks1) {
-                        const double av = wv[ks] * S.w1[b][ks * 4 + kk];
-#pragma unroll
-                        for (int ct = 0; ct < CTMAX; ++ct) {
-                            if (ct < CT) {
-                                const double bv = S.w2[ct * 8 + cr][ks * 4 + kk];
-                                dmma(d[ct], av, bv);
-                            }
-                        }
-                    }
-                }
-                if (b < t.e1) {
-                    const int g1 = wrapi(t.o1 + b, wp.N1);
-                    double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
+                if (ks >= ks0 && ks < ks1) {
+                    const int n = ks * 4 + kk;
+                    const double2 v = S.v[n];
+                    const double av = S.w0[a][n] * S.w1[b][n] * (part ? v.y : v.x);
 #pragma unroll
                     for (int ct = 0; ct < CTMAX; ++ct) {
                         if (ct < CT) {
+                            const double bv = S.w2[ct * 8 + cr][n];
+                            dmma(d[ct], av, bv);
+                        }
+                    }
+                }
+            }
+            if (b < t.e1) {
+                const int g0 = wrapi(t.o0 + a, wp.N0);
+                const int g1 = wrapi(t.o1 + b, wp.N1);
+                double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
 #pragma unroll
-                            for (int j = 0; j < 2; ++j) {
-                                const int c = ct * 8 + 2 * kk + j;
-                                if (c < t.e2) red_add(row + 2 * wrapi(t.o2 + c, wp.N2) + part, d[ct][j]);
-                            }
+                for (int ct = 0; ct < CTMAX; ++ct) {
+                    if (ct < CT) {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const int c = ct * 8 + 2 * kk + j;
+                            if (c < t.e2) red_add(row + 2 * wrapi(t.o2 + c, wp.N2) + part, d[ct][j]);
                         }
                     }
                 }
@@ -461,7 +498,7 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
     if (!p.generic) {
         const size_t sm = sizeof(ScatterSmem);
         SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 4 * 8);
+        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2 * 8);
         if (blocks < 1) blocks = 1;
         k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.tiles, p.n_tiles, p.nodes, p.wp, values,
                                                           reinterpret_cast<double *>(grid));

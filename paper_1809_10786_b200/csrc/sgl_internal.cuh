@@ -19,7 +19,7 @@ constexpr double kTwoPi = 6.28318530717958647692;
 // window tiles:  a tile is <= kTileNodes sorted
 // nodes from one pencil (lo1, lo2 in a W x W cell block), consecutive in lo0.
 // Its box covers the union of the nodes' window supports.
-constexpr int kTileNodes = 32;   // GEMM N-dim (gather) / K-dim (scatter)
+constexpr int kTileNodes = 64;   // GEMM M-dim (gather) / K-dim (scatter)
 constexpr int kBoxMax = 40;      // max box extent on axes 1 and 2
 constexpr int kBox0Max = 48;     // max box extent on axis 0 (slabs)
 constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
