@@ -5,6 +5,7 @@
 // ValueError conditions, reported as SGL_EINVAL + sgl_last_error().
 #include <cufft.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -181,12 +182,17 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         p->s_eff[ax] = (double)p->grid[ax] / p->n_axis[ax];
         p->lam[ax] = p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
     }
-    p->grid_elems = (size_t)p->grid[0] * p->grid[1] * p->grid[2];
     WindowParams &wp = p->wp;
     wp.N0 = p->grid[0];
     wp.N1 = p->grid[1];
     wp.N2 = p->grid[2];
+    wp.N1p = wp.N1 + 2 * q;
+    wp.N2p = wp.N2 + 2 * q;
     wp.q = q;
+    p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
+    // the TMA slab box (kBoxMax^2 cells) must fit the padded plane; tiny grids use
+    // the per-node kernels
+    if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         const double N = p->grid[ax], a = N / kTwoPi, lam = p->lam[ax];
@@ -225,9 +231,14 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         }
     }
     if (rc == SGL_OK) {
-        rc = fft_check(cufftPlan3d(&p->fft, p->grid[0], p->grid[1], p->grid[2], CUFFT_Z2Z), "cufftPlan3d");
+        // transform the interior of the halo-padded grid in place
+        int n[3] = {p->grid[0], p->grid[1], p->grid[2]};
+        int emb[3] = {wp.N0, wp.N1p, wp.N2p};
+        const int dist = (int)std::min<size_t>(p->grid_elems, (size_t)INT32_MAX);
+        rc = fft_check(cufftPlanMany(&p->fft, 3, n, emb, 1, dist, emb, 1, dist, CUFFT_Z2Z, 1), "cufftPlanMany");
         if (rc == SGL_OK) p->fft_ready = true;
     }
+    if (rc == SGL_OK && !p->generic) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && p->profile) {
         for (auto &t : p->timers) {
             for (auto &e : t.ev) cudaEventCreate(&e);
@@ -324,9 +335,11 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
         rec.mark(SGL_STAGE_FFT);
         rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
         if (rc) return rc;
-        rc = fft_check(cufftExecZ2Z(p.fft, reinterpret_cast<cufftDoubleComplex *>(p.grid_buf),
-                                    reinterpret_cast<cufftDoubleComplex *>(p.grid_buf), CUFFT_INVERSE),
-                       "cufftExecZ2Z(inverse)");
+        cufftDoubleComplex *interior =
+            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
+        if (rc) return rc;
+        rc = launch_halo_fill(p, p.grid_buf, st);
         if (rc) return rc;
         rec.mark(SGL_STAGE_WINDOW);
         double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : p.val_buf;
@@ -372,9 +385,10 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
     rec.mark(SGL_STAGE_FFT);
     rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
     if (rc) return rc;
-    rc = fft_check(cufftExecZ2Z(p.fft, reinterpret_cast<cufftDoubleComplex *>(p.grid_buf),
-                                reinterpret_cast<cufftDoubleComplex *>(p.grid_buf), CUFFT_FORWARD),
-                   "cufftExecZ2Z(forward)");
+    rc = launch_halo_fold(p, p.grid_buf, st);
+    if (rc) return rc;
+    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+    rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
     if (rc) return rc;
     rec.mark(SGL_STAGE_BASAL);
     double2 *c = cdev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;

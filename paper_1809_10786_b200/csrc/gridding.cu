@@ -20,6 +20,7 @@
 // Generic kernels (any q, or forced): one warp per node, lanes over axis-2
 // taps, exactly the reference loop nest.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "sgl_internal.cuh"
 
@@ -78,14 +79,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ void red_add(double *addr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
@@ -98,16 +91,20 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
 //     D[node, (b, re|im)] = sum_c W2[c, node] * G[a, b, c]       (DMMA)
 // with the W2 fragments resident in registers and the G fragments read from
 // the shared-memory slab, then applies W1[b, node] and W0[a, node].  The
-// producer streams slabs with cp.async.bulk into a 3-deep ring guarded by
-// full / empty mbarriers, so warps never meet at a CTA barrier inside a tile.
+// producer lane streams one TMA box per slab (cp.async.bulk.tensor.3d, the
+// halo-padded grid needs no wrap on axes 1-2) into a 3-deep ring guarded by
+// full / empty mbarriers; it walks the CTA's tile sequence on its own, so the
+// next tile's first slabs are in flight while the consumers finish a tile.
 
 constexpr int GCW = kTileNodes / 8;   // consumer warps
 constexpr int GT = (GCW + 1) * 32;    // + producer warp
-constexpr int NST = 3;                // slab ring depth
-constexpr int SROWS = kBoxMax;        // slab rows (axis 1)
-constexpr int SSTR = kBoxMax + 4;     // max slab row stride in complex (== 4 mod 8)
+constexpr int NST = 4;                // slab ring depth
+constexpr int SROWS = kBoxMax;        // TMA box rows (axis 1)
+constexpr int SSTR = kBoxMax;         // TMA box width in complex (== 4 mod 8: conflict-free B reads)
+static_assert(SSTR % 8 == 4, "slab row stride must be 4 mod 8 complex");
 constexpr int KSMAX = kBoxMax / 4;    // k-steps over axis 2
 constexpr int NTMAX = kBoxMax / 4;    // 4-row (8 re|im column) tiles over axis 1
+constexpr uint32_t SLAB_BYTES = SROWS * SSTR * 16;
 
 struct GatherSmem {
     double2 slab[NST][SROWS * SSTR];
@@ -122,33 +119,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void issue_slab(GatherSmem &S, int lane, const Tile &t, int a, int buf, int stride,
-                                           const WindowParams &wp, const double2 *grid) {
-    const int g0 = wrapi(t.o0 + a, wp.N0);
-    if (lane == 0) mbar_expect_tx(&S.full[buf], (uint32_t)(t.e1 * t.e2 * 16));
-    __syncwarp();
-    const int g2s = wrapi(t.o2, wp.N2);
-    for (int y = lane; y < t.e1; y += 32) {
-        const int g1 = wrapi(t.o1 + y, wp.N1);
-        const double2 *row = grid + ((size_t)g0 * wp.N1 + g1) * wp.N2;
-        double2 *dst = &S.slab[buf][y * stride];
-        int done = 0, g2 = g2s;
-        while (done < t.e2) {
-            const int n = min(t.e2 - done, wp.N2 - g2);
-            bulk_g2s(dst + done, row + g2, (uint32_t)(n * 16), &S.full[buf]);
-            done += n;
-            g2 = 0;
-        }
-    }
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(GCW * 32) : "memory");
 }
 
 __global__ void __launch_bounds__(GT, 2)
-    k_gather_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
-                   const double2 *__restrict__ grid, double2 *__restrict__ out) {
+    k_gather_tiled(const __grid_constant__ CUtensorMap tmap, const Tile *__restrict__ tiles, int64_t ntiles,
+                   NodeSet nodes, WindowParams wp, double2 *__restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GatherSmem &S = *reinterpret_cast<GatherSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool producer = warp == GCW;
 
     for (int i = tid; i < NST * SROWS * SSTR; i += GT) (&S.slab[0][0])[i] = make_double2(0.0, 0.0);
     if (tid == 0) {
@@ -161,14 +150,38 @@ __global__ void __launch_bounds__(GT, 2)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
 
-    uint32_t seq = 0;                           // slabs streamed by this CTA so far
-    const int node = warp * 8 + (lane >> 2);    // this lane's node (consumers)
+    if (warp == GCW) {
+        // producer: one lane walks the tile sequence and streams slabs
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmap) : "memory");
+            uint32_t q = 0;
+            for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+                const Tile t = tiles[ti];
+                const int c0 = 2 * (t.o2 + wp.q), c1 = t.o1 + wp.q;
+                for (int a = 0; a < t.e0; ++a, ++q) {
+                    const int buf = (int)(q % NST);
+                    const uint32_t use = q / NST;
+                    if (use > 0) mbar_wait(&S.empty[buf], (use - 1) & 1);
+                    mbar_expect_tx(&S.full[buf], SLAB_BYTES);
+                    tma_load_3d(S.slab[buf], &tmap, c0, c1, wrapi(t.o0 + a, wp.N0), &S.full[buf]);
+                }
+            }
+        }
+        return;
+    }
+
+    uint32_t seq = 0;                           // slabs consumed by this CTA so far
+    // node-interleaved M-tiles: warp w owns nodes {w, w+8, ..., w+56} of the
+    // lo0-sorted tile, so every warp spans the tile's whole lo0 range and the
+    // 8 warps stay in lockstep through the slab ring
+    const int node = (lane >> 2) * GCW + warp;  // this lane's node
     const int cc = lane & 3;
     const int rb = lane >> 3, part = (lane >> 2) & 1;
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        consumers_sync();   // previous tile's readers of S.t / S.nu / S.w0 are done
         if (tid == 0) S.t = tiles[ti];
-        __syncthreads();
+        consumers_sync();
         const Tile t = S.t;
         if (tid < kTileNodes) {
             const bool ok = tid < t.count;
@@ -178,30 +191,15 @@ __global__ void __launch_bounds__(GT, 2)
             S.nu[1][tid] = ok ? nodes.u1[s] : -1e9;
             S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
         }
-        __syncthreads();
-        for (int i = tid; i < t.e0 * kTileNodes; i += GT) {
+        consumers_sync();
+        for (int i = tid; i < t.e0 * kTileNodes; i += GCW * 32) {
             const int x = i / kTileNodes, k = i % kTileNodes;
             S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
         }
-        __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
-        const int Cw = KS * 4;
-        const int stride = (Cw & 7) ? Cw : Cw + 4;
-
-        if (producer) {
-            for (int a = 0; a < t.e0; ++a) {
-                const uint32_t q = seq + a;
-                const int buf = (int)(q % NST);
-                const uint32_t use = q / NST;
-                if (use > 0) {
-                    if (lane == 0) mbar_wait(&S.empty[buf], (use - 1) & 1);
-                    __syncwarp();
-                }
-                issue_slab(S, lane, t, a, buf, stride, wp, grid);
-            }
-        } else {
-            double afr[KSMAX], w1r[NTMAX];
+        double afr[KSMAX], w1r[NTMAX];
+        {
             const double u1 = S.nu[1][node], u2 = S.nu[2][node];
 #pragma unroll
             for (int ks = 0; ks < KSMAX; ++ks)
@@ -209,66 +207,67 @@ __global__ void __launch_bounds__(GT, 2)
 #pragma unroll
             for (int nt = 0; nt < NTMAX; ++nt)
                 w1r[nt] = (nt < Mt) ? wfun(u1, t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
-            const bool col_live = warp * 8 < t.count;
-            double acc_re = 0.0, acc_im = 0.0;
-            for (int a = 0; a < t.e0; ++a) {
-                const uint32_t q = seq + a;
-                const int buf = (int)(q % NST);
-                const double w0 = S.w0[a][node];
-                // every consumer observes every phase (keeps the ring's parity
-                // bookkeeping exact); the math is skipped where none of this
-                // warp's 8 nodes has weight on the slab (warp-uniform)
-                mbar_wait(&S.full[buf], (q / NST) & 1);
-                if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
-                    const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
-                    double s_re = 0.0, s_im = 0.0;
+        }
+        consumers_sync();
+        const bool col_live = warp < t.count;
+        double acc_re = 0.0, acc_im = 0.0;
+        for (int a = 0; a < t.e0; ++a) {
+            const uint32_t q = seq + a;
+            const int buf = (int)(q % NST);
+            const double w0 = S.w0[a][node];
+            // every consumer observes every phase (keeps the ring's parity
+            // bookkeeping exact); the math is skipped where none of this
+            // warp's 8 nodes has weight on the slab (warp-uniform)
+            mbar_wait(&S.full[buf], (q / NST) & 1);
+            if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
+                const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
+                double s_re = 0.0, s_im = 0.0;
 #pragma unroll
-                    for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
-                        if (nt0 < Mt) {
-                            double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+                for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
+                    if (nt0 < Mt) {
+                        double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-                            for (int ks = 0; ks < KSMAX; ++ks) {
-                                if (ks < KS) {
+                        for (int ks = 0; ks < KSMAX; ++ks) {
+                            if (ks < KS) {
 #pragma unroll
-                                    for (int i = 0; i < 3; ++i) {
-                                        if (nt0 + i < NTMAX && nt0 + i < Mt) {
-                                            const int b = (nt0 + i) * 4 + rb;
-                                            const double bv = sl[(b * stride + ks * 4 + cc) * 2 + part];
-                                            dmma(d[i], afr[ks], bv);
-                                        }
+                                for (int i = 0; i < 3; ++i) {
+                                    if (nt0 + i < NTMAX && nt0 + i < Mt) {
+                                        const int b = (nt0 + i) * 4 + rb;
+                                        const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
+                                        dmma(d[i], afr[ks], bv);
                                     }
                                 }
                             }
+                        }
 #pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                if (nt0 + i < NTMAX && nt0 + i < Mt) {
-                                    s_re = fma(w1r[nt0 + i], d[i][0], s_re);
-                                    s_im = fma(w1r[nt0 + i], d[i][1], s_im);
-                                }
+                        for (int i = 0; i < 3; ++i) {
+                            if (nt0 + i < NTMAX && nt0 + i < Mt) {
+                                s_re = fma(w1r[nt0 + i], d[i][0], s_re);
+                                s_im = fma(w1r[nt0 + i], d[i][1], s_im);
                             }
                         }
                     }
-                    acc_re = fma(w0, s_re, acc_re);
-                    acc_im = fma(w0, s_im, acc_im);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[buf]);
+                acc_re = fma(w0, s_re, acc_re);
+                acc_im = fma(w0, s_im, acc_im);
             }
-            // reduce over the 4 lanes of a node (their rows b differ)
-            acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
-            acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
-            acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
-            acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
-            if (cc == 0 && node < t.count) out[nodes.perm[t.start + node]] = make_double2(acc_re, acc_im);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[buf]);
         }
         seq += (uint32_t)t.e0;
+        // reduce over the 4 lanes of a node (their rows b differ)
+        acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 1);
+        acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 1);
+        acc_re += __shfl_xor_sync(0xffffffffu, acc_re, 2);
+        acc_im += __shfl_xor_sync(0xffffffffu, acc_im, 2);
+        if (cc == 0 && node < t.count) out[nodes.perm[t.start + node]] = make_double2(acc_re, acc_im);
     }
 }
 
 // ---------------------------------------------------------------------------
 // tiled scatter
 //
-// Work units are (slab a, 4-row M-tile) pairs of the tile's box, dealt
+// Work units are (slab a, 3 x 4-row M-tiles) of the tile's box, dealt
 // round-robin to the CTA's warps.  Per unit
 //     D[(b, re|im), c] = sum_node V[(b, re|im), node] * W2[c, node]   (DMMA)
 // with V = W0[a,node] W1[b,node] v_node formed on the fly, then reduced into
@@ -278,13 +277,16 @@ __global__ void __launch_bounds__(GT, 2)
 constexpr int SW = 8;                 // warps per CTA
 constexpr int STH = SW * 32;
 constexpr int WS = kTileNodes + 4;    // w1/w2 row stride (doubles): conflict-free
-constexpr int CTMAX = kBoxMax / 8;    // 8-column tiles over axis 2
-constexpr int NKS = kTileNodes / 4;   // node k-steps
+constexpr int CTMAX = (kBoxMax + 7) / 8;   // 8-column tiles over axis 2
+
+constexpr int SMT = 3;                // M-tiles per work unit (reuse of each W2 fragment)
+static_assert(CTMAX * 8 >= kBoxMax, "scatter column tiles must cover the box");
+static_assert(KSMAX * 4 >= kBoxMax && NTMAX * 4 >= kBoxMax, "gather tiles must cover the box");
 
 struct ScatterSmem {
     double w0[kBox0Max][kTileNodes];
     double w1[kBoxMax][WS];
-    double w2[kBoxMax][WS];
+    double w2[CTMAX * 8][WS];
     double2 v[kTileNodes];
     double nu[3][kTileNodes];
     Tile t;
@@ -328,9 +330,10 @@ __global__ void __launch_bounds__(STH, 2)
         }
         __syncthreads();
         const int nks = (t.count + 3) >> 2;
-        const int units = t.e0 * Mt;
+        const int mgroups = (Mt + SMT - 1) / SMT;
+        const int units = t.e0 * mgroups;
         for (int u = warp; u < units; u += SW) {
-            const int a = u / Mt, mt = u - a * Mt;
+            const int a = u / mgroups, mt0 = (u - a * mgroups) * SMT;
             // active node k-steps on this slab (nodes sorted by lo0)
             const unsigned lo = __ballot_sync(0xffffffffu, S.w0[a][lane] != 0.0);
             const unsigned hi = __ballot_sync(0xffffffffu, S.w0[a][32 + lane] != 0.0);
@@ -338,36 +341,44 @@ __global__ void __launch_bounds__(STH, 2)
             if (mask == 0ull) continue;
             const int ks0 = (__ffsll((long long)mask) - 1) >> 2;
             const int ks1 = min(nks, ((63 - __clzll((long long)mask)) >> 2) + 1);
-            const int b = mt * 4 + rb;
-            double d[CTMAX][2];
+            double d[SMT][CTMAX][2];
 #pragma unroll
-            for (int ct = 0; ct < CTMAX; ++ct) d[ct][0] = d[ct][1] = 0.0;
+            for (int i = 0; i < SMT; ++i)
 #pragma unroll
-            for (int ks = 0; ks < NKS; ++ks) {
-                if (ks >= ks0 && ks < ks1) {
-                    const int n = ks * 4 + kk;
-                    const double2 v = S.v[n];
-                    const double av = S.w0[a][n] * S.w1[b][n] * (part ? v.y : v.x);
+                for (int ct = 0; ct < CTMAX; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
+#pragma unroll 4
+            for (int ks = ks0; ks < ks1; ++ks) {
+                const int n = ks * 4 + kk;
+                const double2 v = S.v[n];
+                const double wv = S.w0[a][n] * (part ? v.y : v.x);
+                double av[SMT];
 #pragma unroll
-                    for (int ct = 0; ct < CTMAX; ++ct) {
-                        if (ct < CT) {
-                            const double bv = S.w2[ct * 8 + cr][n];
-                            dmma(d[ct], av, bv);
-                        }
-                    }
-                }
-            }
-            if (b < t.e1) {
-                const int g0 = wrapi(t.o0 + a, wp.N0);
-                const int g1 = wrapi(t.o1 + b, wp.N1);
-                double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
+                for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
 #pragma unroll
                 for (int ct = 0; ct < CTMAX; ++ct) {
                     if (ct < CT) {
+                        const double bv = S.w2[ct * 8 + cr][n];
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) {
-                            const int c = ct * 8 + 2 * kk + j;
-                            if (c < t.e2) red_add(row + 2 * wrapi(t.o2 + c, wp.N2) + part, d[ct][j]);
+                        for (int i = 0; i < SMT; ++i)
+                            if (mt0 + i < Mt) dmma(d[i][ct], av[i], bv);
+                    }
+                }
+            }
+            const int g0 = wrapi(t.o0 + a, wp.N0);
+#pragma unroll
+            for (int i = 0; i < SMT; ++i) {
+                const int b = (mt0 + i) * 4 + rb;
+                if (mt0 + i < Mt && b < t.e1) {
+                    // halo-padded grid: rows / columns of the box never wrap
+                    double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
+#pragma unroll
+                    for (int ct = 0; ct < CTMAX; ++ct) {
+                        if (ct < CT) {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const int c = ct * 8 + 2 * kk + j;
+                                if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
+                            }
                         }
                     }
                 }
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(NW_GEN * 32)
         for (int b = 0; b < P; ++b) {
             const double wab = wa * w1[b];
             const int g1 = wrapi(l1 - wp.q + b, wp.N1);
-            const double2 *row = grid + ((size_t)g0 * wp.N1 + g1) * wp.N2;
+            const double2 *row = grid + ((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q;
             double sr = 0.0, si = 0.0;
             for (int c = lane; c < P; c += 32) {
                 const double2 g = row[wrapi(l2 - wp.q + c, wp.N2)];
@@ -451,12 +462,59 @@ __global__ void __launch_bounds__(NW_GEN * 32)
             const double wab = wa * w1[b];
             const double tr = wab * v.x, tim = wab * v.y;
             const int g1 = wrapi(l1 - wp.q + b, wp.N1);
-            double *row = grid + 2 * (((size_t)g0 * wp.N1 + g1) * wp.N2);
+            double *row = grid + 2 * (((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q);
             for (int c = lane; c < P; c += 32) {
                 const int g2 = wrapi(l2 - wp.q + c, wp.N2);
                 red_add(row + 2 * g2, w2[c] * tr);
                 red_add(row + 2 * g2 + 1, w2[c] * tim);
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// periodic halo of the padded grid (axes 1-2)
+
+// copy interior images into the halo (after the inverse FFT, before gather)
+__global__ void k_halo_fill(WindowParams wp, double2 *__restrict__ grid) {
+    const int64_t n = (int64_t)wp.N0 * wp.N1p * wp.N2p;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int p2 = (int)(i % wp.N2p);
+        const int64_t r = i / wp.N2p;
+        const int p1 = (int)(r % wp.N1p);
+        const int64_t g0 = r / wp.N1p;
+        const bool in1 = p1 >= wp.q && p1 < wp.q + wp.N1, in2 = p2 >= wp.q && p2 < wp.q + wp.N2;
+        if (in1 && in2) continue;
+        const int s1 = wrapi(p1 - wp.q, wp.N1) + wp.q, s2 = wrapi(p2 - wp.q, wp.N2) + wp.q;
+        grid[i] = grid[((size_t)g0 * wp.N1p + s1) * wp.N2p + s2];
+    }
+}
+
+// add the halo images back into the interior (after scatter, before FFT)
+__global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
+    const int64_t n = (int64_t)wp.N0 * wp.N1 * wp.N2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int i2 = (int)(i % wp.N2);
+        const int64_t r = i / wp.N2;
+        const int i1 = (int)(r % wp.N1);
+        const int64_t g0 = r / wp.N1;
+        if (i1 >= wp.q && i1 < wp.N1 - wp.q && i2 >= wp.q && i2 < wp.N2 - wp.q) continue;   // no images
+        double2 acc = make_double2(0.0, 0.0);
+        bool any = false;
+        // every padded position p = i + q + k N inside [0, N + 2q), except k = 0 on both axes
+        for (int p1 = (i1 + wp.q) % wp.N1; p1 < wp.N1p; p1 += wp.N1) {
+            for (int p2 = (i2 + wp.q) % wp.N2; p2 < wp.N2p; p2 += wp.N2) {
+                if (p1 == i1 + wp.q && p2 == i2 + wp.q) continue;
+                const double2 v = grid[((size_t)g0 * wp.N1p + p1) * wp.N2p + p2];
+                acc.x += v.x;
+                acc.y += v.y;
+                any = true;
+            }
+        }
+        if (any) {
+            double2 &dst = grid[((size_t)g0 * wp.N1p + i1 + wp.q) * wp.N2p + i2 + wp.q];
+            dst.x += acc.x;
+            dst.y += acc.y;
         }
     }
 }
@@ -480,15 +538,56 @@ int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStrea
     if (!p.generic) {
         const size_t sm = sizeof(GatherSmem);
         SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2 * 8);
+        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2);
         if (blocks < 1) blocks = 1;
-        k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tiles, p.n_tiles, p.nodes, p.wp, grid, values);
+        k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
     } else {
         const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_gather_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(p.M, p.nodes, p.wp,
                                                                                            grid, values);
     }
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int make_grid_tmap(Plan &p) {
+    // FLOAT64 view of the padded grid: dims {2 N2p, N1p, N0}; one box = one slab
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult qr;
+        void *fn = nullptr;
+        SGL_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        if (qr != cudaDriverEntryPointSuccess || !fn) {
+            set_error("cuTensorMapEncodeTiled is unavailable");
+            return SGL_ECUDA;
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const WindowParams &w = p.wp;
+    cuuint64_t dims[3] = {(cuuint64_t)2 * w.N2p, (cuuint64_t)w.N1p, (cuuint64_t)w.N0};
+    cuuint64_t strides[2] = {(cuuint64_t)w.N2p * 16, (cuuint64_t)w.N1p * w.N2p * 16};
+    cuuint32_t box[3] = {2 * SSTR, SROWS, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p.grid_buf, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        return SGL_ECUDA;
+    }
+    p.tmap_ready = true;
+    return SGL_OK;
+}
+
+int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st) {
+    k_halo_fill<<<num_sms() * 8, 256, 0, st>>>(p.wp, grid);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st) {
+    k_halo_fold<<<num_sms() * 8, 256, 0, st>>>(p.wp, grid);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }

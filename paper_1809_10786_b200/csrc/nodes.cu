@@ -123,12 +123,22 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
             double uu[3] = {u0[j], u1[j], u2[j]};
             int l0 = lo_of(uu[0]);
             if (l0 - first0 > g.span0) break;
+            int tmn[3], tmx[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 int lo = lo_of(uu[d]);
-                int lower = lo - g.q + ((uu[d] > (double)lo) ? 1 : 0);
-                mn[d] = min(mn[d], lower);
-                mx[d] = max(mx[d], lo + g.q);
+                int lower = lo - g.q + ((uu[d] > (double)lo) ? 1 : 0);   // a node on a grid line has 2q+1 taps
+                tmn[d] = min(mn[d], lower);
+                tmx[d] = max(mx[d], lo + g.q);
+            }
+            // the box must fit the device slab (axes 1, 2) and the slab-count limit (axis 0)
+            if (j > i && (tmx[1] - tmn[1] + 1 > kBoxMax || tmx[2] - tmn[2] + 1 > kBoxMax ||
+                          tmx[0] - tmn[0] + 1 > kBox0Max))
+                break;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                mn[d] = tmn[d];
+                mx[d] = tmx[d];
             }
         }
         if (out) {

@@ -1,6 +1,7 @@
 // Internal definitions shared by the NFSGLFT CUDA sources (sm_100a).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <stdint.h>
@@ -20,7 +21,7 @@ constexpr double kTwoPi = 6.28318530717958647692;
 // nodes from one pencil (lo1, lo2 in a W x W cell block), consecutive in lo0.
 // Its box covers the union of the nodes' window supports.
 constexpr int kTileNodes = 64;   // GEMM M-dim (gather) / K-dim (scatter)
-constexpr int kBoxMax = 40;      // max box extent on axes 1 and 2
+constexpr int kBoxMax = 36;      // max box extent on axes 1 and 2 (== the TMA slab box)
 constexpr int kBox0Max = 48;     // max box extent on axis 0 (slabs)
 constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
 
@@ -37,8 +38,14 @@ struct NodeSet {
     int32_t *perm = nullptr;   // sorted position -> caller index
 };
 
+// The oversampled grid is stored with a periodic halo of q cells on both
+// sides of axes 1 and 2 (pitches N1p = N1 + 2q, N2p = N2 + 2q): interior cell
+// (g0, g1, g2) sits at padded (g0, g1 + q, g2 + q).  This is the reference's
+// pad_wrap / fold_wrap (_gridding.py:29-50) restricted to axes 1-2, so window
+// boxes never wrap there and one TMA box load fetches a whole slab.
 struct WindowParams {
     int32_t N0, N1, N2;
+    int32_t N1p, N2p;
     int32_t q;
     double c0, c1, c2;          // (N/2pi)/sqrt(2 pi lam)
     double h0, h1, h2;          // 1/(2 lam)
@@ -84,7 +91,9 @@ struct Plan {
     double *dec0 = nullptr, *dec1 = nullptr, *dec2 = nullptr;  // deconv incl. (2pi)^3/prod N
 
     // scratch
-    double2 *grid_buf = nullptr;   // N0 x N1 x N2 complex
+    double2 *grid_buf = nullptr;   // N0 x N1p x N2p complex (halo-padded)
+    alignas(64) CUtensorMap tmap;  // TMA descriptor of grid_buf (FLOAT64 view)
+    bool tmap_ready = false;
     double2 *beta = nullptr;       // B^2 x 4B complex
     double2 *coef_buf = nullptr;   // count complex (staging)
     double2 *val_buf = nullptr;    // M complex (staging)
@@ -116,5 +125,8 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
 int launch_basal_forward(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st,
                          cudaEvent_t mid);
 int launch_basal_adjoint(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
+int make_grid_tmap(Plan &p);
+int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st);
+int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
 
 }  // namespace sgl

@@ -69,7 +69,7 @@ def test_config4_adjoint_matches_reference(sgl):
     assert np.all(np.isfinite(f))
 
 
-@pytest.mark.parametrize("name", ["b8_q16", "b5_q10", "edges_b4_q5", "cfg1"])
+@pytest.mark.parametrize("name", ["b8_q16", "b5_q10", "edges_b8_q16", "cfg1"])
 def test_tiled_and_generic_kernels_agree(sgl, name):
     # the reference's TestBackends pattern (test_nfft.py:213-225)
     g = load_golden(name)
