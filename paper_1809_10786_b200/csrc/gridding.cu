@@ -171,10 +171,10 @@ __global__ void __launch_bounds__(GT, 2)
     }
 
     uint32_t seq = 0;                           // slabs consumed by this CTA so far
-    // node-interleaved M-tiles: warp w owns nodes {w, w+8, ..., w+56} of the
-    // lo0-sorted tile, so every warp spans the tile's whole lo0 range and the
-    // 8 warps stay in lockstep through the slab ring
-    const int node = (lane >> 2) * GCW + warp;  // this lane's node
+    // warp w owns the 8 consecutive nodes 8w .. 8w+7 of the lo0-sorted tile:
+    // its active slab range is short and inactive slabs are skipped; the
+    // 4-deep ring absorbs the few slabs of skew between warps
+    const int node = warp * 8 + (lane >> 2);    // this lane's node
     const int cc = lane & 3;
     const int rb = lane >> 3, part = (lane >> 2) & 1;
 
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(GT, 2)
                 w1r[nt] = (nt < Mt) ? wfun(u1, t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
         }
         consumers_sync();
-        const bool col_live = warp < t.count;
+        const bool col_live = warp * 8 < t.count;
         double acc_re = 0.0, acc_im = 0.0;
         for (int a = 0; a < t.e0; ++a) {
             const uint32_t q = seq + a;
