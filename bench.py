@@ -181,24 +181,22 @@ def main():
 
     import paper_1809_10786_b200 as sgl
     from paper_1809_10786_b200 import _native, workloads
+    from paper_1809_10786_b200.distributed import ShardedPlan
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     w = workloads.config(args.config, M=args.m, seed=rank)
-    # rho: the global maximum radius over all ranks' shards
-    rho_t = torch.tensor([w.rho], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(rho_t, op=dist.ReduceOp.MAX)
-    rho = float(rho_t.item())
-
     coeffs_h = w.coeffs if w.coeffs.ndim == 1 else w.coeffs[0]
     pts_d = torch.as_tensor(w.points, device=dev)
     c_d = torch.as_tensor(coeffs_h, device=dev)
     v_d = torch.as_tensor(w.values, device=dev)
     t0 = time.perf_counter()
-    p = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=False)
+    # rho is global (all-reduce max over the ranks' shards) -- distributed.ShardedPlan
+    sp = ShardedPlan(w.B, pts_d, device=local) if world > 1 else None
+    p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local)
+    rho = sp.rho if sp is not None else p.rho
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - t0
     pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True)
@@ -207,7 +205,7 @@ def main():
     def step(pl):
         f = sgl.forward(pl, c_d)
         a = sgl.adjoint(pl, v_d)
-        if world > 1:
+        if world > 1:   # the adjoint's exchange step (ShardedPlan.adjoint)
             dist.all_reduce(torch.view_as_real(a))
         return f, a
 
