@@ -44,7 +44,7 @@ void free_plan(Plan *p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
-    void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->tiles, p->Kl, p->Km,
+    void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf};
     for (void *b : bufs)

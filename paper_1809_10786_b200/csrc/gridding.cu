@@ -267,28 +267,34 @@ __global__ void __launch_bounds__(GT, 2)
 // ---------------------------------------------------------------------------
 // tiled scatter
 //
-// Work units are (slab a, 3 x 4-row M-tiles) of the tile's box, dealt
-// round-robin to the CTA's warps.  Per unit
-//     D[(b, re|im), c] = sum_node V[(b, re|im), node] * W2[c, node]   (DMMA)
-// with V = W0[a,node] W1[b,node] v_node formed on the fly, then reduced into
-// the grid with RED.ADD.F64.  Node k-steps with no weight on the slab are
-// skipped (nodes are sorted by lo0 inside a tile).
+// Scatter tiles hold up to 128 nodes (twice the gather's) so that each RED
+// of an output fragment carries the sum over more nodes.  A warp owns whole
+// axis-0 slabs of the tile's box.  Per slab it forms W0[a, node] (one exp
+// per node, staged through a per-warp smem row), finds the active node
+// k-steps (nodes are sorted by lo0 inside a tile), and for groups of 3
+// four-row M-tiles computes
+//     D[(b, re|im), c] = sum_node V[(b, re|im), node] * W2[c, node]  (DMMA)
+// with V = W0 W1 v formed on the fly and every W2 fragment feeding 3 DMMAs.
+// D is reduced into the halo-padded grid with RED.E.ADD.F64 (no wrap on
+// axes 1-2; the halo is folded back by k_halo_fold).
 
+constexpr int SN = kSTileNodes;       // nodes per scatter tile
 constexpr int SW = 8;                 // warps per CTA
 constexpr int STH = SW * 32;
-constexpr int WS = kTileNodes + 4;    // w1/w2 row stride (doubles): conflict-free
+constexpr int WS = SN + 4;            // w1/w2 row stride (doubles): == 4 mod 16, conflict-free
 constexpr int CTMAX = (kBoxMax + 7) / 8;   // 8-column tiles over axis 2
-
-constexpr int SMT = 3;                // M-tiles per work unit (reuse of each W2 fragment)
+constexpr int SMT = 3;                // M-tiles per group (reuse of each W2 fragment)
+constexpr int SKS = SN / 4;           // node k-steps
 static_assert(CTMAX * 8 >= kBoxMax, "scatter column tiles must cover the box");
 static_assert(KSMAX * 4 >= kBoxMax && NTMAX * 4 >= kBoxMax, "gather tiles must cover the box");
+static_assert(SN == 128, "the active-k-step mask below assumes 4 x 32 nodes");
 
 struct ScatterSmem {
-    double w0[kBox0Max][kTileNodes];
     double w1[kBoxMax][WS];
     double w2[CTMAX * 8][WS];
-    double2 v[kTileNodes];
-    double nu[3][kTileNodes];
+    double w0[SW][SN];                // per-warp row: W0 of the warp's current slab
+    double2 v[SN];
+    double nu[3][SN];
     Tile t;
 };
 
@@ -299,13 +305,14 @@ __global__ void __launch_bounds__(STH, 2)
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
+    double *w0row = S.w0[warp];
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         __syncthreads();   // previous tile's readers are done
         if (tid == 0) S.t = tiles[ti];
         __syncthreads();
         const Tile t = S.t;
-        if (tid < kTileNodes) {
+        if (tid < SN) {
             const bool ok = tid < t.count;
             const int64_t s = (int64_t)t.start + tid;
             S.nu[0][tid] = ok ? nodes.u0[s] : -1e9;
@@ -316,73 +323,77 @@ __global__ void __launch_bounds__(STH, 2)
         __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
         const int CT = (t.e2 + 7) >> 3;
-        for (int i = tid; i < t.e0 * kTileNodes; i += STH) {
-            const int x = i / kTileNodes, k = i % kTileNodes;
-            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
-        }
-        for (int i = tid; i < Mt * 4 * kTileNodes; i += STH) {
-            const int y = i / kTileNodes, k = i % kTileNodes;
+        for (int i = tid; i < Mt * 4 * SN; i += STH) {
+            const int y = i / SN, k = i % SN;
             S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
         }
-        for (int i = tid; i < CT * 8 * kTileNodes; i += STH) {
-            const int y = i / kTileNodes, k = i % kTileNodes;
+        for (int i = tid; i < CT * 8 * SN; i += STH) {
+            const int y = i / SN, k = i % SN;
             S.w2[y][k] = wfun(S.nu[2][k], t.o2 + y, wp.c2, wp.h2, wp.q);
         }
         __syncthreads();
         const int nks = (t.count + 3) >> 2;
-        const int mgroups = (Mt + SMT - 1) / SMT;
-        const int units = t.e0 * mgroups;
-        for (int u = warp; u < units; u += SW) {
-            const int a = u / mgroups, mt0 = (u - a * mgroups) * SMT;
-            // active node k-steps on this slab (nodes sorted by lo0)
-            const unsigned lo = __ballot_sync(0xffffffffu, S.w0[a][lane] != 0.0);
-            const unsigned hi = __ballot_sync(0xffffffffu, S.w0[a][32 + lane] != 0.0);
-            const unsigned long long mask = ((unsigned long long)hi << 32) | lo;
-            if (mask == 0ull) continue;
-            const int ks0 = (__ffsll((long long)mask) - 1) >> 2;
-            const int ks1 = min(nks, ((63 - __clzll((long long)mask)) >> 2) + 1);
-            double d[SMT][CTMAX][2];
+        for (int a = warp; a < t.e0; a += SW) {
+            // W0 of this slab for all nodes; active k-steps from the nonzero mask
+            int kfirst = SKS, klast = -1;
 #pragma unroll
-            for (int i = 0; i < SMT; ++i)
-#pragma unroll
-                for (int ct = 0; ct < CTMAX; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
-#pragma unroll 4
-            for (int ks = ks0; ks < ks1; ++ks) {
-                const int n = ks * 4 + kk;
-                const double2 v = S.v[n];
-                const double wv = S.w0[a][n] * (part ? v.y : v.x);
-                double av[SMT];
-#pragma unroll
-                for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
-#pragma unroll
-                for (int ct = 0; ct < CTMAX; ++ct) {
-                    if (ct < CT) {
-                        const double bv = S.w2[ct * 8 + cr][n];
-#pragma unroll
-                        for (int i = 0; i < SMT; ++i)
-                            if (mt0 + i < Mt) dmma(d[i][ct], av[i], bv);
-                    }
+            for (int j = 0; j < SN / 32; ++j) {
+                const double w = wfun(S.nu[0][32 * j + lane], t.o0 + a, wp.c0, wp.h0, wp.q);
+                w0row[32 * j + lane] = w;
+                const unsigned m = __ballot_sync(0xffffffffu, w != 0.0);
+                if (m) {
+                    kfirst = min(kfirst, (32 * j + __ffs(m) - 1) >> 2);
+                    klast = max(klast, (32 * j + 31 - __clz(m)) >> 2);
                 }
             }
+            __syncwarp();
+            if (klast < 0) continue;
+            const int ks0 = kfirst, ks1 = min(nks, klast + 1);
             const int g0 = wrapi(t.o0 + a, wp.N0);
+            for (int mt0 = 0; mt0 < Mt; mt0 += SMT) {
+                double d[SMT][CTMAX][2];
 #pragma unroll
-            for (int i = 0; i < SMT; ++i) {
-                const int b = (mt0 + i) * 4 + rb;
-                if (mt0 + i < Mt && b < t.e1) {
-                    // halo-padded grid: rows / columns of the box never wrap
-                    double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
+                for (int i = 0; i < SMT; ++i)
+#pragma unroll
+                    for (int ct = 0; ct < CTMAX; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
+#pragma unroll 2
+                for (int ks = ks0; ks < ks1; ++ks) {
+                    const int n = ks * 4 + kk;
+                    const double2 v = S.v[n];
+                    const double wv = w0row[n] * (part ? v.y : v.x);
+                    double av[SMT];
+#pragma unroll
+                    for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
 #pragma unroll
                     for (int ct = 0; ct < CTMAX; ++ct) {
                         if (ct < CT) {
+                            const double bv = S.w2[ct * 8 + cr][n];
 #pragma unroll
-                            for (int j = 0; j < 2; ++j) {
-                                const int c = ct * 8 + 2 * kk + j;
-                                if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
+                            for (int i = 0; i < SMT; ++i)
+                                if (mt0 + i < Mt) dmma(d[i][ct], av[i], bv);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < SMT; ++i) {
+                    const int b = (mt0 + i) * 4 + rb;
+                    if (mt0 + i < Mt && b < t.e1) {
+                        // halo-padded grid: rows / columns of the box never wrap
+                        double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
+#pragma unroll
+                        for (int ct = 0; ct < CTMAX; ++ct) {
+                            if (ct < CT) {
+#pragma unroll
+                                for (int j = 0; j < 2; ++j) {
+                                    const int c = ct * 8 + 2 * kk + j;
+                                    if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
+                                }
                             }
                         }
                     }
                 }
             }
+            __syncwarp();   // w0row is rewritten for the warp's next slab
         }
     }
 }
@@ -597,9 +608,9 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
     if (!p.generic) {
         const size_t sm = sizeof(ScatterSmem);
         SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2 * 8);
+        int64_t blocks = std::min<int64_t>(p.n_stiles, (int64_t)num_sms() * 2 * 8);
         if (blocks < 1) blocks = 1;
-        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.tiles, p.n_tiles, p.nodes, p.wp, values,
+        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.nodes, p.wp, values,
                                                           reinterpret_cast<double *>(grid));
     } else {
         const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);

@@ -98,12 +98,14 @@ __global__ void k_run_starts(const int32_t *head, const int32_t *rank, int64_t M
 
 struct TileGeom {
     int q;
-    int span0;  // max lo0 span inside a tile
+    int span0;      // max lo0 span inside a tile
+    int max_nodes;  // nodes per tile
+    int box0;       // max box extent on axis 0
 };
 
 __device__ __forceinline__ int lo_of(double u) { return (int)floor(u); }
 
-// One thread per pencil run: greedy cut into tiles of <= kTileNodes nodes
+// One thread per pencil run: greedy cut into tiles of <= max_nodes nodes
 // whose lo0 span is <= span0.  write == nullptr: count only.
 __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const double *u0,
                         const double *u1, const double *u2, TileGeom g, int32_t *counts,
@@ -119,7 +121,7 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
         int first0 = lo_of(u0[i]);
         int mn[3] = {1 << 30, 1 << 30, 1 << 30}, mx[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
         int64_t j = i;
-        for (; j < e && j - i < kTileNodes; ++j) {
+        for (; j < e && j - i < g.max_nodes; ++j) {
             double uu[3] = {u0[j], u1[j], u2[j]};
             int l0 = lo_of(uu[0]);
             if (l0 - first0 > g.span0) break;
@@ -133,7 +135,7 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
             }
             // the box must fit the device slab (axes 1, 2) and the slab-count limit (axis 0)
             if (j > i && (tmx[1] - tmn[1] + 1 > kBoxMax || tmx[2] - tmn[2] + 1 > kBoxMax ||
-                          tmx[0] - tmn[0] + 1 > kBox0Max))
+                          tmx[0] - tmn[0] + 1 > g.box0))
                 break;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
@@ -269,25 +271,31 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     SGL_CUDA_CHECK(counts.alloc(nruns));
     SGL_CUDA_CHECK(offs.alloc(nruns));
     k_run_starts<<<grid_for(M, T), T, 0, st>>>(head.p, rank.p, M, starts.p);
-    TileGeom tg{p.q, kBox0Max - 2 * p.q - 1};
-    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
-                                                 counts.p, nullptr, nullptr);
-    {
-        DevBuf<unsigned char> tmp;
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, offs.p, (int)nruns, st);
-        SGL_CUDA_CHECK(tmp.alloc(tb));
-        cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, offs.p, (int)nruns, st);
-    }
-    int32_t lc = 0, lo = 0;
-    SGL_CUDA_CHECK(cudaMemcpyAsync(&lc, counts.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaMemcpyAsync(&lo, offs.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-    p.n_tiles = (int64_t)lc + lo;
-    SGL_CUDA_CHECK(cudaMalloc(&p.tiles, sizeof(Tile) * p.n_tiles));
-    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
-                                                 counts.p, offs.p, p.tiles);
-    SGL_CUDA_CHECK(cudaGetLastError());
+    auto build = [&](const TileGeom &tg, Tile **out, int64_t *nout) -> int {
+        k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
+                                                     counts.p, nullptr, nullptr);
+        {
+            DevBuf<unsigned char> tmp;
+            size_t tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, offs.p, (int)nruns, st);
+            SGL_CUDA_CHECK(tmp.alloc(tb));
+            cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, offs.p, (int)nruns, st);
+        }
+        int32_t lc = 0, lo = 0;
+        SGL_CUDA_CHECK(cudaMemcpyAsync(&lc, counts.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaMemcpyAsync(&lo, offs.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+        *nout = (int64_t)lc + lo;
+        SGL_CUDA_CHECK(cudaMalloc(out, sizeof(Tile) * (*nout)));
+        k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
+                                                     counts.p, offs.p, *out);
+        SGL_CUDA_CHECK(cudaGetLastError());
+        return SGL_OK;
+    };
+    int rc = build(TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max}, &p.tiles, &p.n_tiles);
+    if (rc) return rc;
+    rc = build(TileGeom{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max}, &p.stiles, &p.n_stiles);
+    if (rc) return rc;
 
     // tile statistics (host): nodes covered and DMMA count of one gather pass
     std::vector<Tile> ht(p.n_tiles);

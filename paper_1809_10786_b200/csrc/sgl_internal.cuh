@@ -20,9 +20,11 @@ constexpr double kTwoPi = 6.28318530717958647692;
 // window tiles:  a tile is <= kTileNodes sorted
 // nodes from one pencil (lo1, lo2 in a W x W cell block), consecutive in lo0.
 // Its box covers the union of the nodes' window supports.
-constexpr int kTileNodes = 64;   // GEMM M-dim (gather) / K-dim (scatter)
+constexpr int kTileNodes = 64;   // gather tiles: GEMM M-dim (8 warps x 8 nodes)
 constexpr int kBoxMax = 36;      // max box extent on axes 1 and 2 (== the TMA slab box)
-constexpr int kBox0Max = 48;     // max box extent on axis 0 (slabs)
+constexpr int kBox0Max = 48;     // gather: max box extent on axis 0 (slabs)
+constexpr int kSTileNodes = 128; // scatter tiles: GEMM K-dim (more nodes per RED)
+constexpr int kSBox0Max = 64;    // scatter: max box extent on axis 0
 constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
 
 struct Tile {
@@ -74,8 +76,10 @@ struct Plan {
 
     WindowParams wp;
     NodeSet nodes;
-    Tile *tiles = nullptr;
+    Tile *tiles = nullptr;        // gather tiles (<= kTileNodes nodes)
     int64_t n_tiles = 0;
+    Tile *stiles = nullptr;       // scatter tiles (<= kSTileNodes nodes)
+    int64_t n_stiles = 0;
     int64_t tile_nodes = 0;
     int64_t tile_dmma = 0;
     double plan_ms = 0;
