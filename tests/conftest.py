@@ -29,7 +29,7 @@ def golden_names(pattern="*"):
     return out
 
 
-SMALL = [n for n in golden_names() if not n.startswith("cfg")]
+SMALL = [n for n in golden_names() if not n.startswith(("cfg", "inv_"))]
 
 
 @pytest.fixture(scope="session")

@@ -167,6 +167,22 @@ def cfg_cases(ref, skip_big):
     return out
 
 
+def invert_cases(ref):
+    """The CG inverse (solvers.py:204-277) on small systems: CGNR and CGNE."""
+    out = {}
+    for name, B, M, rad, seed, it in [("inv_cgnr_b4", 4, 200, 2.5, 301, 60), ("inv_cgne_b6", 6, 60, 2.0, 302, 40)]:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        c = ref.gen_coeffs(B, rng)
+        pts = ref.gen_points_ball(M, rad, rng)
+        vals = ref.forward(ref.plan(B, pts), c)
+        rep = ref.invert(pts, vals, B, max_iter=it, tol=1e-12, true_coeffs=c)
+        out[name] = dict(B=B, q=16, compact=False, points=pts, coeffs=c, values=vals,
+                         solution=rep.solution, iterations=rep.iterations, converged=rep.converged,
+                         residual_history=np.array(rep.residual_history),
+                         abs_error_history=np.array(rep.abs_error_history))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true")
@@ -178,6 +194,8 @@ def main():
         cases.update(small_cases(ref))
     if args.only in ("", "cfg"):
         cases.update(cfg_cases(ref, args.skip_big))
+    if args.only in ("", "invert"):
+        cases.update(invert_cases(ref))
     for name, d in cases.items():
         path = os.path.join(HERE, f"ref_{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})

@@ -179,3 +179,21 @@ def test_config3_full_size(sgl):
     lhs = np.vdot(w.values, f)
     rhs = np.vdot(sgl.adjoint(p, w.values), w.coeffs)
     assert abs(lhs - rhs) <= 1e-11 * np.linalg.norm(f) * np.linalg.norm(w.values)
+
+
+def test_config4_full_size_adjoint(sgl):
+    """BASELINE config 4 at full size (B = 128, M = 1e8 nodes, one GPU): the
+    adjoint over all nodes with values zeroed outside the golden subset must
+    match the reference adjoint of the subset."""
+    from paper_1809_10786_b200 import workloads
+    g = load_golden("cfg4_sub120")
+    w = workloads.config(4)
+    assert w.rho == float(g["rho"])
+    assert np.array_equal(w.points[g["sel"]], g["points"])
+    p = sgl.plan(128, w.points)
+    v = np.zeros(w.M, dtype=complex)
+    v[g["sel"]] = g["values"]
+    del w
+    a = sgl.adjoint(p, v)
+    assert np.all(np.isfinite(a))
+    assert rel(a, g["adj"]) <= TOL_CFG4, rel(a, g["adj"])
