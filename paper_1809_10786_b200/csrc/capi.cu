@@ -44,7 +44,9 @@ void free_plan(Plan *p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
-    void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
+    if (p->snodes_shared) p->snodes = NodeSet();
+    void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->snodes.u0, p->snodes.u1, p->snodes.u2,
+                    p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf};
     for (void *b : bufs)

@@ -610,7 +610,7 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
         SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int64_t blocks = std::min<int64_t>(p.n_stiles, (int64_t)num_sms() * 2 * 8);
         if (blocks < 1) blocks = 1;
-        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.nodes, p.wp, values,
+        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.snodes, p.wp, values,
                                                           reinterpret_cast<double *>(grid));
     } else {
         const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);

@@ -48,11 +48,11 @@ __device__ __forceinline__ void to_u(double tau, int N, double &u, int &lo) {
 }
 
 struct KeyGeom {
-    int N0, N1, N2, W, P2;
+    int N0, N1, N2, W1, W2, P2;   // pencils of W1 x W2 cells on axes 1-2, P2 per row
 };
 
-__global__ void k_warp_key(const double *pts, int64_t M, double rho, KeyGeom g, double *u0,
-                           double *u1, double *u2, uint64_t *key, int32_t *idx) {
+__global__ void k_warp(const double *pts, int64_t M, double rho, int N0, int N1, int N2, double *u0,
+                       double *u1, double *u2) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= M) return;
     double r = pts[3 * i], th = pts[3 * i + 1], ph = pts[3 * i + 2];
@@ -63,13 +63,20 @@ __global__ void k_warp_key(const double *pts, int64_t M, double rho, KeyGeom g, 
     double t2 = reduce_2pi(ph);
     double a, b, c;
     int l0, l1, l2;
-    to_u(t0, g.N0, a, l0);
-    to_u(t1, g.N1, b, l1);
-    to_u(t2, g.N2, c, l2);
+    to_u(t0, N0, a, l0);
+    to_u(t1, N1, b, l1);
+    to_u(t2, N2, c, l2);
     u0[i] = a;
     u1[i] = b;
     u2[i] = c;
-    uint64_t pencil = (uint64_t)(l1 / g.W) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W);
+}
+
+__global__ void k_key(const double *u0, const double *u1, const double *u2, int64_t M, KeyGeom g, uint64_t *key,
+                      int32_t *idx) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int l0 = (int)floor(u0[i]), l1 = (int)floor(u1[i]), l2 = (int)floor(u2[i]);
+    const uint64_t pencil = (uint64_t)(l1 / g.W1) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W2);
     key[i] = pencil * (uint64_t)g.N0 + (uint64_t)l0;
     idx[i] = (int32_t)i;
 }
@@ -174,6 +181,91 @@ inline unsigned grid_for(int64_t n, int threads) {
     return (unsigned)((n + threads - 1) / threads);
 }
 
+// Sort the nodes by (pencil of W1 x W2 cells, lo0) into `ns` and cut the
+// pencil runs into window tiles.
+int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2, int W1, int W2,
+                   const TileGeom &tg, NodeSet &ns, Tile **tiles, int64_t *ntiles, bool make_tiles,
+                   cudaStream_t st, bool reuse_order = false) {
+    const int64_t M = p.M;
+    const int T = 256;
+    if (!reuse_order) {
+        SGL_CUDA_CHECK(cudaMalloc(&ns.u0, sizeof(double) * (M ? M : 1)));
+        SGL_CUDA_CHECK(cudaMalloc(&ns.u1, sizeof(double) * (M ? M : 1)));
+        SGL_CUDA_CHECK(cudaMalloc(&ns.u2, sizeof(double) * (M ? M : 1)));
+        SGL_CUDA_CHECK(cudaMalloc(&ns.perm, sizeof(int32_t) * (M ? M : 1)));
+    }
+    if (M == 0) return SGL_OK;
+    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2};
+    DevBuf<uint64_t> key, key_s;
+    DevBuf<int32_t> idx;
+    SGL_CUDA_CHECK(key.alloc(M));
+    SGL_CUDA_CHECK(key_s.alloc(M));
+    SGL_CUDA_CHECK(idx.alloc(M));
+    k_key<<<grid_for(M, T), T, 0, st>>>(a0, a1, a2, M, kg, key.p, idx.p);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    // sort by (pencil, lo0); only the bits in use
+    const uint64_t maxkey = (uint64_t)((p.grid[1] + W1 - 1) / W1) * kg.P2 * (uint64_t)p.grid[0];
+    int bits = 1;
+    while (bits < 64 && (1ull << bits) < maxkey) ++bits;
+    {
+        DevBuf<int32_t> perm_tmp;
+        if (reuse_order) SGL_CUDA_CHECK(perm_tmp.alloc(M));   // order already in ns; keys needed for the runs
+        int32_t *perm_out = reuse_order ? perm_tmp.p : ns.perm;
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_s.p, idx.p, perm_out, (int)M, 0, bits, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_s.p, idx.p, perm_out, (int)M, 0, bits, st);
+        SGL_CUDA_CHECK(cudaGetLastError());
+    }
+    if (!reuse_order) {
+        k_permute<<<grid_for(M, T), T, 0, st>>>(ns.perm, M, a0, a1, a2, ns.u0, ns.u1, ns.u2);
+        SGL_CUDA_CHECK(cudaGetLastError());
+    }
+    if (!make_tiles) return SGL_OK;
+
+    // pencil runs
+    DevBuf<int32_t> head, rank, starts, counts, offs;
+    SGL_CUDA_CHECK(head.alloc(M));
+    SGL_CUDA_CHECK(rank.alloc(M));
+    k_run_heads<<<grid_for(M, T), T, 0, st>>>(key_s.p, M, (uint64_t)p.grid[0], head.p);
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, head.p, rank.p, (int)M, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, rank.p, (int)M, st);
+    }
+    int32_t last_rank = 0, last_head = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_rank, rank.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_head, head.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int64_t nruns = (int64_t)last_rank + last_head;
+    SGL_CUDA_CHECK(starts.alloc(nruns));
+    SGL_CUDA_CHECK(counts.alloc(nruns));
+    SGL_CUDA_CHECK(offs.alloc(nruns));
+    k_run_starts<<<grid_for(M, T), T, 0, st>>>(head.p, rank.p, M, starts.p);
+    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p, nullptr,
+                                                 nullptr);
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, offs.p, (int)nruns, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, offs.p, (int)nruns, st);
+    }
+    int32_t lc = 0, lo = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&lc, counts.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&lo, offs.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    *ntiles = (int64_t)lc + lo;
+    SGL_CUDA_CHECK(cudaMalloc(tiles, sizeof(Tile) * (*ntiles)));
+    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p, offs.p,
+                                                 *tiles);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
 }  // namespace
 
 int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
@@ -210,91 +302,36 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
             return SGL_EINVAL;
         }
     }
-    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u0, sizeof(double) * (M ? M : 1)));
-    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u1, sizeof(double) * (M ? M : 1)));
-    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.u2, sizeof(double) * (M ? M : 1)));
-    SGL_CUDA_CHECK(cudaMalloc(&p.nodes.perm, sizeof(int32_t) * (M ? M : 1)));
-    if (M == 0) return SGL_OK;
-
-    int W = (4 - (2 * p.q - 1) % 4) % 4;
-    if (W < 2) W += 4;
-    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W, (p.grid[2] + W - 1) / W};
     DevBuf<double> a0, a1, a2;
-    DevBuf<uint64_t> key, key_s;
-    DevBuf<int32_t> idx;
     SGL_CUDA_CHECK(a0.alloc(M));
     SGL_CUDA_CHECK(a1.alloc(M));
     SGL_CUDA_CHECK(a2.alloc(M));
-    SGL_CUDA_CHECK(key.alloc(M));
-    SGL_CUDA_CHECK(key_s.alloc(M));
-    SGL_CUDA_CHECK(idx.alloc(M));
-    k_warp_key<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, kg, a0.p, a1.p, a2.p, key.p, idx.p);
-    SGL_CUDA_CHECK(cudaGetLastError());
-
-    // sort by (pencil, lo0); only the bits in use
-    uint64_t maxkey = (uint64_t)((p.grid[1] + W - 1) / W) * kg.P2 * (uint64_t)p.grid[0];
-    int bits = 1;
-    while (bits < 64 && (1ull << bits) < maxkey) ++bits;
-    {
-        DevBuf<unsigned char> tmp;
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_s.p, idx.p, p.nodes.perm, (int)M, 0, bits,
-                                        st);
-        SGL_CUDA_CHECK(tmp.alloc(tb));
-        cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_s.p, idx.p, p.nodes.perm, (int)M, 0, bits,
-                                        st);
+    if (M > 0) {
+        k_warp<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
         SGL_CUDA_CHECK(cudaGetLastError());
     }
-    k_permute<<<grid_for(M, T), T, 0, st>>>(p.nodes.perm, M, a0.p, a1.p, a2.p, p.nodes.u0, p.nodes.u1,
-                                            p.nodes.u2);
-    SGL_CUDA_CHECK(cudaGetLastError());
-    if (p.generic) return SGL_OK;
-
-    // pencil runs
-    DevBuf<int32_t> head, rank, starts, counts, offs;
-    SGL_CUDA_CHECK(head.alloc(M));
-    SGL_CUDA_CHECK(rank.alloc(M));
-    k_run_heads<<<grid_for(M, T), T, 0, st>>>(key_s.p, M, (uint64_t)p.grid[0], head.p);
-    {
-        DevBuf<unsigned char> tmp;
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, head.p, rank.p, (int)M, st);
-        SGL_CUDA_CHECK(tmp.alloc(tb));
-        cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, rank.p, (int)M, st);
+    // gather order: W x W pencils with 2q - 1 + W == 0 (mod 4) (exact 4-row / 4-column DMMA tiles)
+    int W = (4 - (2 * p.q - 1) % 4) % 4;
+    if (W < 2) W += 4;
+    int rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max},
+                            p.nodes, &p.tiles, &p.n_tiles, !p.generic, st);
+    if (rc || p.generic) return rc;
+    // scatter order: with dense nodes, pencils W x W2 whose axis-2 box is a
+    // multiple of 8 (exact 8-column DMMA tiles, ~17% fewer DMMAs); sparse
+    // node sets keep the gather's W x W pencils, whose wider cross-section
+    // keeps enough nodes per tile to amortise the RED of each box fragment.
+    int W2 = (8 - (2 * p.q - 1) % 8) % 8;
+    if (W2 < 1) W2 += 8;
+    const double cells = (double)p.grid[0] * p.grid[1] * p.grid[2] / 4.0;   // nodes fill axes 0-1 up to pi
+    const double per_row = (double)M / cells * W * W2;                        // nodes per lo0 row of a pencil
+    const TileGeom stg{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max};
+    if (W2 != W && per_row >= 2.5) {
+        rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W2, stg, p.snodes, &p.stiles, &p.n_stiles, true, st);
+    } else {
+        p.snodes_shared = true;
+        p.snodes = p.nodes;
+        rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, stg, p.snodes, &p.stiles, &p.n_stiles, true, st, true);
     }
-    int32_t last_rank = 0, last_head = 0;
-    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_rank, rank.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaMemcpyAsync(&last_head, head.p + M - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-    const int64_t nruns = (int64_t)last_rank + last_head;
-    SGL_CUDA_CHECK(starts.alloc(nruns));
-    SGL_CUDA_CHECK(counts.alloc(nruns));
-    SGL_CUDA_CHECK(offs.alloc(nruns));
-    k_run_starts<<<grid_for(M, T), T, 0, st>>>(head.p, rank.p, M, starts.p);
-    auto build = [&](const TileGeom &tg, Tile **out, int64_t *nout) -> int {
-        k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
-                                                     counts.p, nullptr, nullptr);
-        {
-            DevBuf<unsigned char> tmp;
-            size_t tb = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, offs.p, (int)nruns, st);
-            SGL_CUDA_CHECK(tmp.alloc(tb));
-            cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, offs.p, (int)nruns, st);
-        }
-        int32_t lc = 0, lo = 0;
-        SGL_CUDA_CHECK(cudaMemcpyAsync(&lc, counts.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        SGL_CUDA_CHECK(cudaMemcpyAsync(&lo, offs.p + nruns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-        *nout = (int64_t)lc + lo;
-        SGL_CUDA_CHECK(cudaMalloc(out, sizeof(Tile) * (*nout)));
-        k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, p.nodes.u0, p.nodes.u1, p.nodes.u2, tg,
-                                                     counts.p, offs.p, *out);
-        SGL_CUDA_CHECK(cudaGetLastError());
-        return SGL_OK;
-    };
-    int rc = build(TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max}, &p.tiles, &p.n_tiles);
-    if (rc) return rc;
-    rc = build(TileGeom{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max}, &p.stiles, &p.n_stiles);
     if (rc) return rc;
 
     // tile statistics (host): nodes covered and DMMA count of one gather pass

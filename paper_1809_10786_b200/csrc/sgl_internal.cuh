@@ -75,7 +75,9 @@ struct Plan {
     int device = 0;
 
     WindowParams wp;
-    NodeSet nodes;
+    NodeSet nodes;                // gather order (also the generic kernels)
+    NodeSet snodes;               // scatter order (== nodes when snodes_shared)
+    bool snodes_shared = false;
     Tile *tiles = nullptr;        // gather tiles (<= kTileNodes nodes)
     int64_t n_tiles = 0;
     Tile *stiles = nullptr;       // scatter tiles (<= kSTileNodes nodes)
