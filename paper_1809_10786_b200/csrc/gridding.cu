@@ -2,23 +2,26 @@
 // spreading) on the oversampled grid, FP64, sm_100a.
 //
 // Reference: _gridding.py:53-74 (_gather_kernel), :77-95 (_scatter_kernel)
-// with the wrap padding of :29-50 replaced by modular cell addressing, and
-// the window of nfft.py:123-144:
+// with the wrap padding of :29-50 kept as a resident periodic halo on axes
+// 1-2 (see sgl_internal.cuh) and modular addressing on axis 0, and the
+// window of nfft.py:123-144:
 //     w_j(delta) = (N_j/2pi)/sqrt(2 pi lam_j) * exp(-delta^2/(2 lam_j)),
 //     delta = u_j - cell, zero where |delta| > q.
 //
-// Tiled kernels (q <= 16): a tile is <= 64 sorted nodes whose window boxes
+// Tiled kernels (q <= 16): a tile is a run of sorted nodes (64 for the
+// gather, 128 for the scatter) from one pencil of cells, whose window boxes
 // overlap almost entirely.  Per axis-0 slab of the tile's box the contraction
 // over axis 2 is a real GEMM on the FP64 tensor cores (DMMA m8n8k4):
-//     gather : T[(b,re|im), node] = sum_c G[a,b,c] * W2[c,node]
+//     gather : D[node, (b,re|im)] = sum_c W2[c,node] * G[a,b,c]
 //     scatter: D[(b,re|im), c]    = sum_node V[(b,re|im),node] * W2[c,node]
 // and the axis-1 / axis-0 weights are applied in the epilogue (gather) or
-// folded into V (scatter).  Gather slabs are staged into shared memory by
-// bulk async copies (cp.async.bulk, mbarrier-completed) in a 3-deep ring;
-// scatter fragments are reduced into the grid with RED.ADD.F64.
+// folded into V (scatter).  Gather slabs arrive by TMA (one
+// cp.async.bulk.tensor.3d box per slab) in a 4-deep mbarrier ring fed by a
+// producer warp; scatter fragments are reduced into the grid with
+// RED.E.ADD.F64.
 //
-// Generic kernels (any q, or forced): one warp per node, lanes over axis-2
-// taps, exactly the reference loop nest.
+// Generic kernels (any q, tiny grids, or forced): one warp per node, lanes
+// over axis-2 taps, exactly the reference loop nest.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -92,7 +95,7 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
 // with the W2 fragments resident in registers and the G fragments read from
 // the shared-memory slab, then applies W1[b, node] and W0[a, node].  The
 // producer lane streams one TMA box per slab (cp.async.bulk.tensor.3d, the
-// halo-padded grid needs no wrap on axes 1-2) into a 3-deep ring guarded by
+// halo-padded grid needs no wrap on axes 1-2) into a 4-deep ring guarded by
 // full / empty mbarriers; it walks the CTA's tile sequence on its own, so the
 // next tile's first slabs are in flight while the consumers finish a tile.
 
