@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-sample", type=int, default=4000)
+    ap.add_argument("--direction", default=None, choices=["both", "fwd", "adj"],
+                    help="default: the config's own (3: both, 4: adj, 5: batched fwd)")
     return ap.parse_args()
 
 
@@ -188,7 +190,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     w = workloads.config(args.config, M=args.m, seed=rank)
-    coeffs_h = w.coeffs if w.coeffs.ndim == 1 else w.coeffs[0]
+    direction = args.direction or {"fwd": "fwd", "adj": "adj"}.get(w.directions, "both")
+    coeffs_h = w.coeffs                       # (count,) or (K, count) for the batched config 5
+    K = 1 if coeffs_h.ndim == 1 else coeffs_h.shape[0]
+    if w.values is None:
+        w.values = np.zeros(w.M, dtype=complex)
     pts_d = torch.as_tensor(w.points, device=dev)
     c_d = torch.as_tensor(coeffs_h, device=dev)
     v_d = torch.as_tensor(w.values, device=dev)
@@ -203,10 +209,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step(pl):
-        f = sgl.forward(pl, c_d)
-        a = sgl.adjoint(pl, v_d)
-        if world > 1:   # the adjoint's exchange step (ShardedPlan.adjoint)
-            dist.all_reduce(torch.view_as_real(a))
+        f = a = None
+        if direction in ("both", "fwd"):
+            f = sgl.forward(pl, c_d)
+        if direction in ("both", "adj"):
+            a = sgl.adjoint(pl, v_d)
+            if world > 1:   # the adjoint's exchange step (ShardedPlan.adjoint)
+                dist.all_reduce(torch.view_as_real(a))
         return f, a
 
     # per-kernel timings (CUDA events inside the library, on the launching stream)
@@ -219,8 +228,8 @@ def main():
         torch.cuda.synchronize()
         fw.append(pprof.stage_ms("forward"))
         ad.append(pprof.stage_ms("adjoint"))
-    stages_fwd = {k: statistics.median([d[k] for d in fw]) for k in fw[0]}
-    stages_adj = {k: statistics.median([d[k] for d in ad]) for k in ad[0]}
+    stages_fwd = {k: statistics.median([d[k] for d in fw]) for k in fw[0]} if direction != "adj" else {}
+    stages_adj = {k: statistics.median([d[k] for d in ad]) for k in ad[0]} if direction != "fwd" else {}
     stats = pprof.stats
     pprof.close()
 
@@ -246,7 +255,8 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = world * w.M / (ms / 1e3)
+    units = w.M * (K if direction == "fwd" else 1)   # node evaluations per rank per step
+    value = world * units / (ms / 1e3)
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -255,17 +265,19 @@ def main():
         c_h[:] = coeffs_h
         v_h = torch.empty(w.values.shape, dtype=torch.complex128, pin_memory=True).numpy()
         v_h[:] = w.values
-        fo = torch.empty((w.M,), dtype=torch.complex128, pin_memory=True).numpy()
+        fo = torch.empty((K * w.M,), dtype=torch.complex128, pin_memory=True).numpy()
         ao = torch.empty((p.count,), dtype=torch.complex128, pin_memory=True).numpy()
         L = _native.lib()
 
         def e2e_step():
-            _native.check(L.sgl_forward(p._handle, c_h.ctypes.data, 1, fo.ctypes.data, None))
-            _native.check(L.sgl_adjoint(p._handle, v_h.ctypes.data, ao.ctypes.data, None))
-            if world > 1:
-                t = torch.from_numpy(ao).to(dev)
-                dist.all_reduce(torch.view_as_real(t))
-                ao[:] = t.cpu().numpy()
+            if direction in ("both", "fwd"):
+                _native.check(L.sgl_forward(p._handle, c_h.ctypes.data, K, fo.ctypes.data, None))
+            if direction in ("both", "adj"):
+                _native.check(L.sgl_adjoint(p._handle, v_h.ctypes.data, ao.ctypes.data, None))
+                if world > 1:
+                    t = torch.from_numpy(ao).to(dev)
+                    dist.all_reduce(torch.view_as_real(t))
+                    ao[:] = t.cpu().numpy()
 
         for _ in range(2):
             e2e_step()
@@ -281,17 +293,19 @@ def main():
         if world > 1:
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e_ms = float(e_t.item())
-        e2e = {"value": world * w.M / (e_ms / 1e3), "unit": "nodes/s",
-               "h2d_bytes_per_step": int(c_h.nbytes + v_h.nbytes),
-               "d2h_bytes_per_step": int(fo.nbytes + ao.nbytes), "ms_per_step": e_ms}
+        fw_io, ad_io = direction in ("both", "fwd"), direction in ("both", "adj")
+        e2e = {"value": world * units / (e_ms / 1e3), "unit": "nodes/s",
+               "h2d_bytes_per_step": int(c_h.nbytes * fw_io + v_h.nbytes * ad_io),
+               "d2h_bytes_per_step": int(fo.nbytes * fw_io + ao.nbytes * ad_io), "ms_per_step": e_ms}
 
     # roofline of the dominant kernel (FP64 tensor pipe; algorithmic FLOPs)
     q = 16
     flop_per_node = 4.0 * (2 * q) ** 3     # 2 real FMAs per nonzero tap, (2q)^3 taps
-    kern = {
-        "gather": {"ms": stages_fwd["window"], "flop": w.M * flop_per_node},
-        "scatter": {"ms": stages_adj["window"], "flop": w.M * flop_per_node},
-    }
+    kern = {}
+    if direction in ("both", "fwd"):
+        kern["gather"] = {"ms": stages_fwd["window"] / K, "flop": w.M * flop_per_node}
+    if direction in ("both", "adj"):
+        kern["scatter"] = {"ms": stages_adj["window"], "flop": w.M * flop_per_node}
     for k in kern.values():
         k["tflops"] = k["flop"] / (k["ms"] * 1e-3) / 1e12
         k["frac"] = k["tflops"] / FP64_PEAK_TFLOPS
@@ -317,18 +331,21 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "NFSGLFT nodes/sec fwd+adj at B=64", "value": value, "unit": "nodes/s", "n_gpus": world,
+            "metric": ("NFSGLFT nodes/sec fwd+adj at B=64" if (args.config == 3 and direction == "both")
+                       else f"NFSGLFT nodes/sec {direction} at B={w.B}"),
+            "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded PCG64 inputs of SURVEY 8(d); no public dataset)",
-            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": q, "sigma": 2,
+            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": q, "sigma": 2, "direction": direction,
+                       "vectors": K,
                        "grid": list(p.nfft.grid_shape), "rho": rho,
                        "l2": "inputs larger than L2 (grid 1.07 GB, node arrays 0.28 GB per rank)",
                        "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": 6 * args.steps,
-            "gpu_launches_note": "per step: radial_fwd, sph_fwd, gather_tiled, scatter_tiled, sph_adj, radial_adj "
-                                 "(+ 2 cuFFT executions and 2 memsets, library calls)",
+            "gpu_launches": args.steps * (4 * K * (direction != "adj") + 4 * (direction != "fwd")),
+            "gpu_launches_note": "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled; per adjoint: "
+                                 "scatter_tiled, halo_fold, sph_adj, radial_adj (+ cuFFT and memsets, library calls)",
             "kernels": {k: {"ms": v["ms"], "tflops": v["tflops"], "frac": v["frac"]} for k, v in kern.items()},
             "stages_ms": {"forward": stages_fwd, "adjoint": stages_adj},
             "plan": {"seconds": plan_s, **stats},

@@ -266,6 +266,22 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
     return SGL_OK;
 }
 
+int reorder_tiles(Tile *tiles, int64_t n, cudaStream_t st) {
+    if (n <= 1) return SGL_OK;
+    std::vector<Tile> h(n);
+    SGL_CUDA_CHECK(cudaMemcpyAsync(h.data(), tiles, sizeof(Tile) * n, cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::stable_sort(h.begin(), h.end(), [](const Tile &a, const Tile &b) {
+        const int ba = a.o0 >> 3, bb = b.o0 >> 3;
+        if (ba != bb) return ba < bb;
+        if (a.o1 != b.o1) return a.o1 < b.o1;
+        return a.o2 < b.o2;
+    });
+    SGL_CUDA_CHECK(cudaMemcpyAsync(tiles, h.data(), sizeof(Tile) * n, cudaMemcpyHostToDevice, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    return SGL_OK;
+}
+
 }  // namespace
 
 int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
@@ -332,6 +348,14 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         p.snodes = p.nodes;
         rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, stg, p.snodes, &p.stiles, &p.n_stiles, true, st, true);
     }
+    if (rc) return rc;
+    // L2 locality: CTAs walk the tile list with a grid stride, so the tiles in
+    // flight at any moment are a contiguous stretch of the list.  Ordering the
+    // list by axis-0 band first (then axis 1, axis 2) keeps that stretch inside
+    // a narrow slab band of the grid instead of a few full-length pencils.
+    rc = reorder_tiles(p.tiles, p.n_tiles, st);
+    if (rc) return rc;
+    rc = reorder_tiles(p.stiles, p.n_stiles, st);
     if (rc) return rc;
 
     // tile statistics (host): nodes covered and DMMA count of one gather pass
