@@ -504,32 +504,52 @@ __global__ void k_halo_fill(WindowParams wp, double2 *__restrict__ grid) {
     }
 }
 
-// add the halo images back into the interior (after scatter, before FFT)
+// add the halo images back into the interior (after scatter, before FFT).
+// Only interior cells within q of an axis-1/2 edge have images: thread over
+// that edge set (rows i1 < q or i1 >= N1 - q in full, plus the q-wide column
+// strips of the other rows) instead of the whole plane.
+__device__ __forceinline__ void fold_cell(const WindowParams &wp, double2 *grid, int64_t g0, int i1, int i2) {
+    double2 acc = make_double2(0.0, 0.0);
+    bool any = false;
+    // every padded position p = i + q + k N inside [0, N + 2q), except k = 0 on both axes
+    for (int p1 = (i1 + wp.q) % wp.N1; p1 < wp.N1p; p1 += wp.N1) {
+        for (int p2 = (i2 + wp.q) % wp.N2; p2 < wp.N2p; p2 += wp.N2) {
+            if (p1 == i1 + wp.q && p2 == i2 + wp.q) continue;
+            const double2 v = grid[((size_t)g0 * wp.N1p + p1) * wp.N2p + p2];
+            acc.x += v.x;
+            acc.y += v.y;
+            any = true;
+        }
+    }
+    if (any) {
+        double2 &dst = grid[((size_t)g0 * wp.N1p + i1 + wp.q) * wp.N2p + i2 + wp.q];
+        dst.x += acc.x;
+        dst.y += acc.y;
+    }
+}
+
 __global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
-    const int64_t n = (int64_t)wp.N0 * wp.N1 * wp.N2;
+    const int q1 = min(wp.q, wp.N1), q2 = min(wp.q, wp.N2);
+    const int band_rows = min(wp.N1, 2 * q1);              // rows [0,q) and [N1-q, N1)
+    const int strip = min(wp.N2, 2 * q2);                   // columns [0,q) and [N2-q, N2)
+    const int64_t per_plane = (int64_t)band_rows * wp.N2 + (int64_t)(wp.N1 - band_rows) * strip;
+    const int64_t n = (int64_t)wp.N0 * per_plane;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int i2 = (int)(i % wp.N2);
-        const int64_t r = i / wp.N2;
-        const int i1 = (int)(r % wp.N1);
-        const int64_t g0 = r / wp.N1;
-        if (i1 >= wp.q && i1 < wp.N1 - wp.q && i2 >= wp.q && i2 < wp.N2 - wp.q) continue;   // no images
-        double2 acc = make_double2(0.0, 0.0);
-        bool any = false;
-        // every padded position p = i + q + k N inside [0, N + 2q), except k = 0 on both axes
-        for (int p1 = (i1 + wp.q) % wp.N1; p1 < wp.N1p; p1 += wp.N1) {
-            for (int p2 = (i2 + wp.q) % wp.N2; p2 < wp.N2p; p2 += wp.N2) {
-                if (p1 == i1 + wp.q && p2 == i2 + wp.q) continue;
-                const double2 v = grid[((size_t)g0 * wp.N1p + p1) * wp.N2p + p2];
-                acc.x += v.x;
-                acc.y += v.y;
-                any = true;
-            }
+        const int64_t g0 = i / per_plane;
+        int64_t r = i - g0 * per_plane;
+        int i1, i2;
+        if (r < (int64_t)band_rows * wp.N2) {
+            const int k = (int)(r / wp.N2);
+            i1 = k < q1 ? k : wp.N1 - band_rows + k;
+            i2 = (int)(r - (int64_t)k * wp.N2);
+        } else {
+            r -= (int64_t)band_rows * wp.N2;
+            const int k = (int)(r / strip);
+            i1 = q1 + k;
+            const int c = (int)(r - (int64_t)k * strip);
+            i2 = c < q2 ? c : wp.N2 - strip + c;
         }
-        if (any) {
-            double2 &dst = grid[((size_t)g0 * wp.N1p + i1 + wp.q) * wp.N2p + i2 + wp.q];
-            dst.x += acc.x;
-            dst.y += acc.y;
-        }
+        fold_cell(wp, grid, g0, i1, i2);
     }
 }
 
