@@ -50,7 +50,7 @@ enum {
 /* plan flags */
 enum {
     SGL_FLAG_COMPACT_K1 = 1u << 0,        /* compact_k1=True (transform.py:350)     */
-    SGL_FLAG_EXACT_LAST_STAGE = 1u << 1,  /* exact_last_stage=True: rejected        */
+    SGL_FLAG_EXACT_LAST_STAGE = 1u << 1,  /* exact_last_stage=True: direct NDFT      */
     SGL_FLAG_GENERIC_GRIDDING = 1u << 2,  /* force the per-node window kernels      */
     SGL_FLAG_PROFILE = 1u << 3            /* record per-stage CUDA-event timings    */
 };
@@ -71,6 +71,7 @@ typedef struct {
     int64_t tile_nodes;       /* nodes covered by tiles                        */
     int64_t tile_dmma;        /* DMMA m8n8k4 issued per gather pass            */
     int32_t generic;          /* 1 if the per-node window kernels are used     */
+    int32_t exact;            /* 1 for exact_last_stage plans (direct NDFT)    */
     double plan_ms;           /* device time of plan construction              */
 } sgl_plan_info;
 

@@ -43,6 +43,7 @@ class PlanInfo(ctypes.Structure):
         ("tile_nodes", ctypes.c_int64),
         ("tile_dmma", ctypes.c_int64),
         ("generic", ctypes.c_int32),
+        ("exact", ctypes.c_int32),
         ("plan_ms", ctypes.c_double),
     ]
 

@@ -138,21 +138,24 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         set_error("more than 2^31-1 points per plan: shard the node set");
         return SGL_EUNSUPPORTED;
     }
-    if (flags & SGL_FLAG_EXACT_LAST_STAGE) {
-        set_error("exact_last_stage=True is not provided by the B200 backend");
-        return SGL_EUNSUPPORTED;
-    }
-    if (q < 1) {
-        set_error("cutoff parameter q must be >= 1");
-        return SGL_EINVAL;
-    }
-    if (sigma < 2) {
-        set_error("oversampling factor must be an integer >= 2");
-        return SGL_EINVAL;
-    }
-    if ((int64_t)q >= 4LL * sigma * B) {
-        set_error("cutoff q = " + std::to_string(q) + " must be below 4*sigma*B = " + std::to_string(4LL * sigma * B));
-        return SGL_EINVAL;
+    const bool exact = flags & SGL_FLAG_EXACT_LAST_STAGE;
+    if (!exact) {   // the window parameters are only checked for the fast path (transform.py:352-356)
+        if (q < 1) {
+            set_error("cutoff parameter q must be >= 1");
+            return SGL_EINVAL;
+        }
+        if (sigma < 2) {
+            set_error("oversampling factor must be an integer >= 2");
+            return SGL_EINVAL;
+        }
+        if ((int64_t)q >= 4LL * sigma * B) {
+            set_error("cutoff q = " + std::to_string(q) + " must be below 4*sigma*B = " +
+                      std::to_string(4LL * sigma * B));
+            return SGL_EINVAL;
+        }
+    } else {
+        q = 0;
+        sigma = 1;
     }
     auto t0 = std::chrono::steady_clock::now();
     Plan *p = new Plan();
@@ -165,7 +168,8 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->q = q;
     p->compact = flags & SGL_FLAG_COMPACT_K1;
     p->profile = flags & SGL_FLAG_PROFILE;
-    p->generic = (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
+    p->exact = exact;
+    p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
     p->n_axis[2] = 2 * B;
@@ -178,6 +182,13 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
             while (g < v) g <<= 1;
             return g;
         };
+        if (exact) {   // eta on I_n itself: no oversampling, no window
+            p->sig_axes[ax] = 1;
+            p->grid[ax] = p->n_axis[ax];
+            p->s_eff[ax] = 1.0;
+            p->lam[ax] = 0.0;
+            continue;
+        }
         while (pow2((int64_t)s * p->n_axis[ax]) <= q) s *= 2;
         p->sig_axes[ax] = s;
         p->grid[ax] = (int)pow2((int64_t)s * p->n_axis[ax]);
@@ -197,6 +208,10 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
+        if (exact) {
+            *cs[ax] = *hs[ax] = 0.0;
+            continue;
+        }
         const double N = p->grid[ax], a = N / kTwoPi, lam = p->lam[ax];
         *cs[ax] = a / std::sqrt(kTwoPi * lam);                          // nfft.py:137
         *hs[ax] = ((kTwoPi / N) * (kTwoPi / N)) * (a * a) / (2.0 * lam);  // nfft.py:138
@@ -232,7 +247,7 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
             rc = SGL_ENOMEM;
         }
     }
-    if (rc == SGL_OK) {
+    if (rc == SGL_OK && !exact) {
         // transform the interior of the halo-padded grid in place
         int n[3] = {p->grid[0], p->grid[1], p->grid[2]};
         int emb[3] = {wp.N0, wp.N1p, wp.N2p};
@@ -240,7 +255,7 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         rc = fft_check(cufftPlanMany(&p->fft, 3, n, emb, 1, dist, emb, 1, dist, CUFFT_Z2Z, 1), "cufftPlanMany");
         if (rc == SGL_OK) p->fft_ready = true;
     }
-    if (rc == SGL_OK && !p->generic) rc = make_grid_tmap(*p);
+    if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && p->profile) {
         for (auto &t : p->timers) {
             for (auto &e : t.ev) cudaEventCreate(&e);
@@ -295,6 +310,7 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->tile_nodes = p.tile_nodes;
     info->tile_dmma = p.tile_dmma;
     info->generic = p.generic ? 1 : 0;
+    info->exact = p.exact ? 1 : 0;
     info->plan_ms = p.plan_ms;
     return SGL_OK;
 }
@@ -334,19 +350,25 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
         rec.mark(SGL_STAGE_BASAL);
         int rc = launch_basal_forward(p, c, p.grid_buf, st, nullptr);
         if (rc) return rc;
-        rec.mark(SGL_STAGE_FFT);
-        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-        if (rc) return rc;
-        cufftDoubleComplex *interior =
-            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
-        if (rc) return rc;
-        rc = launch_halo_fill(p, p.grid_buf, st);
-        if (rc) return rc;
-        rec.mark(SGL_STAGE_WINDOW);
         double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : p.val_buf;
-        rc = launch_gather(p, p.grid_buf, v, st);
-        if (rc) return rc;
+        if (p.exact) {   // direct NDFT of eta (transform.py:393-394)
+            rec.mark(SGL_STAGE_WINDOW);
+            rc = launch_exact_forward(p, p.grid_buf, v, st);
+            if (rc) return rc;
+        } else {
+            rec.mark(SGL_STAGE_FFT);
+            rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+            if (rc) return rc;
+            cufftDoubleComplex *interior =
+                reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+            rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
+            if (rc) return rc;
+            rc = launch_halo_fill(p, p.grid_buf, st);
+            if (rc) return rc;
+            rec.mark(SGL_STAGE_WINDOW);
+            rc = launch_gather(p, p.grid_buf, v, st);
+            if (rc) return rc;
+        }
         rec.mark(SGL_STAGE_D2H);
         if (!vdev && p.M > 0)
             SGL_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<double2 *>(values) + k * p.M, p.val_buf,
@@ -381,17 +403,24 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
         v = p.val_buf;
     }
     rec.mark(SGL_STAGE_WINDOW);
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    int rc = launch_scatter(p, v, p.grid_buf, st);
-    if (rc) return rc;
-    rec.mark(SGL_STAGE_FFT);
-    rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-    if (rc) return rc;
-    rc = launch_halo_fold(p, p.grid_buf, st);
-    if (rc) return rc;
-    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-    rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
-    if (rc) return rc;
+    int rc = SGL_OK;
+    if (p.exact) {   // direct adjoint NDFT (transform.py:404-405)
+        rc = launch_exact_adjoint(p, v, p.grid_buf, st);
+        if (rc) return rc;
+    } else {
+        SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+        rc = launch_scatter(p, v, p.grid_buf, st);
+        if (rc) return rc;
+        rec.mark(SGL_STAGE_FFT);
+        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+        if (rc) return rc;
+        rc = launch_halo_fold(p, p.grid_buf, st);
+        if (rc) return rc;
+        cufftDoubleComplex *interior =
+            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
+        if (rc) return rc;
+    }
     rec.mark(SGL_STAGE_BASAL);
     double2 *c = cdev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;
     rc = launch_basal_adjoint(p, p.grid_buf, c, st);

@@ -65,6 +65,7 @@ struct Plan {
     int sigma = 2, q = 16;
     bool compact = false;
     bool generic = false;
+    bool exact = false;           // exact last stage: direct NDFT on I_n (no window, no FFT)
     bool profile = false;
     int n_axis[3];
     int grid[3];
@@ -132,6 +133,8 @@ int launch_basal_forward(const Plan &p, const double2 *coeffs, double2 *grid, cu
                          cudaEvent_t mid);
 int launch_basal_adjoint(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
 int make_grid_tmap(Plan &p);
+int launch_exact_forward(const Plan &p, const double2 *eta, double2 *values, cudaStream_t st);
+int launch_exact_adjoint(const Plan &p, const double2 *values, double2 *eta, cudaStream_t st);
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
 

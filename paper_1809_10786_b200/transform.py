@@ -64,7 +64,7 @@ class SglPlan:
     compact_k1: bool
     points: object
     n_axis: tuple
-    nfft: NfftInfo
+    nfft: NfftInfo | None
     device: int
     _handle: int = field(repr=False)
     _info: _native.PlanInfo = field(repr=False)
@@ -128,8 +128,8 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     otherwise), "tiled", "generic" (per-node kernels).  The reference names
     "numba" / "numpy" are accepted as aliases of "auto".  ``precompute`` is
     accepted for compatibility: window weights are always evaluated on the
-    fly on the device.  ``exact_last_stage=True`` raises ValueError (the exact
-    NDFT is not part of the B200 path)."""
+    fly on the device.  ``exact_last_stage=True`` replaces the window
+    evaluation by the direct NDFT on the device (O(M n^3): verification)."""
     if B < 1:
         raise ValueError("bandwidth must be >= 1")
     if backend not in _BACKENDS:
@@ -153,18 +153,19 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         dev = device
     if rho is not None and not rho > 0:
         raise ValueError("rho must be positive")
-    if exact_last_stage:
-        raise ValueError("exact_last_stage=True is not provided by the B200 backend")
-    if q is None or q < 1:
-        raise ValueError("cutoff parameter q must be >= 1")
-    if q >= 4 * sigma * B:
-        raise ValueError(f"cutoff q = {q} must be below 4*sigma*B = {4 * sigma * B}")
-    if backend == "tiled" and q > 16:
-        raise ValueError("tiled window kernels need q <= 16")
+    if not exact_last_stage:   # window parameters only matter for the fast path (transform.py:352-356)
+        if q is None or q < 1:
+            raise ValueError("cutoff parameter q must be >= 1")
+        if q >= 4 * sigma * B:
+            raise ValueError(f"cutoff q = {q} must be below 4*sigma*B = {4 * sigma * B}")
+        if backend == "tiled" and q > 16:
+            raise ValueError("tiled window kernels need q <= 16")
     L = _native.lib()
     if dev is not None:
         _native.check(L.sgl_set_device(int(dev)))
     flags = 0
+    if exact_last_stage:
+        flags |= _native.FLAG_EXACT_LAST_STAGE
     if compact_k1:
         flags |= _native.FLAG_COMPACT_K1
     if backend == "generic":
@@ -173,13 +174,15 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_PROFILE
     h = ctypes.c_void_p(0)
     stream = _stream_ptr(pts)
-    _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q),
+    _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q or 0),
                                     float(rho) if rho is not None else 0.0, flags, stream, ctypes.byref(h)))
     info = _native.PlanInfo()
     _native.check(L.sgl_plan_get_info(h, ctypes.byref(info)))
-    nf = NfftInfo(3, tuple(info.n_axis), tuple(info.sigma_axes), int(q), tuple(info.grid),
-                  tuple(info.sigma_eff), tuple(info.lam), "generic" if info.generic else "tiled")
-    return SglPlan(B=int(B), rho=float(info.rho), sigma=int(sigma), q=int(q), exact=False,
+    nf = None if exact_last_stage else NfftInfo(
+        3, tuple(info.n_axis), tuple(info.sigma_axes), int(q), tuple(info.grid), tuple(info.sigma_eff),
+        tuple(info.lam), "generic" if info.generic else "tiled")
+    return SglPlan(B=int(B), rho=float(info.rho), sigma=int(sigma), q=None if exact_last_stage else int(q),
+                   exact=bool(exact_last_stage),
                    compact_k1=bool(compact_k1), points=points, n_axis=tuple(info.n_axis), nfft=nf,
                    device=int(dev) if dev is not None else 0, _handle=h.value, _info=info)
 

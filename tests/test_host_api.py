@@ -18,7 +18,6 @@ def pts(n=5, r=1.0):
     (dict(B=4, q=None), "cutoff parameter q"),
     (dict(B=4, rho=0.0), "rho must be positive"),
     (dict(B=4, rho=-1.0), "rho must be positive"),
-    (dict(B=4, exact_last_stage=True), "exact_last_stage"),
     (dict(B=4, backend="fortran"), "backend"),
     (dict(B=4, q=20, backend="tiled"), "q <= 16"),
 ])

@@ -40,7 +40,6 @@ def test_version_and_device_count():
     (4, 1, 2, 0, 0, "cutoff parameter q must be >= 1"),
     (2, 1, 2, 16, 0, "cutoff q = 16 must be below 4*sigma*B = 16"),
     (4, 1, 1, 4, 0, "oversampling factor must be an integer >= 2"),
-    (4, 1, 2, 4, _native.FLAG_EXACT_LAST_STAGE, "exact_last_stage"),
 ])
 def test_plan_create_rejects_like_reference(B, M, sigma, q, flags, msg):
     lib = _native.lib()

@@ -197,3 +197,56 @@ def test_config4_full_size_adjoint(sgl):
     a = sgl.adjoint(p, v)
     assert np.all(np.isfinite(a))
     assert rel(a, g["adj"]) <= TOL_CFG4, rel(a, g["adj"])
+
+
+# --- exact last stage (transform.py:393-394, 404-405): direct NDFT on device ---
+
+@pytest.mark.parametrize("B", [1, 2, 4, 8])
+def test_exact_stage_matches_direct_sums(sgl, B):
+    # reference test_transform.py:215-223, with the direct sums of the oracle
+    from oracle import sgl_oracle as o
+    rng = np.random.default_rng(10 + B)
+    c = sgl.gen_coeffs(B, rng)
+    pts = sgl.gen_points_ball(25, 3.0, rng)
+    p = sgl.plan(B, pts, exact_last_stage=True)
+    assert p.exact and p.q is None and p.nfft is None
+    ref = o.evaluate_direct(c, B, pts)
+    assert rel(sgl.forward(p, c), ref) <= 1e-10
+
+
+def test_exact_stage_adjoint_and_pairing(sgl):
+    # reference test_transform.py:296-315
+    from oracle import sgl_oracle as o
+    rng = np.random.default_rng(31)
+    B, m = 6, 50
+    pts = sgl.gen_points_ball(m, 3.0, rng)
+    v = rng.normal(size=m) + 1j * rng.normal(size=m)
+    p = sgl.plan(B, pts, exact_last_stage=True)
+    assert rel(sgl.adjoint(p, v), o.evaluate_direct_adjoint(v, B, pts)) <= 1e-9
+    x = sgl.gen_coeffs(B, rng)
+    lhs = np.vdot(v, sgl.forward(p, x))
+    rhs = np.vdot(sgl.adjoint(p, v), x)
+    assert abs(lhs - rhs) <= 1e-11 * np.linalg.norm(x) * np.linalg.norm(v)
+
+
+def test_exact_compact_grid_agrees(sgl):
+    # reference test_transform.py:265-272
+    rng = np.random.default_rng(23)
+    B = 4
+    c = sgl.gen_coeffs(B, rng)
+    pts = sgl.gen_points_ball(40, 2.5, rng)
+    ref = sgl.forward(sgl.plan(B, pts, exact_last_stage=True), c)
+    out = sgl.forward(sgl.plan(B, pts, exact_last_stage=True, compact_k1=True), c)
+    assert rel(out, ref) <= 1e-11
+
+
+def test_fast_vs_exact_stage_window_error(sgl):
+    # the fast path deviates from the exact stage only by the window error,
+    # which decays in q (test_transform.py:225-252)
+    rng = np.random.default_rng(20)
+    B = 8
+    c = sgl.gen_coeffs(B, rng)
+    pts = sgl.gen_points_ball(300, 5.0, rng)
+    exact = sgl.forward(sgl.plan(B, pts, exact_last_stage=True), c)
+    errs = {q: rel(sgl.forward(sgl.plan(B, pts, q=q), c), exact) for q in (4, 8, 12, 16)}
+    assert errs[16] <= 1e-4 * errs[4] and errs[16] <= 1e-9
