@@ -20,8 +20,9 @@
  * (CUDA) memory; the library detects which.  Host outputs are complete when
  * the call returns; device outputs are complete in stream order.
  *
- * Calls on one plan must be serialised (the plan owns its scratch grid),
- * unlike the CPU reference's "share across threads" (README.md:66-67).
+ * A plan may be shared by host threads and streams like the reference's
+ * (README.md:66-67): calls on one plan are serialised by a mutex and by
+ * stream-ordering on the previous call (the plan owns its scratch grid).
  */
 #ifndef SGL_B200_H
 #define SGL_B200_H

@@ -52,12 +52,25 @@ void free_plan(Plan *p) {
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
+    if (p->done) cudaEventDestroy(p->done);
     for (auto &t : p->timers)
         if (t.ready)
             for (auto &e : t.ev) cudaEventDestroy(e);
     cudaSetDevice(cur);
     delete p;
 }
+
+struct PlanGuard {
+    Plan &p;
+    cudaStream_t st;
+    std::lock_guard<std::mutex> lock;
+    PlanGuard(Plan &pl, cudaStream_t s) : p(pl), st(s), lock(pl.mu) {
+        if (p.done) cudaStreamWaitEvent(st, p.done, 0);
+    }
+    ~PlanGuard() {
+        if (p.done) cudaEventRecord(p.done, st);
+    }
+};
 
 struct StageRec {
     // events recorded in call order; slot i..i+1 is charged to stage_of[i]
@@ -256,6 +269,10 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         if (rc == SGL_OK) p->fft_ready = true;
     }
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
+    if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
+        set_error("cudaEventCreate failed");
+        rc = SGL_ECUDA;
+    }
     if (rc == SGL_OK && p->profile) {
         for (auto &t : p->timers) {
             for (auto &e : t.ev) cudaEventCreate(&e);
@@ -333,6 +350,7 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
     }
     Plan &p = *reinterpret_cast<Plan *>(plan);
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    PlanGuard guard(p, (cudaStream_t)stream);
     if (K < 1 || !coeffs || (!values && p.M > 0)) {
         set_error("coefficient length does not match the bandwidth");
         return SGL_EINVAL;
@@ -389,6 +407,7 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
     }
     Plan &p = *reinterpret_cast<Plan *>(plan);
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    PlanGuard guard(p, (cudaStream_t)stream);
     if (!coeffs || (!values && p.M > 0)) {
         set_error("values length does not match the plan");
         return SGL_EINVAL;

@@ -6,6 +6,7 @@
 #include <cufft.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -110,6 +111,12 @@ struct Plan {
 
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
+
+    // Calls on a plan are serialised across host threads (mutex) and across
+    // CUDA streams (each call's stream waits for the previous call's event),
+    // so a plan can be shared like the reference's (README.md:66-67).
+    std::mutex mu;
+    cudaEvent_t done = nullptr;
 };
 
 // error state

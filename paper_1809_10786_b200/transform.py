@@ -53,9 +53,8 @@ class SglPlan:
     """Per-point-set plan; owns the device state of libsgl_b200 (sorted nodes,
     window tiles, basal matrices, cuFFT plan, scratch grid).
 
-    Calls on one plan are serialised by the plan's scratch buffers; use one
-    plan per concurrent stream (the reference plan is shareable across
-    threads, README.md:66-67)."""
+    Shareable across threads and streams like the reference's plan
+    (README.md:66-67): the library serialises calls on one plan."""
     B: int
     rho: float
     sigma: int

@@ -250,3 +250,29 @@ def test_fast_vs_exact_stage_window_error(sgl):
     exact = sgl.forward(sgl.plan(B, pts, exact_last_stage=True), c)
     errs = {q: rel(sgl.forward(sgl.plan(B, pts, q=q), c), exact) for q in (4, 8, 12, 16)}
     assert errs[16] <= 1e-4 * errs[4] and errs[16] <= 1e-9
+
+
+def test_plan_shared_across_threads(sgl):
+    """Concurrent forward/adjoint calls on one plan from several host threads
+    (the reference's plans are shareable, README.md:66-67)."""
+    import threading
+    g = load_golden("b12_q12")
+    p = sgl.plan(12, g["points"], q=12, rho=float(g["rho"]))
+    res, errs = {}, []
+
+    def work(k):
+        try:
+            for _ in range(5):
+                res[("f", k)] = sgl.forward(p, g["coeffs"])
+                res[("a", k)] = sgl.adjoint(p, g["values"])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for k in range(4):
+        assert rel(res[("f", k)], g["fwd"]) <= TOL and rel(res[("a", k)], g["adj"]) <= TOL
