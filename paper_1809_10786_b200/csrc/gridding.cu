@@ -107,6 +107,7 @@ constexpr int SSTR = kBoxMax;         // TMA box width in complex (== 4 mod 8: c
 static_assert(SSTR % 8 == 4, "slab row stride must be 4 mod 8 complex");
 constexpr int KSMAX = kBoxMax / 4;    // k-steps over axis 2
 constexpr int NTMAX = kBoxMax / 4;    // 4-row (8 re|im column) tiles over axis 1
+static_assert(NTMAX % 3 == 0, "gather N-tile loop runs in groups of 3");
 constexpr uint32_t SLAB_BYTES = SROWS * SSTR * 16;
 
 struct GatherSmem {
@@ -225,30 +226,26 @@ __global__ void __launch_bounds__(GT, 2)
             if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
                 const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
                 double s_re = 0.0, s_im = 0.0;
+                // fixed 9 x 9 fragment loops with no predicates around the DMMAs
+                // (a .sync.aligned MMA under a runtime guard costs a WARPSYNC,
+                // a branch and a NOP each): fragments beyond the tile's box have
+                // zero W1 / W2 weights and multiply finite smem data
 #pragma unroll
                 for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
-                    if (nt0 < Mt) {
-                        double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+                    double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-                        for (int ks = 0; ks < KSMAX; ++ks) {
-                            if (ks < KS) {
-#pragma unroll
-                                for (int i = 0; i < 3; ++i) {
-                                    if (nt0 + i < NTMAX && nt0 + i < Mt) {
-                                        const int b = (nt0 + i) * 4 + rb;
-                                        const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
-                                        dmma(d[i], afr[ks], bv);
-                                    }
-                                }
-                            }
-                        }
+                    for (int ks = 0; ks < KSMAX; ++ks) {
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
-                            if (nt0 + i < NTMAX && nt0 + i < Mt) {
-                                s_re = fma(w1r[nt0 + i], d[i][0], s_re);
-                                s_im = fma(w1r[nt0 + i], d[i][1], s_im);
-                            }
+                            const int b = (nt0 + i) * 4 + rb;
+                            const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
+                            dmma(d[i], afr[ks], bv);
                         }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        s_re = fma(w1r[nt0 + i], d[i][0], s_re);
+                        s_im = fma(w1r[nt0 + i], d[i][1], s_im);
                     }
                 }
                 acc_re = fma(w0, s_re, acc_re);
@@ -291,6 +288,8 @@ constexpr int SKS = SN / 4;           // node k-steps
 static_assert(CTMAX * 8 >= kBoxMax, "scatter column tiles must cover the box");
 static_assert(KSMAX * 4 >= kBoxMax && NTMAX * 4 >= kBoxMax, "gather tiles must cover the box");
 static_assert(SN == 128, "the active-k-step mask below assumes 4 x 32 nodes");
+static_assert(CTMAX == 5 && kBoxMax > 32, "scatter column tiles: 4 (box <= 32) or 5 (box <= 40)");
+static_assert(((kBoxMax / 4 + SMT - 1) / SMT) * SMT * 4 <= kBoxMax, "padded M-tile groups fit the W1 table");
 
 struct ScatterSmem {
     double w1[kBoxMax][WS];
@@ -301,13 +300,58 @@ struct ScatterSmem {
     Tile t;
 };
 
+// One group of SMT four-row M-tiles x NCT eight-column tiles of slab a,
+// accumulated over the active node k-steps, then reduced into the grid.
+// NCT is a template parameter so no runtime predicate sits around a DMMA.
+template <int NCT>
+__device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double *w0row, int mt0, int ks0, int ks1,
+                                              int g0, const Tile &t, const WindowParams &wp, double *grid,
+                                              int lane) {
+    const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
+    double d[SMT][NCT][2];
+#pragma unroll
+    for (int i = 0; i < SMT; ++i)
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
+#pragma unroll 2
+    for (int ks = ks0; ks < ks1; ++ks) {
+        const int n = ks * 4 + kk;
+        const double2 v = S.v[n];
+        const double wv = w0row[n] * (part ? v.y : v.x);
+        double av[SMT];
+#pragma unroll
+        for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct) {
+            const double bv = S.w2[ct * 8 + cr][n];
+#pragma unroll
+            for (int i = 0; i < SMT; ++i) dmma(d[i][ct], av[i], bv);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < SMT; ++i) {
+        const int b = (mt0 + i) * 4 + rb;
+        if (b < t.e1) {
+            // halo-padded grid: rows / columns of the box never wrap
+            double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int c = ct * 8 + 2 * kk + j;
+                    if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(STH, 2)
     k_scatter_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
                     const double2 *__restrict__ values, double *__restrict__ grid) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
     double *w0row = S.w0[warp];
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
@@ -326,7 +370,8 @@ __global__ void __launch_bounds__(STH, 2)
         __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
         const int CT = (t.e2 + 7) >> 3;
-        for (int i = tid; i < Mt * 4 * SN; i += STH) {
+        // every row up to the groups' extent (formula gives 0 outside the box)
+        for (int i = tid; i < ((Mt + SMT - 1) / SMT) * SMT * 4 * SN; i += STH) {
             const int y = i / SN, k = i % SN;
             S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
         }
@@ -354,47 +399,10 @@ __global__ void __launch_bounds__(STH, 2)
             const int ks0 = kfirst, ks1 = min(nks, klast + 1);
             const int g0 = wrapi(t.o0 + a, wp.N0);
             for (int mt0 = 0; mt0 < Mt; mt0 += SMT) {
-                double d[SMT][CTMAX][2];
-#pragma unroll
-                for (int i = 0; i < SMT; ++i)
-#pragma unroll
-                    for (int ct = 0; ct < CTMAX; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
-#pragma unroll 2
-                for (int ks = ks0; ks < ks1; ++ks) {
-                    const int n = ks * 4 + kk;
-                    const double2 v = S.v[n];
-                    const double wv = w0row[n] * (part ? v.y : v.x);
-                    double av[SMT];
-#pragma unroll
-                    for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
-#pragma unroll
-                    for (int ct = 0; ct < CTMAX; ++ct) {
-                        if (ct < CT) {
-                            const double bv = S.w2[ct * 8 + cr][n];
-#pragma unroll
-                            for (int i = 0; i < SMT; ++i)
-                                if (mt0 + i < Mt) dmma(d[i][ct], av[i], bv);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < SMT; ++i) {
-                    const int b = (mt0 + i) * 4 + rb;
-                    if (mt0 + i < Mt && b < t.e1) {
-                        // halo-padded grid: rows / columns of the box never wrap
-                        double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
-#pragma unroll
-                        for (int ct = 0; ct < CTMAX; ++ct) {
-                            if (ct < CT) {
-#pragma unroll
-                                for (int j = 0; j < 2; ++j) {
-                                    const int c = ct * 8 + 2 * kk + j;
-                                    if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
-                                }
-                            }
-                        }
-                    }
-                }
+                if (CT == CTMAX)
+                    scatter_group<CTMAX>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
+                else
+                    scatter_group<CTMAX - 1>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
             }
             __syncwarp();   // w0row is rewritten for the warp's next slab
         }
