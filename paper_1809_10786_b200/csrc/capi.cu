@@ -262,11 +262,17 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     }
     if (rc == SGL_OK && !exact) {
         // transform the interior of the halo-padded grid in place
-        int n[3] = {p->grid[0], p->grid[1], p->grid[2]};
-        int emb[3] = {wp.N0, wp.N1p, wp.N2p};
-        const int dist = (int)std::min<size_t>(p->grid_elems, (size_t)INT32_MAX);
-        rc = fft_check(cufftPlanMany(&p->fft, 3, n, emb, 1, dist, emb, 1, dist, CUFFT_Z2Z, 1), "cufftPlanMany");
-        if (rc == SGL_OK) p->fft_ready = true;
+        // 64-bit plan: the padded grid exceeds 2^31 elements from B = 256 on
+        long long n[3] = {p->grid[0], p->grid[1], p->grid[2]};
+        long long emb[3] = {wp.N0, wp.N1p, wp.N2p};
+        const long long dist = (long long)p->grid_elems;
+        size_t work = 0;
+        rc = fft_check(cufftCreate(&p->fft), "cufftCreate");
+        if (rc == SGL_OK) {
+            p->fft_ready = true;
+            rc = fft_check(cufftMakePlanMany64(p->fft, 3, n, emb, 1, dist, emb, 1, dist, CUFFT_Z2Z, 1, &work),
+                           "cufftMakePlanMany64");
+        }
     }
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
