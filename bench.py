@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--m", type=int, default=None, help="override the node count per rank")
+    ap.add_argument("--points", type=int, default=None, help="override the node count per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-sample", type=int, default=4000)
@@ -147,7 +147,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_1809_10786_b200 import workloads
-    w = workloads.config(args.config, M=args.m)
+    w = workloads.config(args.config, M=args.points)
     steps = max(1, min(args.steps, 3))
     vals = []
     base = None
@@ -185,11 +185,20 @@ def main():
     from paper_1809_10786_b200 import _native, workloads
     from paper_1809_10786_b200.distributed import ShardedPlan
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # test hooks: SGL_BENCH_DEVICE pins every rank to one GPU and
+    # SGL_BENCH_BACKEND=gloo replaces NCCL, so the multi-rank logic can be
+    # exercised on a single-GPU box (never used for reported numbers)
+    gpu = int(os.environ.get("SGL_BENCH_DEVICE", local))
+    backend = os.environ.get("SGL_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    local = gpu
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    w = workloads.config(args.config, M=args.m, seed=rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    w = workloads.config(args.config, M=args.points, seed=rank)
     direction = args.direction or {"fwd": "fwd", "adj": "adj"}.get(w.directions, "both")
     coeffs_h = w.coeffs                       # (count,) or (K, count) for the batched config 5
     K = 1 if coeffs_h.ndim == 1 else coeffs_h.shape[0]
