@@ -93,15 +93,16 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
 // producer warp.  Per box slab a (axis 0), consumer warp w computes
 //     D[node, (b, re|im)] = sum_c W2[c, node] * G[a, b, c]       (DMMA)
 // with the W2 fragments resident in registers and the G fragments read from
-// the shared-memory slab, then applies W1[b, node] and W0[a, node].  The
+// the shared-memory slab, then applies W1[b, node] (registers) and W0[a, node]
+// (a per-thread recurrence along the slabs).  The
 // producer lane streams one TMA box per slab (cp.async.bulk.tensor.3d, the
-// halo-padded grid needs no wrap on axes 1-2) into a 4-deep ring guarded by
+// halo-padded grid needs no wrap on axes 1-2) into a 5-deep ring guarded by
 // full / empty mbarriers; it walks the CTA's tile sequence on its own, so the
 // next tile's first slabs are in flight while the consumers finish a tile.
 
 constexpr int GCW = kTileNodes / 8;   // consumer warps
 constexpr int GT = (GCW + 1) * 32;    // + producer warp
-constexpr int NST = 4;                // slab ring depth
+constexpr int NST = 5;                // slab ring depth
 constexpr int SROWS = kBoxMax;        // TMA box rows (axis 1)
 constexpr int SSTR = kBoxMax;         // TMA box width in complex (== 4 mod 8: conflict-free B reads)
 static_assert(SSTR % 8 == 4, "slab row stride must be 4 mod 8 complex");
@@ -112,7 +113,6 @@ constexpr uint32_t SLAB_BYTES = SROWS * SSTR * 16;
 
 struct GatherSmem {
     double2 slab[NST][SROWS * SSTR];
-    double w0[kBox0Max][kTileNodes];
     double nu[3][kTileNodes];
     uint64_t full[NST];
     uint64_t empty[NST];
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(GT, 2)
     const int rb = lane >> 3, part = (lane >> 2) & 1;
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        consumers_sync();   // previous tile's readers of S.t / S.nu / S.w0 are done
+        consumers_sync();   // previous tile's readers of S.t / S.nu are done
         if (tid == 0) S.t = tiles[ti];
         consumers_sync();
         const Tile t = S.t;
@@ -196,10 +196,19 @@ __global__ void __launch_bounds__(GT, 2)
             S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
         }
         consumers_sync();
-        for (int i = tid; i < t.e0 * kTileNodes; i += GCW * 32) {
-            const int x = i / kTileNodes, k = i % kTileNodes;
-            S.w0[x][k] = wfun(S.nu[0][k], t.o0 + x, wp.c0, wp.h0, wp.q);
+        // W0[a, node] by the Gaussian's two-term recurrence along axis 0:
+        // w(a+1) = w(a) r(a), r(a+1) = r(a) exp(-2h), seeded exactly at the
+        // node's first in-window slab (relative drift <= e0 ulps); the
+        // truncation |delta| <= q is applied exactly
+        const double u0n = S.nu[0][node];
+        const int a_first = max(0, (int)ceil(u0n - wp.q) - t.o0);
+        double w0r, r0r;
+        {
+            const double d = u0n - (double)(t.o0 + a_first);
+            w0r = wp.c0 * exp(-d * d * wp.h0);
+            r0r = exp(wp.h0 * (2.0 * d - 1.0));
         }
+        const double r0step = exp(-2.0 * wp.h0);
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
         double afr[KSMAX], w1r[NTMAX];
@@ -218,7 +227,13 @@ __global__ void __launch_bounds__(GT, 2)
         for (int a = 0; a < t.e0; ++a) {
             const uint32_t q = seq + a;
             const int buf = (int)(q % NST);
-            const double w0 = S.w0[a][node];
+            double w0 = 0.0;
+            if (a >= a_first) {
+                const double d = u0n - (double)(t.o0 + a);
+                w0 = (fabs(d) <= (double)wp.q) ? w0r : 0.0;
+                w0r *= r0r;
+                r0r *= r0step;
+            }
             // every consumer observes every phase (keeps the ring's parity
             // bookkeeping exact); the math is skipped where none of this
             // warp's 8 nodes has weight on the slab (warp-uniform)
