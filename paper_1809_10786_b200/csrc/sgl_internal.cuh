@@ -23,7 +23,7 @@ constexpr double kTwoPi = 6.28318530717958647692;
 // Its box covers the union of the nodes' window supports.
 constexpr int kTileNodes = 64;   // gather tiles: GEMM M-dim (8 warps x 8 nodes)
 constexpr int kBoxMax = 36;      // max box extent on axes 1 and 2 (== the TMA slab box)
-constexpr int kBox0Max = 64;     // gather: max box extent on axis 0 (slabs; no smem cost)
+constexpr int kBox0Max = 96;     // gather: max box extent on axis 0 (slabs; no smem cost)
 constexpr int kSTileNodes = 128; // scatter tiles: GEMM K-dim (more nodes per RED)
 constexpr int kSBox0Max = 96;    // scatter: max box extent on axis 0 (no smem cost)
 constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
