@@ -136,6 +136,34 @@ __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;\n" ::"n"(GCW * 32) : "memory");
 }
 
+// One slab of one warp's 8 nodes: fixed NTMAX x NKS fragment loops with no
+// predicates around the DMMAs (a .sync.aligned MMA under a runtime guard costs
+// a WARPSYNC, a branch and a NOP each); fragments beyond the tile's box have
+// zero W1 / W2 weights and multiply finite smem data.  NKS is 8 for boxes of
+// <= 32 columns (narrow pencils) and 9 otherwise.
+template <int NKS>
+__device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[KSMAX], const double (&w1r)[NTMAX],
+                                            int rb, int cc, int part, double &s_re, double &s_im) {
+#pragma unroll
+    for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
+        double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int b = (nt0 + i) * 4 + rb;
+                const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
+                dmma(d[i], afr[ks], bv);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            s_re = fma(w1r[nt0 + i], d[i][0], s_re);
+            s_im = fma(w1r[nt0 + i], d[i][1], s_im);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(GT, 2)
     k_gather_tiled(const __grid_constant__ CUtensorMap tmap, const Tile *__restrict__ tiles, int64_t ntiles,
                    NodeSet nodes, WindowParams wp, double2 *__restrict__ out) {
@@ -241,28 +269,10 @@ __global__ void __launch_bounds__(GT, 2)
             if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
                 const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
                 double s_re = 0.0, s_im = 0.0;
-                // fixed 9 x 9 fragment loops with no predicates around the DMMAs
-                // (a .sync.aligned MMA under a runtime guard costs a WARPSYNC,
-                // a branch and a NOP each): fragments beyond the tile's box have
-                // zero W1 / W2 weights and multiply finite smem data
-#pragma unroll
-                for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
-                    double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-                    for (int ks = 0; ks < KSMAX; ++ks) {
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            const int b = (nt0 + i) * 4 + rb;
-                            const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
-                            dmma(d[i], afr[ks], bv);
-                        }
-                    }
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        s_re = fma(w1r[nt0 + i], d[i][0], s_re);
-                        s_im = fma(w1r[nt0 + i], d[i][1], s_im);
-                    }
-                }
+                if (KS <= KSMAX - 1)
+                    gather_slab<KSMAX - 1>(sl, afr, w1r, rb, cc, part, s_re, s_im);
+                else
+                    gather_slab<KSMAX>(sl, afr, w1r, rb, cc, part, s_re, s_im);
                 acc_re = fma(w0, s_re, acc_re);
                 acc_im = fma(w0, s_im, acc_im);
             }

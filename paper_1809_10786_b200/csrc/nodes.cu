@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "sgl_internal.cuh"
 
@@ -326,22 +328,30 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         k_warp<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
         SGL_CUDA_CHECK(cudaGetLastError());
     }
-    // gather order: W x W pencils with 2q - 1 + W == 0 (mod 4) (exact 4-row / 4-column DMMA tiles)
+    // Gather order: W x W pencils (cells on axes 1-2), nodes by lo0 inside a
+    // pencil; 2q - 1 + W == 0 (mod 4) gives exact 4-row / 4-column DMMA tiles.
+    // The wide cross-section keeps a 64-node tile within a few lo0 rows, so
+    // the 8 consumer warps stay close together in the slab ring.
     int W = (4 - (2 * p.q - 1) % 4) % 4;
     if (W < 2) W += 4;
     int rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max},
                             p.nodes, &p.tiles, &p.n_tiles, !p.generic, st);
     if (rc || p.generic) return rc;
-    // scatter order: with dense nodes, pencils W x W2 whose axis-2 box is a
-    // multiple of 8 (exact 8-column DMMA tiles, ~17% fewer DMMAs); sparse
-    // node sets keep the gather's W x W pencils, whose wider cross-section
-    // keeps enough nodes per tile to amortise the RED of each box fragment.
+    // Scatter order: with dense nodes, W x W2 pencils whose axis-2 box is a
+    // multiple of 8 (exact 8-column DMMA tiles, ~17 % fewer DMMAs; warps own
+    // whole slabs, so a long lo0 span costs nothing); sparse node sets keep
+    // the gather order, whose wider cross-section keeps enough nodes per tile
+    // to amortise the RED of each box fragment.
     int W2 = (8 - (2 * p.q - 1) % 8) % 8;
     if (W2 < 1) W2 += 8;
     const double cells = (double)p.grid[0] * p.grid[1] * p.grid[2] / 4.0;   // nodes fill axes 0-1 up to pi
     const double per_row = (double)M / cells * W * W2;                        // nodes per lo0 row of a pencil
+    const char *force = getenv("SGL_SCATTER_PENCIL");                        // "wide" / "narrow": experiments
+    bool narrow = W2 != W && per_row >= 2.5;
+    if (force && !strcmp(force, "wide")) narrow = false;
+    if (force && !strcmp(force, "narrow")) narrow = W2 != W;
     const TileGeom stg{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max};
-    if (W2 != W && per_row >= 2.5) {
+    if (narrow) {
         rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W2, stg, p.snodes, &p.stiles, &p.n_stiles, true, st);
     } else {
         p.snodes_shared = true;
