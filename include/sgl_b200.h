@@ -100,6 +100,13 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
 /* Adjoint: values is M complex128, coeffs receives coeff_count(B). */
 int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, void *stream);
 
+/* Forward of `coeffs` and adjoint of `values_in` on one plan in one call
+ * (independent inputs, e.g. a benchmark or a block solver step).  With host
+ * buffers the value H2D overlaps the forward and the value D2H overlaps the
+ * adjoint on a side stream.  values_out: M, coeffs_out: coeff_count(B). */
+int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *values_out,
+                        const sgl_cdouble *values_in, sgl_cdouble *coeffs_out, void *stream);
+
 void sgl_plan_destroy(sgl_plan *plan);
 
 int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info);

@@ -21,7 +21,7 @@ STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares
 EXPORTS = (
-    "sgl_plan_create", "sgl_forward", "sgl_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
+    "sgl_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
 )
 
@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
     L.sgl_forward.restype = ctypes.c_int
     L.sgl_adjoint.argtypes = [vp, vp, vp, vp]
     L.sgl_adjoint.restype = ctypes.c_int
+    L.sgl_forward_adjoint.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.sgl_forward_adjoint.restype = ctypes.c_int
     L.sgl_plan_destroy.argtypes = [vp]
     L.sgl_plan_destroy.restype = None
     L.sgl_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]

@@ -53,6 +53,11 @@ void free_plan(Plan *p) {
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
     if (p->done) cudaEventDestroy(p->done);
+    if (p->ev_a) cudaEventDestroy(p->ev_a);
+    if (p->ev_b) cudaEventDestroy(p->ev_b);
+    if (p->ev_c) cudaEventDestroy(p->ev_c);
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+    if (p->val_buf2) cudaFree(p->val_buf2);
     for (auto &t : p->timers)
         if (t.ready)
             for (auto &e : t.ev) cudaEventDestroy(e);
@@ -103,6 +108,72 @@ struct StageRec {
         n = 0;
     }
 };
+
+
+// ---------------------------------------------------------------------------
+// device-pointer cores shared by the entry points
+
+// side stream, events and the second value buffer for copy/compute overlap
+// (created on first use)
+cudaError_t ensure_side(Plan &p) {
+    if (p.copy_stream) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&p.val_buf2, sizeof(double2) * (p.M ? p.M : 1));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_b, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_c, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking);
+    return e;
+}
+
+int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRec *rec) {
+    auto mark = [&](int s) {
+        if (rec) rec->mark(s);
+    };
+    mark(SGL_STAGE_BASAL);
+    int rc = launch_basal_forward(p, c, p.grid_buf, st, nullptr);
+    if (rc) return rc;
+    if (p.exact) {   // direct NDFT of eta (transform.py:393-394)
+        mark(SGL_STAGE_WINDOW);
+        return launch_exact_forward(p, p.grid_buf, v, st);
+    }
+    mark(SGL_STAGE_FFT);
+    rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+    if (rc) return rc;
+    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+    rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
+    if (rc) return rc;
+    rc = launch_halo_fill(p, p.grid_buf, st);
+    if (rc) return rc;
+    mark(SGL_STAGE_WINDOW);
+    return launch_gather(p, p.grid_buf, v, st);
+}
+
+int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRec *rec) {
+    auto mark = [&](int s) {
+        if (rec) rec->mark(s);
+    };
+    mark(SGL_STAGE_WINDOW);
+    int rc = SGL_OK;
+    if (p.exact) {   // direct adjoint NDFT (transform.py:404-405)
+        rc = launch_exact_adjoint(p, v, p.grid_buf, st);
+        if (rc) return rc;
+    } else {
+        SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+        rc = launch_scatter(p, v, p.grid_buf, st);
+        if (rc) return rc;
+        mark(SGL_STAGE_FFT);
+        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+        if (rc) return rc;
+        rc = launch_halo_fold(p, p.grid_buf, st);
+        if (rc) return rc;
+        cufftDoubleComplex *interior =
+            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
+        if (rc) return rc;
+    }
+    mark(SGL_STAGE_BASAL);
+    return launch_basal_adjoint(p, p.grid_buf, c, st);
+}
 
 }  // namespace
 }  // namespace sgl
@@ -363,6 +434,10 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
     }
     cudaStream_t st = (cudaStream_t)stream;
     const bool cdev = is_device_ptr(coeffs), vdev = values ? is_device_ptr(values) : true;
+    // K > 1 into host memory: double-buffer the values and download vector k
+    // on the side stream while vector k+1 is computed
+    const bool overlap = !vdev && p.M > 0 && K > 1;
+    if (overlap) SGL_CUDA_CHECK(ensure_side(p));
     StageRec rec(p, 0, st);
     for (int64_t k = 0; k < K; ++k) {
         rec.mark(SGL_STAGE_H2D);
@@ -371,34 +446,31 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
             SGL_CUDA_CHECK(cudaMemcpyAsync(p.coef_buf, c, sizeof(double2) * p.count, cudaMemcpyHostToDevice, st));
             c = p.coef_buf;
         }
-        rec.mark(SGL_STAGE_BASAL);
-        int rc = launch_basal_forward(p, c, p.grid_buf, st, nullptr);
-        if (rc) return rc;
+        double2 *host_v = vdev ? nullptr : reinterpret_cast<double2 *>(values) + k * p.M;
         double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : p.val_buf;
-        if (p.exact) {   // direct NDFT of eta (transform.py:393-394)
-            rec.mark(SGL_STAGE_WINDOW);
-            rc = launch_exact_forward(p, p.grid_buf, v, st);
-            if (rc) return rc;
-        } else {
-            rec.mark(SGL_STAGE_FFT);
-            rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-            if (rc) return rc;
-            cufftDoubleComplex *interior =
-                reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-            rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
-            if (rc) return rc;
-            rc = launch_halo_fill(p, p.grid_buf, st);
-            if (rc) return rc;
-            rec.mark(SGL_STAGE_WINDOW);
-            rc = launch_gather(p, p.grid_buf, v, st);
-            if (rc) return rc;
+        cudaEvent_t drained = p.ev_a;
+        if (overlap && (k & 1)) {
+            v = p.val_buf2;
+            drained = p.ev_b;
         }
+        if (overlap && k >= 2) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, drained, 0));   // download of k-2 done
+        const int rc = forward_core(p, c, v, st, &rec);
+        if (rc) return rc;
         rec.mark(SGL_STAGE_D2H);
-        if (!vdev && p.M > 0)
-            SGL_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<double2 *>(values) + k * p.M, p.val_buf,
-                                           sizeof(double2) * p.M, cudaMemcpyDeviceToHost, st));
+        if (overlap) {
+            SGL_CUDA_CHECK(cudaEventRecord(p.ev_c, st));
+            SGL_CUDA_CHECK(cudaStreamWaitEvent(p.copy_stream, p.ev_c, 0));
+            SGL_CUDA_CHECK(cudaMemcpyAsync(host_v, v, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, p.copy_stream));
+            SGL_CUDA_CHECK(cudaEventRecord(drained, p.copy_stream));
+        } else if (!vdev && p.M > 0) {
+            SGL_CUDA_CHECK(cudaMemcpyAsync(host_v, v, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, st));
+        }
         rec.mark(SGL_STAGE_COUNT);
         rec.flush();
+    }
+    if (overlap) {   // join the side stream back into st
+        SGL_CUDA_CHECK(cudaEventRecord(p.ev_c, p.copy_stream));
+        SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_c, 0));
     }
     if (!vdev) SGL_CUDA_CHECK(cudaStreamSynchronize(st));
     SGL_CUDA_CHECK(cudaGetLastError());
@@ -427,28 +499,8 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
         SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf, v, sizeof(double2) * p.M, cudaMemcpyHostToDevice, st));
         v = p.val_buf;
     }
-    rec.mark(SGL_STAGE_WINDOW);
-    int rc = SGL_OK;
-    if (p.exact) {   // direct adjoint NDFT (transform.py:404-405)
-        rc = launch_exact_adjoint(p, v, p.grid_buf, st);
-        if (rc) return rc;
-    } else {
-        SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-        rc = launch_scatter(p, v, p.grid_buf, st);
-        if (rc) return rc;
-        rec.mark(SGL_STAGE_FFT);
-        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-        if (rc) return rc;
-        rc = launch_halo_fold(p, p.grid_buf, st);
-        if (rc) return rc;
-        cufftDoubleComplex *interior =
-            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
-        if (rc) return rc;
-    }
-    rec.mark(SGL_STAGE_BASAL);
     double2 *c = cdev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;
-    rc = launch_basal_adjoint(p, p.grid_buf, c, st);
+    const int rc = adjoint_core(p, v, c, st, &rec);
     if (rc) return rc;
     rec.mark(SGL_STAGE_D2H);
     if (!cdev) {
@@ -457,6 +509,64 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
     }
     rec.mark(SGL_STAGE_COUNT);
     rec.flush();
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *values_out,
+                        const sgl_cdouble *values_in, sgl_cdouble *coeffs_out, void *stream) {
+    g_err.clear();
+    if (!plan) {
+        set_error("NULL plan");
+        return SGL_EINVAL;
+    }
+    Plan &p = *reinterpret_cast<Plan *>(plan);
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    PlanGuard guard(p, (cudaStream_t)stream);
+    if (!coeffs || !coeffs_out || (p.M > 0 && (!values_out || !values_in))) {
+        set_error("coefficient / value arrays do not match the plan");
+        return SGL_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    SGL_CUDA_CHECK(ensure_side(p));
+    cudaStream_t cs = p.copy_stream;
+    const bool cdev = is_device_ptr(coeffs), codev = is_device_ptr(coeffs_out);
+    const bool vodev = values_out ? is_device_ptr(values_out) : true;
+    const bool videv = values_in ? is_device_ptr(values_in) : true;
+    // coefficients first: a copy queued behind the large value upload would
+    // hold up the forward (copies in one direction share an engine queue)
+    const double2 *c = reinterpret_cast<const double2 *>(coeffs);
+    if (!cdev) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(p.coef_buf, c, sizeof(double2) * p.count, cudaMemcpyHostToDevice, st));
+        c = p.coef_buf;
+    }
+    // adjoint input: H2D on the side stream, overlapped with the forward
+    const double2 *vin = reinterpret_cast<const double2 *>(values_in);
+    if (!videv && p.M > 0) {
+        SGL_CUDA_CHECK(cudaEventRecord(p.ev_a, st));   // the plan's previous work is ordered before
+        SGL_CUDA_CHECK(cudaStreamWaitEvent(cs, p.ev_a, 0));
+        SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf2, vin, sizeof(double2) * p.M, cudaMemcpyHostToDevice, cs));
+        SGL_CUDA_CHECK(cudaEventRecord(p.ev_a, cs));   // the adjoint waits on this upload only
+        vin = p.val_buf2;
+    }
+    double2 *vout = vodev ? reinterpret_cast<double2 *>(values_out) : p.val_buf;
+    int rc = forward_core(p, c, vout, st, nullptr);
+    if (rc) return rc;
+    // forward output: D2H on the side stream, overlapped with the adjoint
+    SGL_CUDA_CHECK(cudaEventRecord(p.ev_b, st));
+    SGL_CUDA_CHECK(cudaStreamWaitEvent(cs, p.ev_b, 0));
+    if (!vodev && p.M > 0)
+        SGL_CUDA_CHECK(cudaMemcpyAsync(values_out, p.val_buf, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, cs));
+    if (!videv && p.M > 0) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_a, 0));
+    double2 *cout = codev ? reinterpret_cast<double2 *>(coeffs_out) : p.coef_buf;
+    rc = adjoint_core(p, vin, cout, st, nullptr);
+    if (rc) return rc;
+    if (!codev)
+        SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs_out, p.coef_buf, sizeof(double2) * p.count, cudaMemcpyDeviceToHost, st));
+    // join the side stream back into st (the next call on this plan reuses val_buf)
+    SGL_CUDA_CHECK(cudaEventRecord(p.ev_b, cs));
+    SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_b, 0));
+    if (!codev || !vodev) SGL_CUDA_CHECK(cudaStreamSynchronize(st));
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }

@@ -117,6 +117,13 @@ struct Plan {
     // so a plan can be shared like the reference's (README.md:66-67).
     std::mutex mu;
     cudaEvent_t done = nullptr;
+
+    // copy/compute overlap (sgl_forward_adjoint, batched sgl_forward into
+    // host memory): side stream for the host copies, events, a second value
+    // buffer; created on first use
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    double2 *val_buf2 = nullptr;
 };
 
 // error state

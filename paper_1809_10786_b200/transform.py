@@ -239,6 +239,42 @@ def adjoint(p: SglPlan, values, precise: bool = False):
     return out
 
 
+def forward_adjoint(p: SglPlan, coeffs, values):
+    """``(forward(p, coeffs), adjoint(p, values))`` in one library call.
+
+    The two inputs are independent; with host (numpy) arrays the library
+    overlaps the value upload with the forward and the value download with
+    the adjoint (sgl_forward_adjoint).  Same checks as `forward`/`adjoint`."""
+    cnt, M = p.count, p.m_points
+    L = _native.lib()
+    if _is_torch(coeffs) or _is_torch(values):
+        torch = _torch()
+        c = torch.as_tensor(coeffs).to(torch.complex128).contiguous()
+        v = torch.as_tensor(values).to(torch.complex128).contiguous()
+        if tuple(c.shape) != (cnt,):
+            raise ValueError("coefficient length does not match the bandwidth")
+        if tuple(v.shape) != (M,):
+            raise ValueError("values length does not match the plan")
+        dev = c.device if c.is_cuda else v.device
+        out_v = torch.empty((M,), dtype=torch.complex128, device=dev)
+        out_c = torch.empty((cnt,), dtype=torch.complex128, device=dev)
+        _native.check(L.sgl_forward_adjoint(p._handle, c.data_ptr(), out_v.data_ptr() if M else None,
+                                            v.data_ptr() if M else None, out_c.data_ptr(),
+                                            _stream_ptr(out_c)))
+        return out_v, out_c
+    c = np.ascontiguousarray(coeffs, dtype=np.complex128)
+    v = np.ascontiguousarray(values, dtype=np.complex128)
+    if c.shape != (cnt,):
+        raise ValueError("coefficient length does not match the bandwidth")
+    if v.shape != (M,):
+        raise ValueError("values length does not match the plan")
+    out_v = np.empty(M, dtype=np.complex128)
+    out_c = np.empty(cnt, dtype=np.complex128)
+    _native.check(L.sgl_forward_adjoint(p._handle, c.ctypes.data, out_v.ctypes.data if M else None,
+                                        v.ctypes.data if M else None, out_c.ctypes.data, None))
+    return out_v, out_c
+
+
 def choose_rho(points) -> float:
     """Largest sample radius; 1.0 if all points sit at the origin (transform.py:39-43)."""
     pts = np.atleast_2d(np.asarray(points, dtype=float))

@@ -133,6 +133,18 @@ def test_batched_forward_matches_single(sgl):
         assert np.array_equal(fb[k], sgl.forward(p, g["coeffs"][k]))
 
 
+def test_batched_forward_host_double_buffer(sgl):
+    """K = 5 vectors into host memory: downloads overlap the next vector on a
+    side stream with two alternating value buffers."""
+    g = load_golden("cfg2_sub2000")
+    p = _plan(sgl, g)
+    rng = np.random.default_rng(7)
+    C = np.stack([sgl.gen_coeffs(int(g["B"]), rng) for _ in range(5)])
+    fb = sgl.forward(p, C)
+    for k in range(5):
+        assert np.array_equal(fb[k], sgl.forward(p, C[k]))
+
+
 def test_torch_device_tensors(sgl):
     import torch
     g = load_golden("b12_q12")
@@ -144,6 +156,33 @@ def test_torch_device_tensors(sgl):
     assert rel(f.cpu().numpy(), g["fwd"]) <= TOL
     a = sgl.adjoint(p, torch.as_tensor(g["values"], device=dev))
     assert rel(a.cpu().numpy(), g["adj"]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["b12_q12", "cfg2_sub2000"])
+def test_forward_adjoint_fused_call(sgl, name):
+    """sgl_forward_adjoint == separate forward + adjoint (host buffers:
+    side-stream copies; device tensors: plain stream order).  The forward is
+    bit-identical; the adjoint's RED accumulation order varies run to run, so
+    it agrees to rounding."""
+    import torch
+    g = load_golden(name)
+    p = _plan(sgl, g)
+    c = g["coeffs"] if g["coeffs"].ndim == 1 else g["coeffs"][0]
+    f, a = sgl.forward_adjoint(p, c, g["values"])
+    assert np.array_equal(f, sgl.forward(p, c))
+    assert rel(a, sgl.adjoint(p, g["values"])) <= 1e-13
+    assert rel(a, g["adj"]) <= TOL
+    for _ in range(3):   # repeated calls reuse the side stream and buffers
+        f2, a2 = sgl.forward_adjoint(p, c, g["values"])
+        assert np.array_equal(f2, f) and rel(a2, a) <= 1e-13
+    dev = torch.device("cuda", 0)
+    fd, ad = sgl.forward_adjoint(p, torch.as_tensor(c, device=dev), torch.as_tensor(g["values"], device=dev))
+    assert np.array_equal(fd.cpu().numpy(), f) and rel(ad.cpu().numpy(), a) <= 1e-13
+    with pytest.raises(ValueError):
+        sgl.forward_adjoint(p, c[:-1], g["values"])
+    e = sgl.plan(3, np.zeros((0, 3)), q=4)
+    fe, ae = sgl.forward_adjoint(e, np.ones(14), np.zeros(0))
+    assert fe.shape == (0,) and np.all(ae == 0)
 
 
 def test_empty_and_single_node(sgl):
