@@ -139,27 +139,20 @@ __device__ __forceinline__ void consumers_sync() {
 // One slab of one warp's 8 nodes: fixed NTMAX x NKS fragment loops with no
 // predicates around the DMMAs (a .sync.aligned MMA under a runtime guard costs
 // a WARPSYNC, a branch and a NOP each); fragments beyond the tile's box have
-// zero W1 / W2 weights and multiply finite smem data.  NKS is 8 for boxes of
-// <= 32 columns (narrow pencils) and 9 otherwise.
+// zero W2 weights and multiply finite smem data.  NKS is 8 for boxes of
+// <= 32 columns (narrow pencils) and 9 otherwise.  W0[a, node] is folded
+// into the A fragments, so the NTMAX accumulators run over the whole tile
+// (K = slabs x columns) and W1 is applied once per tile.
 template <int NKS>
-__device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[KSMAX], const double (&w1r)[NTMAX],
-                                            int rb, int cc, int part, double &s_re, double &s_im) {
+__device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[KSMAX], double w0, int rb, int cc,
+                                            int part, double (&d)[NTMAX][2]) {
 #pragma unroll
-    for (int nt0 = 0; nt0 < NTMAX; nt0 += 3) {
-        double d[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int ks = 0; ks < NKS; ++ks) {
+        const double a = w0 * afr[ks];
 #pragma unroll
-        for (int ks = 0; ks < NKS; ++ks) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int b = (nt0 + i) * 4 + rb;
-                const double bv = sl[(b * SSTR + ks * 4 + cc) * 2 + part];
-                dmma(d[i], afr[ks], bv);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            s_re = fma(w1r[nt0 + i], d[i][0], s_re);
-            s_im = fma(w1r[nt0 + i], d[i][1], s_im);
+        for (int nt = 0; nt < NTMAX; ++nt) {
+            const int b = nt * 4 + rb;
+            dmma(d[nt], a, sl[(b * SSTR + ks * 4 + cc) * 2 + part]);
         }
     }
 }
@@ -251,14 +244,16 @@ __global__ void __launch_bounds__(GT, 2)
         }
         consumers_sync();
         const bool col_live = warp * 8 < t.count;
-        double acc_re = 0.0, acc_im = 0.0;
+        double d[NTMAX][2];
+#pragma unroll
+        for (int nt = 0; nt < NTMAX; ++nt) d[nt][0] = d[nt][1] = 0.0;
         for (int a = 0; a < t.e0; ++a) {
             const uint32_t q = seq + a;
             const int buf = (int)(q % NST);
             double w0 = 0.0;
             if (a >= a_first) {
-                const double d = u0n - (double)(t.o0 + a);
-                w0 = (fabs(d) <= (double)wp.q) ? w0r : 0.0;
+                const double dl = u0n - (double)(t.o0 + a);
+                w0 = (fabs(dl) <= (double)wp.q) ? w0r : 0.0;
                 w0r *= r0r;
                 r0r *= r0step;
             }
@@ -268,16 +263,19 @@ __global__ void __launch_bounds__(GT, 2)
             mbar_wait(&S.full[buf], (q / NST) & 1);
             if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
                 const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
-                double s_re = 0.0, s_im = 0.0;
                 if (KS <= KSMAX - 1)
-                    gather_slab<KSMAX - 1>(sl, afr, w1r, rb, cc, part, s_re, s_im);
+                    gather_slab<KSMAX - 1>(sl, afr, w0, rb, cc, part, d);
                 else
-                    gather_slab<KSMAX>(sl, afr, w1r, rb, cc, part, s_re, s_im);
-                acc_re = fma(w0, s_re, acc_re);
-                acc_im = fma(w0, s_im, acc_im);
+                    gather_slab<KSMAX>(sl, afr, w0, rb, cc, part, d);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[buf]);
+        }
+        double acc_re = 0.0, acc_im = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NTMAX; ++nt) {
+            acc_re = fma(w1r[nt], d[nt][0], acc_re);
+            acc_im = fma(w1r[nt], d[nt][1], acc_im);
         }
         seq += (uint32_t)t.e0;
         // reduce over the 4 lanes of a node (their rows b differ)
