@@ -15,6 +15,8 @@
  *   sgl_last_error    <- the ValueError message text raised by the above
  *   sgl_plan_get_info <- SglPlan / NfftPlan fields (transform.py:292-317,
  *                        nfft.py:101-120)
+ *   sgl_direct_forward  <- transform.evaluate_direct         (transform.py:95-117)
+ *   sgl_direct_adjoint  <- transform.evaluate_direct_adjoint (transform.py:120-139)
  *
  * Pointers to points / coefficients / values may be host or device
  * (CUDA) memory; the library detects which.  Host outputs are complete when
@@ -108,6 +110,15 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
                         const sgl_cdouble *values_in, sgl_cdouble *coeffs_out, void *stream);
 
 void sgl_plan_destroy(sgl_plan *plan);
+
+/* Direct summation of the expansion (no plan, O(M * count) FP64; the
+ * reference's verification path and the CLI's --method naive).
+ * points: M x 3 (r, theta, phi); coeffs: coeff_count(B); values: M.
+ * Errors as the reference: bandwidth < 1, length mismatches (SGL_EINVAL). */
+int sgl_direct_forward(int32_t B, int64_t M, const double *points, const sgl_cdouble *coeffs,
+                       sgl_cdouble *values, void *stream);
+int sgl_direct_adjoint(int32_t B, int64_t M, const double *points, const sgl_cdouble *values,
+                       sgl_cdouble *coeffs, void *stream);
 
 int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info);
 

@@ -8,10 +8,11 @@ There is no CPU fallback.
 """
 from .generate import (cartesian_to_spherical, coeff_count, gen_coeffs, gen_grid,  # noqa: F401
                        gen_points_ball)
-from .transform import SglPlan, adjoint, choose_rho, forward, forward_adjoint, plan  # noqa: F401
+from .transform import (SglPlan, adjoint, choose_rho, evaluate_direct, evaluate_direct_adjoint,  # noqa: F401
+                        forward, forward_adjoint, plan)
 
 __all__ = [
-    "SglPlan", "adjoint", "cartesian_to_spherical", "choose_rho", "coeff_count", "forward", "forward_adjoint",
-    "gen_coeffs", "gen_grid", "gen_points_ball", "plan",
+    "SglPlan", "adjoint", "cartesian_to_spherical", "choose_rho", "coeff_count", "evaluate_direct",
+    "evaluate_direct_adjoint", "forward", "forward_adjoint", "gen_coeffs", "gen_grid", "gen_points_ball", "plan",
 ]
 __version__ = "0.1.0"

@@ -21,7 +21,8 @@ STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares
 EXPORTS = (
-    "sgl_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
+    "sgl_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_direct_forward",
+    "sgl_direct_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
 )
 
@@ -74,6 +75,9 @@ def lib() -> ctypes.CDLL:
     L.sgl_adjoint.restype = ctypes.c_int
     L.sgl_forward_adjoint.argtypes = [vp, vp, vp, vp, vp, vp]
     L.sgl_forward_adjoint.restype = ctypes.c_int
+    for fn in (L.sgl_direct_forward, L.sgl_direct_adjoint):
+        fn.argtypes = [ctypes.c_int32, ctypes.c_int64, vp, vp, vp, vp]
+        fn.restype = ctypes.c_int
     L.sgl_plan_destroy.argtypes = [vp]
     L.sgl_plan_destroy.restype = None
     L.sgl_plan_get_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libsgl_b200.so")
-SOURCES = ["capi.cu", "nodes.cu", "basal.cu", "gridding.cu", "exact.cu"]
+SOURCES = ["capi.cu", "nodes.cu", "basal.cu", "gridding.cu", "exact.cu", "direct.cu"]
 HEADERS = ["sgl_internal.cuh", os.path.join("..", "..", "include", "sgl_b200.h")]
 
 

@@ -571,4 +571,122 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
     return SGL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// direct sums (transform.py:95-139)
+
+}  // extern "C"
+
+namespace {
+
+struct DeviceScratch {
+    std::vector<void *> ptrs;
+    cudaStream_t st;
+    explicit DeviceScratch(cudaStream_t s) : st(s) {}
+    ~DeviceScratch() {
+        for (void *p : ptrs) cudaFreeAsync(p, st);
+    }
+    // device copy of a host input (or the pointer itself when on the device)
+    template <typename T>
+    int input(const T *src, size_t n, const T **dst) {
+        if (!src || n == 0 || is_device_ptr(src)) {
+            *dst = src;
+            return SGL_OK;
+        }
+        void *d = nullptr;
+        SGL_CUDA_CHECK(cudaMallocAsync(&d, sizeof(T) * n, st));
+        ptrs.push_back(d);
+        SGL_CUDA_CHECK(cudaMemcpyAsync(d, src, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+        *dst = reinterpret_cast<const T *>(d);
+        return SGL_OK;
+    }
+    template <typename T>
+    int output(T *user, size_t n, T **dst) {
+        if (!user || n == 0 || is_device_ptr(user)) {
+            *dst = user;
+            return SGL_OK;
+        }
+        void *d = nullptr;
+        SGL_CUDA_CHECK(cudaMallocAsync(&d, sizeof(T) * n, st));
+        ptrs.push_back(d);
+        *dst = reinterpret_cast<T *>(d);
+        return SGL_OK;
+    }
+};
+
+int direct_check(int32_t B, int64_t M, const double *points) {
+    if (B < 1) {
+        set_error("bandwidth must be >= 1");
+        return SGL_EINVAL;
+    }
+    if (M < 0 || (M > 0 && !points)) {
+        set_error("points must be (M, 3) spherical coordinates");
+        return SGL_EINVAL;
+    }
+    return SGL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgl_direct_forward(int32_t B, int64_t M, const double *points, const sgl_cdouble *coeffs,
+                       sgl_cdouble *values, void *stream) {
+    g_err.clear();
+    int rc = direct_check(B, M, points);
+    if (rc) return rc;
+    if (!coeffs || (M > 0 && !values)) {
+        set_error("coefficient length does not match the bandwidth");
+        return SGL_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t count = (int64_t)B * (B + 1) * (2 * B + 1) / 6;
+    DeviceScratch sc(st);
+    const double *dp;
+    const double2 *dc;
+    double2 *dv;
+    if ((rc = sc.input(points, (size_t)M * 3, &dp))) return rc;
+    if ((rc = sc.input(reinterpret_cast<const double2 *>(coeffs), (size_t)count, &dc))) return rc;
+    if ((rc = sc.output(reinterpret_cast<double2 *>(values), (size_t)M, &dv))) return rc;
+    if ((rc = launch_direct_forward(B, M, dp, dc, dv, st))) {
+        set_error("CUDA error in the direct forward kernel");
+        return rc;
+    }
+    if (M > 0 && dv != reinterpret_cast<double2 *>(values)) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(values, dv, sizeof(double2) * M, cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int sgl_direct_adjoint(int32_t B, int64_t M, const double *points, const sgl_cdouble *values,
+                       sgl_cdouble *coeffs, void *stream) {
+    g_err.clear();
+    int rc = direct_check(B, M, points);
+    if (rc) return rc;
+    if (!coeffs || (M > 0 && !values)) {
+        set_error("values length does not match the point count");
+        return SGL_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t count = (int64_t)B * (B + 1) * (2 * B + 1) / 6;
+    DeviceScratch sc(st);
+    const double *dp;
+    const double2 *dv;
+    double2 *dc;
+    if ((rc = sc.input(points, (size_t)M * 3, &dp))) return rc;
+    if ((rc = sc.input(reinterpret_cast<const double2 *>(values), (size_t)M, &dv))) return rc;
+    if ((rc = sc.output(reinterpret_cast<double2 *>(coeffs), (size_t)count, &dc))) return rc;
+    if ((rc = launch_direct_adjoint(B, M, dp, dv, dc, count, st))) {
+        set_error("CUDA error in the direct adjoint kernel");
+        return rc;
+    }
+    if (dc != reinterpret_cast<double2 *>(coeffs)) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs, dc, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
 }  // extern "C"

@@ -149,6 +149,9 @@ int launch_basal_adjoint(const Plan &p, const double2 *grid, double2 *coeffs, cu
 int make_grid_tmap(Plan &p);
 int launch_exact_forward(const Plan &p, const double2 *eta, double2 *values, cudaStream_t st);
 int launch_exact_adjoint(const Plan &p, const double2 *values, double2 *eta, cudaStream_t st);
+int launch_direct_forward(int B, int64_t M, const double *pts, const double2 *c, double2 *out, cudaStream_t st);
+int launch_direct_adjoint(int B, int64_t M, const double *pts, const double2 *v, double2 *c, int64_t count,
+                          cudaStream_t st);
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
 

@@ -18,6 +18,13 @@ def coeff_count(B: int) -> int:
     return B * (B + 1) * (2 * B + 1) // 6
 
 
+def nlm_table(B: int) -> np.ndarray:
+    """(count, 3) int64 rows (n, l, m) in mu order, mu = n(n-1)(2n-1)/6 +
+    l(l+1) + m (indexing.py:41-81)."""
+    rows = [(n, l, m) for n in range(1, B + 1) for l in range(n) for m in range(-l, l + 1)]
+    return np.array(rows, dtype=np.int64).reshape(-1, 3)
+
+
 def rng_from(seed) -> np.random.Generator:
     """PCG64 generator, or pass-through of an existing one (generate.py:17-20)."""
     if isinstance(seed, np.random.Generator):

@@ -275,6 +275,77 @@ def forward_adjoint(p: SglPlan, coeffs, values):
     return out_v, out_c
 
 
+def _direct_points(points):
+    if _is_torch(points):
+        torch = _torch()
+        pts = points.to(torch.float64)
+        pts = (pts.reshape(1, -1) if pts.dim() == 1 else pts).contiguous()
+        if pts.dim() != 2 or pts.shape[1] != 3:
+            raise ValueError("points must be (M, 3) spherical coordinates")
+        return pts, pts.data_ptr(), int(pts.shape[0])
+    pts = np.atleast_2d(np.ascontiguousarray(points, dtype=np.float64))
+    if pts.ndim != 2 or pts.shape[1] != 3:
+        raise ValueError("points must be (M, 3) spherical coordinates")
+    return pts, pts.ctypes.data, int(pts.shape[0])
+
+
+def evaluate_direct(coeffs, B: int, points):
+    """Direct summation of the expansion at the points, on the device
+    (reference transform.py:95-117; O(M * count): verification / the CLI's
+    ``--method naive``)."""
+    if B < 1:
+        raise ValueError("bandwidth must be >= 1")
+    pts, pptr, M = _direct_points(points)
+    cnt = coeff_count(B)
+    L = _native.lib()
+    if _is_torch(coeffs) or _is_torch(points):
+        torch = _torch()
+        dev = next(x.device for x in (coeffs, points) if _is_torch(x))
+        c = torch.as_tensor(coeffs, device=dev).to(torch.complex128).contiguous()
+        if tuple(c.shape) != (cnt,):
+            raise ValueError("coefficient length does not match the bandwidth")
+        pts = torch.as_tensor(pts, device=c.device)
+        out = torch.empty((M,), dtype=torch.complex128, device=c.device)
+        _native.check(L.sgl_direct_forward(int(B), M, pts.data_ptr() if M else None, c.data_ptr(),
+                                           out.data_ptr() if M else None, _stream_ptr(out)))
+        return out
+    c = np.ascontiguousarray(coeffs, dtype=np.complex128)
+    if c.shape != (cnt,):
+        raise ValueError("coefficient length does not match the bandwidth")
+    out = np.empty(M, dtype=np.complex128)
+    _native.check(L.sgl_direct_forward(int(B), M, pptr if M else None, c.ctypes.data,
+                                       out.ctypes.data if M else None, None))
+    return out
+
+
+def evaluate_direct_adjoint(values, B: int, points):
+    """Direct adjoint sums c_mu = sum_i v_i conj(H_mu(x_i)) on the device
+    (reference transform.py:120-139)."""
+    if B < 1:
+        raise ValueError("bandwidth must be >= 1")
+    pts, pptr, M = _direct_points(points)
+    cnt = coeff_count(B)
+    L = _native.lib()
+    if _is_torch(values) or _is_torch(points):
+        torch = _torch()
+        dev = next(x.device for x in (values, points) if _is_torch(x))
+        v = torch.as_tensor(values, device=dev).to(torch.complex128).contiguous()
+        if tuple(v.shape) != (M,):
+            raise ValueError("values length does not match the point count")
+        pts = torch.as_tensor(pts, device=v.device)
+        out = torch.empty((cnt,), dtype=torch.complex128, device=v.device)
+        _native.check(L.sgl_direct_adjoint(int(B), M, pts.data_ptr() if M else None,
+                                           v.data_ptr() if M else None, out.data_ptr(), _stream_ptr(out)))
+        return out
+    v = np.ascontiguousarray(values, dtype=np.complex128)
+    if v.shape != (M,):
+        raise ValueError("values length does not match the point count")
+    out = np.empty(cnt, dtype=np.complex128)
+    _native.check(L.sgl_direct_adjoint(int(B), M, pptr if M else None, v.ctypes.data if M else None,
+                                       out.ctypes.data, None))
+    return out
+
+
 def choose_rho(points) -> float:
     """Largest sample radius; 1.0 if all points sit at the origin (transform.py:39-43)."""
     pts = np.atleast_2d(np.asarray(points, dtype=float))

@@ -29,7 +29,8 @@ def golden_names(pattern="*"):
     return out
 
 
-SMALL = [n for n in golden_names() if not n.startswith(("cfg", "inv_"))]
+SMALL = [n for n in golden_names() if not n.startswith(("cfg", "inv_", "direct_"))]
+DIRECT = [n for n in golden_names() if n.startswith("direct_")]
 
 
 @pytest.fixture(scope="session")

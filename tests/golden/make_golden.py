@@ -180,7 +180,76 @@ def invert_cases(ref):
                          solution=rep.solution, iterations=rep.iterations, converged=rep.converged,
                          residual_history=np.array(rep.residual_history),
                          abs_error_history=np.array(rep.abs_error_history))
+    # midpoint seed (solvers.py:166-191) on Cartesian-grid samples + CGNR from it
+    B, kappa, N = 4, 1.5, 8
+    pts = ref.gen_grid(N, kappa)
+    rng = np.random.Generator(np.random.PCG64(303))
+    c = ref.gen_coeffs(B, rng)
+    vals = ref.forward(ref.plan(B, pts), c)
+    from sglnufft.solvers import midpoint_initial_guess
+    x0 = midpoint_initial_guess(vals, pts, B, kappa, N)
+    rep = ref.invert(pts, vals, B, x0_mode="midpoint", kappa=kappa, grid_n=N, max_iter=30, tol=1e-12)
+    out["inv_mid_b4"] = dict(B=B, q=16, compact=False, points=pts, coeffs=c, values=vals, kappa=kappa, grid_n=N,
+                             x0=x0, solution=rep.solution, iterations=rep.iterations, converged=rep.converged,
+                             residual_history=np.array(rep.residual_history))
     return out
+
+
+def direct_cases(ref):
+    """The reference's direct sums evaluate_direct / evaluate_direct_adjoint
+    (transform.py:95-139) at small B, including r = 0, the poles and phi = 0."""
+    out = {}
+    special = np.array([[0.0, 0.0, 0.0], [0.0, 1.0, 2.0], [1.0, 0.0, 0.3], [1.2, np.pi, 5.0],
+                        [2.0, np.pi / 2, 0.0], [0.7, 1e-9, 2 * np.pi - 1e-12], [2.5, 2.0, np.pi]])
+    for name, B, M, rad, seed in [("direct_b1", 1, 5, 1.0, 401), ("direct_b7", 7, 60, 2.0, 402),
+                                  ("direct_b16", 16, 200, 3.5, 403), ("direct_b24", 24, 120, 4.0, 404)]:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        c = ref.gen_coeffs(B, rng)
+        pts = np.concatenate([special, ref.gen_points_ball(M, rad, rng)])
+        v = _vals(rng, pts.shape[0])
+        out[name] = dict(B=B, points=pts, coeffs=c, values=v, fwd=ref.transform.evaluate_direct(c, B, pts),
+                         adj=ref.transform.evaluate_direct_adjoint(v, B, pts))
+    return out
+
+
+def csv_cases(ref):
+    """Files written by the reference CLI (cli.py) itself: generators and the
+    three transform methods on a small problem (tests/golden/csv/)."""
+    import shutil
+    import tempfile
+    from sglnufft import cli
+    d = os.path.join(HERE, "csv")
+    os.makedirs(d, exist_ok=True)
+    tmp = tempfile.mkdtemp()
+    runs = [
+        ["gen-coeffs", "-B", "5", "--seed", "7", "--out", "c_b5.csv"],
+        ["gen-points", "-M", "40", "--kappa", "2.5", "--seed", "3", "--out", "p_m40.csv"],
+        ["gen-grid", "-N", "4", "--kappa", "1.5", "--out", "g_n4.csv"],
+        ["forward", "--coeffs", "c_b5.csv", "--points", "p_m40.csv", "--method", "naive", "--out", "f_naive.csv"],
+        ["forward", "--coeffs", "c_b5.csv", "--points", "p_m40.csv", "-q", "8", "--out", "f_fast.csv"],
+        ["forward", "--coeffs", "c_b5.csv", "--points", "p_m40.csv", "--method", "fast-exact",
+         "--out", "f_exact.csv"],
+        ["adjoint", "--values", "f_naive.csv", "--points", "p_m40.csv", "-B", "5", "--method", "naive",
+         "--out", "a_naive.csv"],
+        ["adjoint", "--values", "f_naive.csv", "--points", "p_m40.csv", "-B", "5", "-q", "8", "--out", "a_fast.csv"],
+        ["invert", "--values", "f_naive.csv", "--points", "p_m40.csv", "-B", "3", "--max-iter", "50",
+         "--out", "inv_b3.csv"],
+    ]
+    cwd = os.getcwd()
+    os.chdir(tmp)
+    try:
+        for argv in runs:
+            rc = cli.main(argv)
+            assert rc == 0, argv
+        for f in sorted(os.listdir(tmp)):
+            shutil.copy(os.path.join(tmp, f), os.path.join(d, f))
+            print("wrote", os.path.join(d, f))
+    finally:
+        os.chdir(cwd)
+        shutil.rmtree(tmp)
+    with open(os.path.join(d, "RUNS.txt"), "w") as fh:
+        fh.write("\n".join(" ".join(r) for r in runs) + "\n")
+    return {}
 
 
 def main():
@@ -196,6 +265,10 @@ def main():
         cases.update(cfg_cases(ref, args.skip_big))
     if args.only in ("", "invert"):
         cases.update(invert_cases(ref))
+    if args.only in ("", "direct"):
+        cases.update(direct_cases(ref))
+    if args.only in ("", "csv"):
+        csv_cases(ref)
     for name, d in cases.items():
         path = os.path.join(HERE, f"ref_{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})

@@ -4,7 +4,7 @@ reference's own known-answer values."""
 import numpy as np
 import pytest
 
-from conftest import SMALL, load_golden
+from conftest import DIRECT, SMALL, load_golden
 from oracle import sgl_oracle as o
 
 TOL = 1e-12
@@ -20,6 +20,15 @@ def test_oracle_matches_reference_goldens(name, oracle_built):
     assert o.rel_linf(f, g["fwd"]) <= TOL
     a = o.oracle_adjoint(p, g["values"], threads=1)
     assert o.rel_linf(a, g["adj"]) <= TOL
+
+
+@pytest.mark.parametrize("name", DIRECT)
+def test_oracle_direct_sums_match_reference(name):
+    # evaluate_direct(_adjoint) (transform.py:95-139) against the reference's own output
+    g = load_golden(name)
+    B = int(g["B"])
+    assert o.rel_linf(o.evaluate_direct(g["coeffs"], B, g["points"]), g["fwd"]) <= TOL
+    assert o.rel_linf(o.evaluate_direct_adjoint(g["values"], B, g["points"]), g["adj"]) <= TOL
 
 
 def test_oracle_numpy_and_c_gridding_agree(oracle_built):

@@ -34,6 +34,21 @@ def test_cgne_matches_reference(solvers):
     np.testing.assert_allclose(rep.residual_history[:20], g["residual_history"][:20], rtol=1e-6)
 
 
+def test_midpoint_seed_and_cgnr_match_reference(solvers):
+    # midpoint_initial_guess (solvers.py:166-191) by device direct sums, then CGNR from it
+    g = load_golden("inv_mid_b4")
+    B, kappa, N = int(g["B"]), float(g["kappa"]), int(g["grid_n"])
+    x0 = solvers.midpoint_initial_guess(g["values"], g["points"], B, kappa, N)
+    assert np.max(np.abs(x0 - g["x0"])) <= 1e-12 * np.max(np.abs(g["x0"]))
+    rep = solvers.invert(g["points"], g["values"], B, x0_mode="midpoint", kappa=kappa, grid_n=N, max_iter=30,
+                         tol=1e-12)
+    assert rep.converged == bool(g["converged"]) and abs(rep.iterations - int(g["iterations"])) <= 1
+    sol = g["solution"]
+    assert np.max(np.abs(rep.solution - sol)) <= 1e-9 * np.max(np.abs(sol))
+    with pytest.raises(ValueError):
+        solvers.midpoint_initial_guess(g["values"], g["points"], B, kappa, N, weight="volume")
+
+
 def test_operator_pairing_and_errors(solvers):
     import paper_1809_10786_b200 as sgl
     g = load_golden("b8_q16")
