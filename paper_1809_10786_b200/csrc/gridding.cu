@@ -41,7 +41,7 @@ __device__ __forceinline__ double wfun(double u, int cell, double c, double h, i
 }
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
@@ -146,14 +146,21 @@ __device__ __forceinline__ void consumers_sync() {
 template <int NKS>
 __device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[KSMAX], double w0, int rb, int cc,
                                             int part, double (&d)[NTMAX][2]) {
+    // B fragments double-buffered one k-step ahead, so no DMMA waits on the
+    // shared-memory load feeding it
+    double bf[2][NTMAX];
+#pragma unroll
+    for (int nt = 0; nt < NTMAX; ++nt) bf[0][nt] = sl[((nt * 4 + rb) * SSTR + cc) * 2 + part];
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
+        if (ks + 1 < NKS) {
+#pragma unroll
+            for (int nt = 0; nt < NTMAX; ++nt)
+                bf[(ks + 1) & 1][nt] = sl[((nt * 4 + rb) * SSTR + (ks + 1) * 4 + cc) * 2 + part];
+        }
         const double a = w0 * afr[ks];
 #pragma unroll
-        for (int nt = 0; nt < NTMAX; ++nt) {
-            const int b = nt * 4 + rb;
-            dmma(d[nt], a, sl[(b * SSTR + ks * 4 + cc) * 2 + part]);
-        }
+        for (int nt = 0; nt < NTMAX; ++nt) dmma(d[nt], a, bf[ks & 1][nt]);
     }
 }
 
@@ -232,15 +239,12 @@ __global__ void __launch_bounds__(GT, 2)
         const double r0step = exp(-2.0 * wp.h0);
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
-        double afr[KSMAX], w1r[NTMAX];
+        double afr[KSMAX];
         {
             const double u1 = S.nu[1][node], u2 = S.nu[2][node];
 #pragma unroll
             for (int ks = 0; ks < KSMAX; ++ks)
                 afr[ks] = (ks < KS) ? wfun(u2, t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
-#pragma unroll
-            for (int nt = 0; nt < NTMAX; ++nt)
-                w1r[nt] = (nt < Mt) ? wfun(u1, t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
         }
         consumers_sync();
         const bool col_live = warp * 8 < t.count;
@@ -274,8 +278,10 @@ __global__ void __launch_bounds__(GT, 2)
         double acc_re = 0.0, acc_im = 0.0;
 #pragma unroll
         for (int nt = 0; nt < NTMAX; ++nt) {
-            acc_re = fma(w1r[nt], d[nt][0], acc_re);
-            acc_im = fma(w1r[nt], d[nt][1], acc_im);
+            // W1 once per tile, evaluated here so it holds no registers in the slab loop
+            const double w1 = (nt < Mt) ? wfun(S.nu[1][node], t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
+            acc_re = fma(w1, d[nt][0], acc_re);
+            acc_im = fma(w1, d[nt][1], acc_im);
         }
         seq += (uint32_t)t.e0;
         // reduce over the 4 lanes of a node (their rows b differ)
