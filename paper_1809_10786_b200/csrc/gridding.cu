@@ -323,7 +323,7 @@ static_assert(((kBoxMax / 4 + SMT - 1) / SMT) * SMT * 4 <= kBoxMax, "padded M-ti
 struct ScatterSmem {
     double w1[kBoxMax][WS];
     double w2[CTMAX * 8][WS];
-    double w0[SW][SN];                // per-warp row: W0 of the warp's current slab
+    double w0[SW][2][SN];             // per-warp rows: W0 v (re, im) of the warp's current slab
     double2 v[SN];
     double nu[3][SN];
     Tile t;
@@ -333,7 +333,7 @@ struct ScatterSmem {
 // accumulated over the active node k-steps, then reduced into the grid.
 // NCT is a template parameter so no runtime predicate sits around a DMMA.
 template <int NCT>
-__device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double *w0row, int mt0, int ks0, int ks1,
+__device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double (*w0row)[SN], int mt0, int ks0, int ks1,
                                               int g0, const Tile &t, const WindowParams &wp, double *grid,
                                               int lane) {
     const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
@@ -345,8 +345,7 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
 #pragma unroll 2
     for (int ks = ks0; ks < ks1; ++ks) {
         const int n = ks * 4 + kk;
-        const double2 v = S.v[n];
-        const double wv = w0row[n] * (part ? v.y : v.x);
+        const double wv = w0row[part][n];
         double av[SMT];
 #pragma unroll
         for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
@@ -381,7 +380,7 @@ __global__ void __launch_bounds__(STH, 2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double *w0row = S.w0[warp];
+    double (*w0row)[SN] = S.w0[warp];
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         __syncthreads();   // previous tile's readers are done
@@ -416,7 +415,9 @@ __global__ void __launch_bounds__(STH, 2)
 #pragma unroll
             for (int j = 0; j < SN / 32; ++j) {
                 const double w = wfun(S.nu[0][32 * j + lane], t.o0 + a, wp.c0, wp.h0, wp.q);
-                w0row[32 * j + lane] = w;
+                const double2 v = S.v[32 * j + lane];
+                w0row[0][32 * j + lane] = w * v.x;
+                w0row[1][32 * j + lane] = w * v.y;
                 const unsigned m = __ballot_sync(0xffffffffu, w != 0.0);
                 if (m) {
                     kfirst = min(kfirst, (32 * j + __ffs(m) - 1) >> 2);
