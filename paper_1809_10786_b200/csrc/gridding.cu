@@ -102,6 +102,7 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
 
 constexpr int GCW = kTileNodes / 8;   // consumer warps
 constexpr int GT = (GCW + 1) * 32;    // + producer warp
+constexpr int GCPS = 2;               // resident CTAs per SM (3 with NST = 3 and 72 registers: no faster)
 constexpr int NST = 5;                // slab ring depth
 constexpr int SROWS = kBoxMax;        // TMA box rows (axis 1)
 constexpr int SSTR = kBoxMax;         // TMA box width in complex (== 4 mod 8: conflict-free B reads)
@@ -164,7 +165,7 @@ __device__ __forceinline__ void gather_slab(const double *sl, const double (&afr
     }
 }
 
-__global__ void __launch_bounds__(GT, 2)
+__global__ void __launch_bounds__(GT, GCPS)
     k_gather_tiled(const __grid_constant__ CUtensorMap tmap, const Tile *__restrict__ tiles, int64_t ntiles,
                    NodeSet nodes, WindowParams wp, double2 *__restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -610,7 +611,7 @@ int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStrea
     if (!p.generic) {
         const size_t sm = sizeof(GatherSmem);
         SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * 2);
+        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * GCPS);
         if (blocks < 1) blocks = 1;
         k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
     } else {
