@@ -51,6 +51,7 @@ __device__ __forceinline__ void to_u(double tau, int N, double &u, int &lo) {
 
 struct KeyGeom {
     int N0, N1, N2, W1, W2, P2;   // pencils of W1 x W2 cells on axes 1-2, P2 per row
+    uint64_t line_base;           // first key of the grid-line nodes (see k_key)
 };
 
 __global__ void k_warp(const double *pts, int64_t M, double rho, int N0, int N1, int N2, double *u0,
@@ -77,9 +78,19 @@ __global__ void k_key(const double *u0, const double *u1, const double *u2, int6
                       int32_t *idx) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= M) return;
-    const int l0 = (int)floor(u0[i]), l1 = (int)floor(u1[i]), l2 = (int)floor(u2[i]);
-    const uint64_t pencil = (uint64_t)(l1 / g.W1) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W2);
-    key[i] = pencil * (uint64_t)g.N0 + (uint64_t)l0;
+    const double v1 = u1[i], v2 = u2[i];
+    const int l0 = (int)floor(u0[i]), l1 = (int)floor(v1), l2 = (int)floor(v2);
+    // A node exactly on a grid line of axis 1 or 2 has 2q+1 taps there, so in
+    // a W-wide pencil its box would exceed the device slab and cut the tile
+    // short (structured inputs: config 2's lattice puts ~2 % of its nodes on
+    // the phi = k pi/2 and theta = pi/2 planes).  Such nodes get their own
+    // single-cell pencils after all regular ones.
+    if (g.line_base && (v1 == (double)l1 || v2 == (double)l2)) {
+        key[i] = g.line_base + ((uint64_t)l1 * (uint64_t)g.N2 + (uint64_t)l2) * (uint64_t)g.N0 + (uint64_t)l0;
+    } else {
+        const uint64_t pencil = (uint64_t)(l1 / g.W1) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W2);
+        key[i] = pencil * (uint64_t)g.N0 + (uint64_t)l0;
+    }
     idx[i] = (int32_t)i;
 }
 
@@ -197,7 +208,9 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
         SGL_CUDA_CHECK(cudaMalloc(&ns.perm, sizeof(int32_t) * (M ? M : 1)));
     }
     if (M == 0) return SGL_OK;
-    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2};
+    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2, 0};
+    const uint64_t regular = (uint64_t)((p.grid[1] + W1 - 1) / W1) * kg.P2 * (uint64_t)p.grid[0];
+    if (W1 > 1 || W2 > 1) kg.line_base = regular;
     DevBuf<uint64_t> key, key_s;
     DevBuf<int32_t> idx;
     SGL_CUDA_CHECK(key.alloc(M));
@@ -206,7 +219,8 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
     k_key<<<grid_for(M, T), T, 0, st>>>(a0, a1, a2, M, kg, key.p, idx.p);
     SGL_CUDA_CHECK(cudaGetLastError());
     // sort by (pencil, lo0); only the bits in use
-    const uint64_t maxkey = (uint64_t)((p.grid[1] + W1 - 1) / W1) * kg.P2 * (uint64_t)p.grid[0];
+    const uint64_t maxkey =
+        regular + (kg.line_base ? (uint64_t)p.grid[1] * (uint64_t)p.grid[2] * (uint64_t)p.grid[0] : 0);
     int bits = 1;
     while (bits < 64 && (1ull << bits) < maxkey) ++bits;
     {

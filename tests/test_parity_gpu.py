@@ -79,6 +79,23 @@ def test_tiled_and_generic_kernels_agree(sgl, name):
     assert rel(sgl.adjoint(pa, g["values"]), sgl.adjoint(pb, g["values"])) <= 1e-12
 
 
+def test_grid_line_nodes_tiled(sgl):
+    # a Cartesian lattice (config 2's generator) puts many nodes exactly on
+    # grid lines of axes 1-2 (phi = k pi/2, theta = pi/2): they are tiled in
+    # their own single-cell pencils; results equal the per-node kernels and
+    # the oracle, and tiles stay full
+    from oracle import sgl_oracle as o
+    pts = sgl.gen_grid(20, 3.0)
+    rng = np.random.default_rng(5)
+    c = sgl.gen_coeffs(12, rng)
+    v = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    pa, pb = sgl.plan(12, pts, backend="tiled"), sgl.plan(12, pts, backend="generic")
+    fa, aa = sgl.forward(pa, c), sgl.adjoint(pa, v)
+    assert rel(fa, sgl.forward(pb, c)) <= 1e-12 and rel(aa, sgl.adjoint(pb, v)) <= 1e-12
+    op = o.oracle_plan(12, pts)
+    assert rel(fa, o.oracle_forward(op, c)) <= TOL and rel(aa, o.oracle_adjoint(op, v)) <= TOL
+
+
 @pytest.mark.parametrize("B,M,q,rad", [(5, 40, 10, 2.5), (8, 500, 16, 3.0), (16, 3000, 16, 4.0), (6, 200, 20, 2.0)])
 def test_pairing(sgl, B, M, q, rad):
     # <y, F x> == <F^H y, x> (test_transform.py:305-315)
