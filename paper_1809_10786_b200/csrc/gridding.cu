@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(GT, GCPS)
         const int KS = (t.e2 + 3) >> 2;
         double afr[KSMAX];
         {
-            const double u1 = S.nu[1][node], u2 = S.nu[2][node];
+            const double u2 = S.nu[2][node];
 #pragma unroll
             for (int ks = 0; ks < KSMAX; ++ks)
                 afr[ks] = (ks < KS) ? wfun(u2, t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
