@@ -1,0 +1,7 @@
+set -x
+python -m pytest tests -m gpu -q 2>&1 | tail -3
+python bench.py > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+for c in 1 2 4 5; do python bench.py --config $c > gpurun_out/bench_cfg$c.json 2> gpurun_out/bench_cfg$c.err; done
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
+tail -1 gpurun_out/bench_cfg3.err
