@@ -300,10 +300,6 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         *cs[ax] = a / std::sqrt(kTwoPi * lam);                          // nfft.py:137
         *hs[ax] = ((kTwoPi / N) * (kTwoPi / N)) * (a * a) / (2.0 * lam);  // nfft.py:138
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, st);
     int rc = SGL_OK;
     const double *dpts = points;
     double *owned = nullptr;
@@ -356,15 +352,9 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
             t.ready = true;
         }
     }
-    cudaEventRecord(e1, st);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaStreamSynchronize(st);   // the plan is complete (and the caller's points are free) on return
     auto t1 = std::chrono::steady_clock::now();
     p->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    (void)ms;
     if (rc != SGL_OK) {
         free_plan(p);
         return rc;
