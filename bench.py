@@ -106,7 +106,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(work, rho, sample, rank_threads=0):
+def metric_name(cfg: int, direction: str, B: int, K: int) -> str:
+    """BASELINE.json's metric for its headline config; the same wording for
+    the other configs (their parity-bench lines)."""
+    if cfg == 3 and direction == "both":
+        return "NFSGLFT nodes/sec fwd+adj at B=64"
+    d = {"both": "fwd+adj", "fwd": "fwd", "adj": "adj"}[direction]
+    if K > 1 and direction == "fwd":
+        return f"NFSGLFT node-evaluations/sec fwd at B={B} ({K} vectors per plan)"
+    return f"NFSGLFT nodes/sec {d} at B={B}"
+
+
+def cpu_reference(work, rho, sample, direction="both", K=1, rank_threads=0):
     """The reference algorithm on the host (oracle port of the reference path):
     the per-call fixed stages (basal + FFT, both directions) are timed in
     full; the window loops are timed on a rho-pinned S-node sample and scaled
@@ -121,26 +132,42 @@ def cpu_reference(work, rho, sample, rank_threads=0):
     # warm-up (thread pools, first-touch pages), excluded as the reference
     # excludes its JIT warm-up (experiments.py:240-243)
     warm = o.oracle_plan(work.B, work.points[idx[:64]], rho=rho)
-    o.oracle_adjoint(warm, work.values[idx[:64]], threads=threads, workers=workers)
-    o.oracle_forward(warm, c, threads=threads, workers=workers)
-    t0 = time.perf_counter()
-    grid = o.spectral_forward(p, o.basal_forward(p, c), workers)
-    t1 = time.perf_counter()
-    o.gather(grid, p.base, p.win, p.q, threads)
-    t2 = time.perf_counter()
-    g2 = o.scatter(p.grid, p.base, p.win, work.values[idx], p.q, threads)
-    t3 = time.perf_counter()
-    o.basal_adjoint(p, o.spectral_adjoint(p, g2, workers))
-    t4 = time.perf_counter()
-    t_fixed = (t1 - t0) + (t4 - t3)
-    t_node = ((t2 - t1) + (t3 - t2)) / len(idx)
-    T = t_fixed + work.M * t_node
-    return {"value": work.M / T, "unit": "nodes/s", "cores": int(threads), "kind": "port",
-            "sample": (f"oracle port of the reference path; basal+FFT (fwd {t1 - t0:.2f} s, adj {t4 - t3:.2f} s) "
-                       f"timed in full, gather+scatter timed on {len(idx)} rho-pinned nodes "
-                       f"({t_node * 1e6:.1f} us/node) and scaled to M={work.M}; window loops on {threads} "
-                       f"OpenMP threads, scipy.fft on {workers} workers"),
-            "t_fixed_s": t_fixed, "t_node_us": t_node * 1e6}
+    if direction in ("both", "adj"):
+        o.oracle_adjoint(warm, work.values[idx[:64]], threads=threads, workers=workers)
+    if direction in ("both", "fwd"):
+        o.oracle_forward(warm, c, threads=threads, workers=workers)
+    fw, ad = direction in ("both", "fwd"), direction in ("both", "adj")
+    t_ff = t_fa = t_g = t_s = 0.0
+    if fw:
+        t0 = time.perf_counter()
+        grid = o.spectral_forward(p, o.basal_forward(p, c), workers)
+        t1 = time.perf_counter()
+        o.gather(grid, p.base, p.win, p.q, threads)
+        t2 = time.perf_counter()
+        t_ff, t_g = t1 - t0, (t2 - t1) / len(idx)
+        del grid
+    if ad:
+        t2 = time.perf_counter()
+        g2 = o.scatter(p.grid, p.base, p.win, work.values[idx], p.q, threads)
+        t3 = time.perf_counter()
+        o.basal_adjoint(p, o.spectral_adjoint(p, g2, workers))
+        t4 = time.perf_counter()
+        t_fa, t_s = t4 - t3, (t3 - t2) / len(idx)
+    nvec = K if direction == "fwd" else 1
+    # one step: nvec forwards (+ one adjoint); units as the device arm counts them
+    T = nvec * (t_ff + work.M * t_g) + (t_fa + work.M * t_s if ad else 0.0)
+    units = work.M * nvec
+    parts = []
+    if fw:
+        parts.append(f"forward basal+FFT {t_ff:.2f} s in full, gather {t_g * 1e6:.1f} us/node")
+    if ad:
+        parts.append(f"adjoint basal+FFT {t_fa:.2f} s in full, scatter {t_s * 1e6:.1f} us/node")
+    return {"value": units / T, "unit": "nodes/s", "cores": int(threads), "kind": "port",
+            "sample": (f"oracle port of the reference path, {direction}"
+                       + (f" x {nvec} vectors" if nvec > 1 else "") + ": " + "; ".join(parts)
+                       + f"; window loops timed on {len(idx)} rho-pinned nodes and scaled to M={work.M}; "
+                       f"{threads} OpenMP threads, scipy.fft on {workers} workers"),
+            "t_fixed_s": nvec * t_ff + t_fa, "t_node_us": (nvec * t_g + t_s) * 1e6}
 
 
 def run_reference(args, rank, world):
@@ -148,20 +175,25 @@ def run_reference(args, rank, world):
         return
     from paper_1809_10786_b200 import workloads
     w = workloads.config(args.config, M=args.points)
+    direction = args.direction or {"fwd": "fwd", "adj": "adj"}.get(w.directions, "both")
+    K = 1 if w.coeffs.ndim == 1 else w.coeffs.shape[0]
     steps = max(1, min(args.steps, 3))
     vals = []
     base = None
     for i in range(steps + min(args.warmup, 1)):
-        r = cpu_reference(w, w.rho, args.cpu_sample)
+        r = cpu_reference(w, w.rho, args.cpu_sample, direction, K)
         if i >= min(args.warmup, 1):
             vals.append(r["value"])
             base = r
     v = statistics.median(vals)
-    line = {"metric": "NFSGLFT nodes/sec fwd+adj at B=64", "impl": "reference", "value": v, "unit": "nodes/s",
+    line = {"metric": metric_name(args.config, direction, w.B, K), "impl": "reference", "value": v,
+            "unit": "nodes/s",
             "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
-            "ms_per_step": 1e3 * w.M / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * w.M * (K if direction == "fwd" else 1) / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic (seeded PCG64, SURVEY 8(d))",
-            "config": {"workload": w.name, "B": w.B, "M": w.M, "q": 16, "sigma": 2},
+            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": 16, "sigma": 2,
+                       "direction": direction, "vectors": K},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": ("the reference is a pure-Python package; this arm times the oracle port of its algorithm "
@@ -329,8 +361,9 @@ def main():
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+        if args.config == 3 and w.M == 10_000_000:   # the configuration the ncu capture was taken on
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(dom)
     except Exception:
         pass
     roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": FP64_PEAK_TFLOPS,
@@ -341,15 +374,18 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            r = cpu_reference(w, rho, args.cpu_sample)
+            r = cpu_reference(w, rho, args.cpu_sample, direction, K)
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "nodes/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
 
+    grid_gb = 16.0 * float(np.prod(p.nfft.grid_shape)) / 1e9 if p.nfft else 0.0
+    node_gb = w.M * (3 * 8 * 2 + 4 * 2 + 16) / 1e9   # sorted u0..u2 + perm (gather and scatter orders) + values
+    l2_note = (f"{'inputs larger than L2' if grid_gb + node_gb > 0.126 else 'working set fits L2 (126 MB)'} "
+               f"(grid {grid_gb:.3g} GB, node arrays {node_gb:.3g} GB per rank)")
     if rank == 0:
         line = {
-            "metric": ("NFSGLFT nodes/sec fwd+adj at B=64" if (args.config == 3 and direction == "both")
-                       else f"NFSGLFT nodes/sec {direction} at B={w.B}"),
+            "metric": metric_name(args.config, direction, w.B, K),
             "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128",
@@ -357,7 +393,7 @@ def main():
             "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": q, "sigma": 2, "direction": direction,
                        "vectors": K,
                        "grid": list(p.nfft.grid_shape), "rho": rho,
-                       "l2": "inputs larger than L2 (grid 1.07 GB, node arrays 0.28 GB per rank)",
+                       "l2": l2_note,
                        "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": args.steps * (4 * K * (direction != "adj") + 4 * (direction != "fwd")),
