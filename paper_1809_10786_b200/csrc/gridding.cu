@@ -324,7 +324,8 @@ static_assert(((kBoxMax / 4 + SMT - 1) / SMT) * SMT * 4 <= kBoxMax, "padded M-ti
 struct ScatterSmem {
     double w1[kBoxMax][WS];
     double w2[CTMAX * 8][WS];
-    double w0[SW][2][SN];             // per-warp rows: W0 v (re, im) of the warp's current slab
+    double w0[SW][2][WS];             // per-warp rows: W0 v (re, im) of the warp's current slab
+                                      // (pitch WS: the re and im rows sit in different banks)
     double2 v[SN];
     double nu[3][SN];
     Tile t;
@@ -334,7 +335,7 @@ struct ScatterSmem {
 // accumulated over the active node k-steps, then reduced into the grid.
 // NCT is a template parameter so no runtime predicate sits around a DMMA.
 template <int NCT>
-__device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double (*w0row)[SN], int mt0, int ks0, int ks1,
+__device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double (*w0row)[WS], int mt0, int ks0, int ks1,
                                               int g0, const Tile &t, const WindowParams &wp, double *grid,
                                               int lane) {
     const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(STH, 2)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double (*w0row)[SN] = S.w0[warp];
+    double (*w0row)[WS] = S.w0[warp];
 
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         __syncthreads();   // previous tile's readers are done
