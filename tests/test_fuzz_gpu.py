@@ -1,0 +1,54 @@
+"""Seeded random plans (bandwidth, cutoff, oversampling, compact grid, node
+distribution, explicit rho) through the tiled and per-node kernels against
+the oracle: catches tiling / halo / sigma-escalation corner cases the fixed
+goldens do not enumerate."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(x, ref):
+    return float(np.max(np.abs(np.asarray(x) - ref)) / np.max(np.abs(ref)))
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 11))
+    sigma = int(rng.choice([2, 2, 3, 4]))
+    q = int(rng.integers(1, min(17, 4 * sigma * B)))
+    compact = bool(rng.random() < 0.3)
+    M = int(rng.integers(1, 1500))
+    kind = rng.integers(0, 3)
+    if kind == 0:      # ball
+        r = 3.0 * rng.random(M) ** (1 / 3)
+    elif kind == 1:    # clustered near the origin and the shell
+        r = np.where(rng.random(M) < 0.5, 0.05 * rng.random(M), 3.0 - 1e-3 * rng.random(M))
+    else:              # a few distinct radii (lattice-like)
+        r = rng.choice([0.0, 0.5, 1.5, 3.0], M)
+    th = np.arccos(rng.uniform(-1, 1, M))
+    ph = rng.uniform(0, 2 * np.pi, M)
+    if kind == 2:      # axis-aligned angles put nodes on grid lines
+        th = rng.choice([0.0, np.pi / 2, np.pi], M)
+        ph = rng.choice([0.0, np.pi / 2, np.pi, 3 * np.pi / 2], M)
+    pts = np.column_stack([r, th, ph])
+    rho = None if rng.random() < 0.7 else 3.5
+    return B, sigma, q, compact, pts, rho, rng
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_plan_matches_oracle(seed):
+    import paper_1809_10786_b200 as sgl
+    from oracle import sgl_oracle as o
+    B, sigma, q, compact, pts, rho, rng = _case(seed)
+    if np.all(pts[:, 0] == 0) and rho is None:
+        rho = 1.0
+    c = sgl.gen_coeffs(B, rng)
+    v = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    op = o.oracle_plan(B, pts, sigma=sigma, q=q, rho=rho, compact_k1=compact)
+    f_ref, a_ref = o.oracle_forward(op, c), o.oracle_adjoint(op, v)
+    for backend in ("auto", "generic"):
+        p = sgl.plan(B, pts, sigma=sigma, q=q, rho=rho, compact_k1=compact, backend=backend)
+        assert p.nfft.grid_shape == tuple(op.grid)
+        assert rel(sgl.forward(p, c), f_ref) <= 1e-10, (backend, B, sigma, q, compact)
+        assert rel(sgl.adjoint(p, v), a_ref) <= 1e-10, (backend, B, sigma, q, compact)
