@@ -40,6 +40,29 @@ __device__ __forceinline__ double wfun(double u, int cell, double c, double h, i
     return (fabs(d) <= (double)q) ? c * exp(-d * d * h) : 0.0;
 }
 
+// w(j) = wfun(u, o + s j) for j = 0 .. N-1 (j < n live, 0 beyond) by the
+// Gaussian's two-term recurrence w(j+1) = w(j) r(j), r(j+1) = r(j) e^{-2 h s^2},
+// seeded exactly at the first j inside the window; d = u - (o + s j) is formed
+// exactly as wfun forms it, so the truncation |d| <= q is bit-identical and
+// the values differ from wfun's by a few ulps.  3 exps instead of N.
+template <int N, int S>
+__device__ __forceinline__ void wwalk(double u, int o, int n, double c, double h, int q, double (&w)[N]) {
+    const double base = u - (double)o;
+    const int j0 = max(0, (int)ceil((base - q) / S));
+    const double d0 = base - (double)(S * j0);
+    double cur = c * exp(-d0 * d0 * h), r = exp(h * (2.0 * S * d0 - (double)(S * S)));
+    const double rs = exp(-2.0 * h * (double)(S * S));
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double d = base - (double)(S * j);
+        w[j] = (j >= j0 && j < n && fabs(d) <= (double)q) ? cur : 0.0;
+        if (j >= j0) {
+            cur *= r;
+            r *= rs;
+        }
+    }
+}
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d[0]), "+d"(d[1])
@@ -241,12 +264,7 @@ __global__ void __launch_bounds__(GT, GCPS)
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
         double afr[KSMAX];
-        {
-            const double u2 = S.nu[2][node];
-#pragma unroll
-            for (int ks = 0; ks < KSMAX; ++ks)
-                afr[ks] = (ks < KS) ? wfun(u2, t.o2 + ks * 4 + cc, wp.c2, wp.h2, wp.q) : 0.0;
-        }
+        wwalk<KSMAX, 4>(S.nu[2][node], t.o2 + cc, KS, wp.c2, wp.h2, wp.q, afr);
         consumers_sync();
         const bool col_live = warp * 8 < t.count;
         double d[NTMAX][2];
@@ -277,12 +295,15 @@ __global__ void __launch_bounds__(GT, GCPS)
             if (lane == 0) mbar_arrive(&S.empty[buf]);
         }
         double acc_re = 0.0, acc_im = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NTMAX; ++nt) {
+        {
             // W1 once per tile, evaluated here so it holds no registers in the slab loop
-            const double w1 = (nt < Mt) ? wfun(S.nu[1][node], t.o1 + nt * 4 + cc, wp.c1, wp.h1, wp.q) : 0.0;
-            acc_re = fma(w1, d[nt][0], acc_re);
-            acc_im = fma(w1, d[nt][1], acc_im);
+            double w1[NTMAX];
+            wwalk<NTMAX, 4>(S.nu[1][node], t.o1 + cc, Mt, wp.c1, wp.h1, wp.q, w1);
+#pragma unroll
+            for (int nt = 0; nt < NTMAX; ++nt) {
+                acc_re = fma(w1[nt], d[nt][0], acc_re);
+                acc_im = fma(w1[nt], d[nt][1], acc_im);
+            }
         }
         seq += (uint32_t)t.e0;
         // reduce over the 4 lanes of a node (their rows b differ)
@@ -400,14 +421,25 @@ __global__ void __launch_bounds__(STH, 2)
         __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
         const int CT = (t.e2 + 7) >> 3;
-        // every row up to the groups' extent (formula gives 0 outside the box)
-        for (int i = tid; i < ((Mt + SMT - 1) / SMT) * SMT * 4 * SN; i += STH) {
-            const int y = i / SN, k = i % SN;
-            S.w1[y][k] = wfun(S.nu[1][k], t.o1 + y, wp.c1, wp.h1, wp.q);
-        }
-        for (int i = tid; i < CT * 8 * SN; i += STH) {
-            const int y = i / SN, k = i % SN;
-            S.w2[y][k] = wfun(S.nu[2][k], t.o2 + y, wp.c2, wp.h2, wp.q);
+        // W1 / W2 tables: one thread per (node, axis) walks the rows with the
+        // Gaussian recurrence (every row up to the groups' extent; 0 outside the box)
+        static_assert(STH == 2 * SN, "one thread per node and table");
+        {
+            const int k = tid % SN;
+            if (tid < SN) {
+                double w[kBoxMax];
+                wwalk<kBoxMax, 1>(S.nu[1][k], t.o1, kBoxMax, wp.c1, wp.h1, wp.q, w);
+                const int rows = ((Mt + SMT - 1) / SMT) * SMT * 4;
+#pragma unroll
+                for (int y = 0; y < kBoxMax; ++y)
+                    if (y < rows) S.w1[y][k] = w[y];
+            } else {
+                double w[CTMAX * 8];
+                wwalk<CTMAX * 8, 1>(S.nu[2][k], t.o2, CTMAX * 8, wp.c2, wp.h2, wp.q, w);
+#pragma unroll
+                for (int y = 0; y < CTMAX * 8; ++y)
+                    if (y < CT * 8) S.w2[y][k] = w[y];
+            }
         }
         __syncthreads();
         const int nks = (t.count + 3) >> 2;
