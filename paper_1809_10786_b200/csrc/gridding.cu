@@ -443,12 +443,33 @@ __global__ void __launch_bounds__(STH, 2)
         }
         __syncthreads();
         const int nks = (t.count + 3) >> 2;
+        // W0 along this warp's slabs a = warp, warp + SW, ...: per node the
+        // Gaussian recurrence with stride SW, seeded exactly at the node's
+        // first in-window slab of the warp (2 exps per node instead of one
+        // per slab); the truncation |d| <= q is tested on the exact d
+        double w0s[SN / 32], r0s[SN / 32];
+        int a0s[SN / 32];
+        const double r0step = exp(-2.0 * wp.h0 * (double)(SW * SW));
+#pragma unroll
+        for (int j = 0; j < SN / 32; ++j) {
+            const double F = S.nu[0][32 * j + lane] - (double)t.o0;
+            const int k0 = max(0, (int)ceil((ceil(F - wp.q) - warp) / (double)SW));
+            a0s[j] = warp + SW * k0;
+            const double df = F - (double)a0s[j];
+            w0s[j] = wp.c0 * exp(-df * df * wp.h0);
+            r0s[j] = exp(wp.h0 * (2.0 * SW * df - (double)(SW * SW)));
+        }
         for (int a = warp; a < t.e0; a += SW) {
             // W0 of this slab for all nodes; active k-steps from the nonzero mask
             int kfirst = SKS, klast = -1;
 #pragma unroll
             for (int j = 0; j < SN / 32; ++j) {
-                const double w = wfun(S.nu[0][32 * j + lane], t.o0 + a, wp.c0, wp.h0, wp.q);
+                const double dl = S.nu[0][32 * j + lane] - (double)(t.o0 + a);
+                const double w = (a >= a0s[j] && fabs(dl) <= (double)wp.q) ? w0s[j] : 0.0;
+                if (a >= a0s[j]) {
+                    w0s[j] *= r0s[j];
+                    r0s[j] *= r0step;
+                }
                 const double2 v = S.v[32 * j + lane];
                 w0row[0][32 * j + lane] = w * v.x;
                 w0row[1][32 * j + lane] = w * v.y;
