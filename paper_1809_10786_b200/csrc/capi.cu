@@ -300,6 +300,12 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         *cs[ax] = a / std::sqrt(kTwoPi * lam);                          // nfft.py:137
         *hs[ax] = ((kTwoPi / N) * (kTwoPi / N)) * (a * a) / (2.0 * lam);  // nfft.py:138
     }
+    wp.r0_1 = std::exp(-2.0 * wp.h0);
+    wp.r0_8 = std::exp(-2.0 * wp.h0 * 64.0);
+    wp.r1_1 = std::exp(-2.0 * wp.h1);
+    wp.r1_4 = std::exp(-2.0 * wp.h1 * 16.0);
+    wp.r2_1 = std::exp(-2.0 * wp.h2);
+    wp.r2_4 = std::exp(-2.0 * wp.h2 * 16.0);
     int rc = SGL_OK;
     const double *dpts = points;
     double *owned = nullptr;

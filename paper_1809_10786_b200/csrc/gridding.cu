@@ -46,12 +46,11 @@ __device__ __forceinline__ double wfun(double u, int cell, double c, double h, i
 // exactly as wfun forms it, so the truncation |d| <= q is bit-identical and
 // the values differ from wfun's by a few ulps.  3 exps instead of N.
 template <int N, int S>
-__device__ __forceinline__ void wwalk(double u, int o, int n, double c, double h, int q, double (&w)[N]) {
+__device__ __forceinline__ void wwalk(double u, int o, int n, double c, double h, double rs, int q, double (&w)[N]) {
     const double base = u - (double)o;
     const int j0 = max(0, (int)ceil((base - q) / S));
     const double d0 = base - (double)(S * j0);
     double cur = c * exp(-d0 * d0 * h), r = exp(h * (2.0 * S * d0 - (double)(S * S)));
-    const double rs = exp(-2.0 * h * (double)(S * S));
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const double d = base - (double)(S * j);
@@ -260,11 +259,11 @@ __global__ void __launch_bounds__(GT, GCPS)
             w0r = wp.c0 * exp(-d * d * wp.h0);
             r0r = exp(wp.h0 * (2.0 * d - 1.0));
         }
-        const double r0step = exp(-2.0 * wp.h0);
+        const double r0step = wp.r0_1;
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
         double afr[KSMAX];
-        wwalk<KSMAX, 4>(S.nu[2][node], t.o2 + cc, KS, wp.c2, wp.h2, wp.q, afr);
+        wwalk<KSMAX, 4>(S.nu[2][node], t.o2 + cc, KS, wp.c2, wp.h2, wp.r2_4, wp.q, afr);
         consumers_sync();
         const bool col_live = warp * 8 < t.count;
         double d[NTMAX][2];
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(GT, GCPS)
         {
             // W1 once per tile, evaluated here so it holds no registers in the slab loop
             double w1[NTMAX];
-            wwalk<NTMAX, 4>(S.nu[1][node], t.o1 + cc, Mt, wp.c1, wp.h1, wp.q, w1);
+            wwalk<NTMAX, 4>(S.nu[1][node], t.o1 + cc, Mt, wp.c1, wp.h1, wp.r1_4, wp.q, w1);
 #pragma unroll
             for (int nt = 0; nt < NTMAX; ++nt) {
                 acc_re = fma(w1[nt], d[nt][0], acc_re);
@@ -428,14 +427,14 @@ __global__ void __launch_bounds__(STH, 2)
             const int k = tid % SN;
             if (tid < SN) {
                 double w[kBoxMax];
-                wwalk<kBoxMax, 1>(S.nu[1][k], t.o1, kBoxMax, wp.c1, wp.h1, wp.q, w);
+                wwalk<kBoxMax, 1>(S.nu[1][k], t.o1, kBoxMax, wp.c1, wp.h1, wp.r1_1, wp.q, w);
                 const int rows = ((Mt + SMT - 1) / SMT) * SMT * 4;
 #pragma unroll
                 for (int y = 0; y < kBoxMax; ++y)
                     if (y < rows) S.w1[y][k] = w[y];
             } else {
                 double w[CTMAX * 8];
-                wwalk<CTMAX * 8, 1>(S.nu[2][k], t.o2, CTMAX * 8, wp.c2, wp.h2, wp.q, w);
+                wwalk<CTMAX * 8, 1>(S.nu[2][k], t.o2, CTMAX * 8, wp.c2, wp.h2, wp.r2_1, wp.q, w);
 #pragma unroll
                 for (int y = 0; y < CTMAX * 8; ++y)
                     if (y < CT * 8) S.w2[y][k] = w[y];
@@ -449,7 +448,8 @@ __global__ void __launch_bounds__(STH, 2)
         // per slab); the truncation |d| <= q is tested on the exact d
         double w0s[SN / 32], r0s[SN / 32];
         int a0s[SN / 32];
-        const double r0step = exp(-2.0 * wp.h0 * (double)(SW * SW));
+        static_assert(SW == 8, "the stride-8 ratio wp.r0_8 assumes 8 warps");
+        const double r0step = wp.r0_8;
 #pragma unroll
         for (int j = 0; j < SN / 32; ++j) {
             const double F = S.nu[0][32 * j + lane] - (double)t.o0;

@@ -52,6 +52,10 @@ struct WindowParams {
     int32_t q;
     double c0, c1, c2;          // (N/2pi)/sqrt(2 pi lam)
     double h0, h1, h2;          // 1/(2 lam)
+    // recurrence ratios e^{-2 h s^2} of the Gaussian walks (stride s in cells)
+    double r0_1, r0_8;          // axis 0: s = 1 (gather), s = 8 (scatter warp stride)
+    double r1_1, r1_4;          // axis 1: s = 1 (scatter table), s = 4 (gather fragments)
+    double r2_1, r2_4;          // axis 2
 };
 
 struct StageTimer {
