@@ -583,18 +583,27 @@ __global__ void __launch_bounds__(NW_GEN * 32)
 // periodic halo of the padded grid (axes 1-2)
 
 // copy interior images into the halo (after the inverse FFT, before gather)
+// copy interior images into the halo (after the inverse FFT).  One thread
+// per halo cell of a plane (blockIdx.y = axis-0 plane): the q-row bands above
+// and below the interior (full padded width) and the q-column strips beside
+// it; 32-bit index math, no pass over the interior.
 __global__ void k_halo_fill(WindowParams wp, double2 *__restrict__ grid) {
-    const int64_t n = (int64_t)wp.N0 * wp.N1p * wp.N2p;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int p2 = (int)(i % wp.N2p);
-        const int64_t r = i / wp.N2p;
-        const int p1 = (int)(r % wp.N1p);
-        const int64_t g0 = r / wp.N1p;
-        const bool in1 = p1 >= wp.q && p1 < wp.q + wp.N1, in2 = p2 >= wp.q && p2 < wp.q + wp.N2;
-        if (in1 && in2) continue;
-        const int s1 = wrapi(p1 - wp.q, wp.N1) + wp.q, s2 = wrapi(p2 - wp.q, wp.N2) + wp.q;
-        grid[i] = grid[((size_t)g0 * wp.N1p + s1) * wp.N2p + s2];
+    const int q = wp.q, band = 2 * q * wp.N2p, per_plane = band + 2 * q * wp.N1;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= per_plane) return;
+    int p1, p2;
+    if (r < band) {
+        const int k = r / wp.N2p;
+        p1 = k < q ? k : wp.N1 + k;            // rows [0, q) and [N1 + q, N1 + 2q)
+        p2 = r - k * wp.N2p;
+    } else {
+        const int s = r - band, k = s / (2 * q), cc = s - k * (2 * q);
+        p1 = q + k;
+        p2 = cc < q ? cc : wp.N2 + cc;          // columns [0, q) and [N2 + q, N2 + 2q)
     }
+    const int s1 = wrapi(p1 - q, wp.N1) + q, s2 = wrapi(p2 - q, wp.N2) + q;
+    double2 *plane = grid + (size_t)blockIdx.y * wp.N1p * wp.N2p;
+    plane[(size_t)p1 * wp.N2p + p2] = plane[(size_t)s1 * wp.N2p + s2];
 }
 
 // add the halo images back into the interior (after scatter, before FFT).
@@ -622,28 +631,26 @@ __device__ __forceinline__ void fold_cell(const WindowParams &wp, double2 *grid,
 }
 
 __global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
+    // blockIdx.y = axis-0 plane; 32-bit index math within the plane
     const int q1 = min(wp.q, wp.N1), q2 = min(wp.q, wp.N2);
     const int band_rows = min(wp.N1, 2 * q1);              // rows [0,q) and [N1-q, N1)
     const int strip = min(wp.N2, 2 * q2);                   // columns [0,q) and [N2-q, N2)
-    const int64_t per_plane = (int64_t)band_rows * wp.N2 + (int64_t)(wp.N1 - band_rows) * strip;
-    const int64_t n = (int64_t)wp.N0 * per_plane;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g0 = i / per_plane;
-        int64_t r = i - g0 * per_plane;
-        int i1, i2;
-        if (r < (int64_t)band_rows * wp.N2) {
-            const int k = (int)(r / wp.N2);
-            i1 = k < q1 ? k : wp.N1 - band_rows + k;
-            i2 = (int)(r - (int64_t)k * wp.N2);
-        } else {
-            r -= (int64_t)band_rows * wp.N2;
-            const int k = (int)(r / strip);
-            i1 = q1 + k;
-            const int c = (int)(r - (int64_t)k * strip);
-            i2 = c < q2 ? c : wp.N2 - strip + c;
-        }
-        fold_cell(wp, grid, g0, i1, i2);
+    const int per_plane = band_rows * wp.N2 + (wp.N1 - band_rows) * strip;
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= per_plane) return;
+    int i1, i2;
+    if (r < band_rows * wp.N2) {
+        const int k = r / wp.N2;
+        i1 = k < q1 ? k : wp.N1 - band_rows + k;
+        i2 = r - k * wp.N2;
+    } else {
+        r -= band_rows * wp.N2;
+        const int k = r / strip;
+        i1 = q1 + k;
+        const int cc = r - k * strip;
+        i2 = cc < q2 ? cc : wp.N2 - strip + cc;
     }
+    fold_cell(wp, grid, blockIdx.y, i1, i2);
 }
 
 int g_num_sms = 0;
@@ -708,13 +715,19 @@ int make_grid_tmap(Plan &p) {
 }
 
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st) {
-    k_halo_fill<<<num_sms() * 8, 256, 0, st>>>(p.wp, grid);
+    if (p.wp.q == 0) return SGL_OK;
+    const int per_plane = 2 * p.wp.q * p.wp.N2p + 2 * p.wp.q * p.wp.N1;
+    k_halo_fill<<<dim3((per_plane + 255) / 256, p.wp.N0), 256, 0, st>>>(p.wp, grid);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
 
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st) {
-    k_halo_fold<<<num_sms() * 8, 256, 0, st>>>(p.wp, grid);
+    if (p.wp.q == 0) return SGL_OK;
+    const int q1 = std::min(p.wp.q, p.wp.N1), q2 = std::min(p.wp.q, p.wp.N2);
+    const int band_rows = std::min(p.wp.N1, 2 * q1), strip = std::min(p.wp.N2, 2 * q2);
+    const int per_plane = band_rows * p.wp.N2 + (p.wp.N1 - band_rows) * strip;
+    k_halo_fold<<<dim3((per_plane + 255) / 256, p.wp.N0), 256, 0, st>>>(p.wp, grid);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
