@@ -371,6 +371,22 @@ def main():
             "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
             "algorithmic": f"{flop_per_node:.0f} FLOP/node x {w.M} nodes per launch"}
 
+    # whole-step roofline: window FLOPs at the FP64 peak + the
+    # FFTs at the HBM copy bandwidth (3 passes x read+write x 16 B per cell)
+    hbm_gbs = 6534.1
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_gbs = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        pass
+    n_fwd, n_adj = (K if direction in ("both", "fwd") else 0), (1 if direction in ("both", "adj") else 0)
+    cells = float(np.prod(p.nfft.grid_shape)) if p.nfft else 0.0
+    t_win = (n_fwd + n_adj) * w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    t_fft = (n_fwd + n_adj) * 3 * 2 * 16.0 * cells / (hbm_gbs * 1e9) * 1e3
+    step_roof = {"t_roof_ms": t_win + t_fft, "window_ms": t_win, "fft_ms": t_fft, "frac": (t_win + t_fft) / ms,
+                 "model": "window FLOPs / 37.1 TF/s (FP64 DMMA peak) + 3-pass FFT bytes / HBM copy GB/s "
+                          "(MEASURED_PEAKS.json); basal and halo work not counted"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -395,7 +411,7 @@ def main():
                        "grid": list(p.nfft.grid_shape), "rho": rho,
                        "l2": l2_note,
                        "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": args.steps * (4 * K * (direction != "adj") + 4 * (direction != "fwd")),
             "gpu_launches_note": "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled; per adjoint: "
                                  "scatter_tiled, halo_fold, sph_adj, radial_adj (+ cuFFT and memsets, library calls)",
