@@ -15,6 +15,11 @@
  *   sgl_last_error    <- the ValueError message text raised by the above
  *   sgl_plan_get_info <- SglPlan / NfftPlan fields (transform.py:292-317,
  *                        nfft.py:101-120)
+ *   sgl_nfft_plan_create <- nfft.nfft_plan (nfft.py:147-207): a plain 3-D
+ *                        NFFT plan; sgl_forward / sgl_adjoint on it are
+ *                        nfft_execute / nfft_adjoint_execute (nfft.py:234-273)
+ *                        (with SGL_FLAG_EXACT_LAST_STAGE: ndft / ndft_adjoint,
+ *                        nfft.py:51-82)
  *   sgl_direct_forward  <- transform.evaluate_direct         (transform.py:95-117)
  *   sgl_direct_adjoint  <- transform.evaluate_direct_adjoint (transform.py:120-139)
  *
@@ -110,6 +115,17 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
                         const sgl_cdouble *values_in, sgl_cdouble *coeffs_out, void *stream);
 
 void sgl_plan_destroy(sgl_plan *plan);
+
+/* Plain 3-D NFFT on the torus (the reference's NFFT layer): trigonometric
+ * polynomial coefficients on I_n = prod [-n_j/2, n_j/2) in the centred layout
+ * (position p on axis j holds frequency p - n_j/2), nodes (M x 3) reduced
+ * into [0, 2 pi).  n_axis[j] even >= 2; oversampled length pow2(sigma n_j);
+ * q must be below every oversampled length (no escalation).  Use sgl_forward
+ * (coefficients: n0*n1*n2, K vectors) and sgl_adjoint on the plan.
+ * Flags: SGL_FLAG_EXACT_LAST_STAGE (direct NDFT), SGL_FLAG_GENERIC_GRIDDING,
+ * SGL_FLAG_PROFILE. */
+int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, int32_t sigma, int32_t q,
+                         uint32_t flags, void *stream, sgl_plan **out);
 
 /* Direct summation of the expansion (no plan, O(M * count) FP64; the
  * reference's verification path and the CLI's --method naive).

@@ -21,7 +21,7 @@ STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares
 EXPORTS = (
-    "sgl_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_direct_forward",
+    "sgl_plan_create", "sgl_nfft_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_direct_forward",
     "sgl_direct_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
 )
@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
     L.sgl_forward.restype = ctypes.c_int
     L.sgl_adjoint.argtypes = [vp, vp, vp, vp]
     L.sgl_adjoint.restype = ctypes.c_int
+    L.sgl_nfft_plan_create.argtypes = [vp, ctypes.c_int64, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp, vp]
+    L.sgl_nfft_plan_create.restype = ctypes.c_int
     L.sgl_forward_adjoint.argtypes = [vp, vp, vp, vp, vp, vp]
     L.sgl_forward_adjoint.restype = ctypes.c_int
     for fn in (L.sgl_direct_forward, L.sgl_direct_adjoint):

@@ -130,7 +130,7 @@ int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRe
         if (rec) rec->mark(s);
     };
     mark(SGL_STAGE_BASAL);
-    int rc = launch_basal_forward(p, c, p.grid_buf, st, nullptr);
+    int rc = p.raw ? launch_place_raw(p, c, p.grid_buf, st) : launch_basal_forward(p, c, p.grid_buf, st, nullptr);
     if (rc) return rc;
     if (p.exact) {   // direct NDFT of eta (transform.py:393-394)
         mark(SGL_STAGE_WINDOW);
@@ -172,13 +172,18 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
         if (rc) return rc;
     }
     mark(SGL_STAGE_BASAL);
-    return launch_basal_adjoint(p, p.grid_buf, c, st);
+    return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
 }
 
 }  // namespace
 }  // namespace sgl
 
 using namespace sgl;
+
+namespace {
+int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
+                std::chrono::steady_clock::time_point t0);
+}  // namespace
 
 extern "C" {
 
@@ -279,6 +284,20 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         p->s_eff[ax] = (double)p->grid[ax] / p->n_axis[ax];
         p->lam[ax] = p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
     }
+    return plan_finish(p, points, st, out, t0);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Shared second half of plan creation: window constants, halo geometry,
+// nodes, tables, buffers, cuFFT plan, TMA descriptor.
+int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
+                std::chrono::steady_clock::time_point t0) {
+    const int64_t M = p->M;
+    const int q = p->q;
+    const bool exact = p->exact;
     WindowParams &wp = p->wp;
     wp.N0 = p->grid[0];
     wp.N1 = p->grid[1];
@@ -322,10 +341,10 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         cudaStreamSynchronize(st);
         cudaFree(owned);
     }
-    if (rc == SGL_OK) rc = build_basal_tables(*p);
+    if (rc == SGL_OK) rc = p->raw ? build_deconv_tables(*p) : build_basal_tables(*p);
     if (rc == SGL_OK) {
         if (cudaMalloc(&p->grid_buf, sizeof(double2) * p->grid_elems) != cudaSuccess ||
-            cudaMalloc(&p->beta, sizeof(double2) * (size_t)B * B * 4 * B) != cudaSuccess ||
+            cudaMalloc(&p->beta, sizeof(double2) * (size_t)std::max(1, p->B * p->B * 4 * p->B)) != cudaSuccess ||
             cudaMalloc(&p->coef_buf, sizeof(double2) * p->count) != cudaSuccess ||
             cudaMalloc(&p->val_buf, sizeof(double2) * (M ? M : 1)) != cudaSuccess) {
             cudaGetLastError();
@@ -373,6 +392,80 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     }
     *out = reinterpret_cast<sgl_plan *>(p);
     return SGL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, int32_t sigma, int32_t q,
+                         uint32_t flags, void *stream, sgl_plan **out) {
+    g_err.clear();
+    if (!out || !n_axis) {
+        set_error("NULL n_axis or output plan pointer");
+        return SGL_EINVAL;
+    }
+    *out = nullptr;
+    // nfft.py:164-176
+    for (int ax = 0; ax < 3; ++ax)
+        if (n_axis[ax] < 2 || n_axis[ax] % 2) {
+            set_error("per-axis degree must be even and >= 2");
+            return SGL_EINVAL;
+        }
+    if (M < 0 || (M > 0 && !nodes)) {
+        set_error("nodes must be (m, d)");
+        return SGL_EINVAL;
+    }
+    if (M > (int64_t)INT32_MAX) {
+        set_error("more than 2^31-1 points per plan: shard the node set");
+        return SGL_EUNSUPPORTED;
+    }
+    const bool exact = flags & SGL_FLAG_EXACT_LAST_STAGE;
+    auto pow2 = [](int64_t v) {
+        int64_t g = 1;
+        while (g < v) g <<= 1;
+        return g;
+    };
+    if (!exact) {
+        if (sigma < 2) {
+            set_error("oversampling factor must be an integer >= 2");
+            return SGL_EINVAL;
+        }
+        if (q < 1) {
+            set_error("cutoff parameter must be >= 1");
+            return SGL_EINVAL;
+        }
+        int64_t gmin = INT64_MAX;
+        for (int ax = 0; ax < 3; ++ax) gmin = std::min<int64_t>(gmin, pow2((int64_t)sigma * n_axis[ax]));
+        if (q >= gmin) {
+            set_error("cutoff q = " + std::to_string(q) + " must be below sigma*n = " + std::to_string(gmin));
+            return SGL_EINVAL;
+        }
+    } else {
+        q = 0;
+        sigma = 1;
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    Plan *p = new Plan();
+    cudaGetDevice(&p->device);
+    p->raw = true;
+    p->B = 0;
+    p->M = M;
+    p->rho = 1.0;
+    p->sigma = sigma;
+    p->q = q;
+    p->profile = flags & SGL_FLAG_PROFILE;
+    p->exact = exact;
+    p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
+    p->count = (int64_t)n_axis[0] * n_axis[1] * n_axis[2];
+    for (int ax = 0; ax < 3; ++ax) {   // nfft.py:174, 181-182 (no sigma escalation in the NFFT layer)
+        p->n_axis[ax] = n_axis[ax];
+        p->sig_axes[ax] = sigma;
+        p->grid[ax] = exact ? n_axis[ax] : (int)pow2((int64_t)sigma * n_axis[ax]);
+        p->s_eff[ax] = (double)p->grid[ax] / n_axis[ax];
+        p->lam[ax] = exact ? 0.0 : p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
+    }
+    return plan_finish(p, nodes, (cudaStream_t)stream, out, t0);
 }
 
 void sgl_plan_destroy(sgl_plan *plan) { free_plan(reinterpret_cast<Plan *>(plan)); }

@@ -49,6 +49,16 @@ __device__ __forceinline__ void to_u(double tau, int N, double &u, int &lo) {
     }
 }
 
+// plain NFFT nodes: already on the torus (nfft.py:177-178, 131-133)
+__global__ void k_torus(const double *pts, int64_t M, int N0, int N1, int N2, double *u0, double *u1, double *u2) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    int l;
+    to_u(reduce_2pi(pts[3 * i]), N0, u0[i], l);
+    to_u(reduce_2pi(pts[3 * i + 1]), N1, u1[i], l);
+    to_u(reduce_2pi(pts[3 * i + 2]), N2, u2[i], l);
+}
+
 struct KeyGeom {
     int N0, N1, N2, W1, W2, P2;   // pencils of W1 x W2 cells on axes 1-2, P2 per row
     uint64_t line_base;           // first key of the grid-line nodes (see k_key)
@@ -304,7 +314,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     const int64_t M = p.M;
     const int T = 256;
     // rho: explicit, or the largest radius (choose_rho, transform.py:39-43)
-    if (!(p.rho > 0)) {
+    if (!p.raw && !(p.rho > 0)) {
         double rmax = 0.0;
         if (M > 0) {
             DevBuf<double> r, out;
@@ -321,7 +331,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         }
         p.rho = rmax > 0 ? rmax : 1.0;
     }
-    if (M > 0) {
+    if (M > 0 && !p.raw) {
         DevBuf<int> bad;
         SGL_CUDA_CHECK(bad.alloc(1));
         SGL_CUDA_CHECK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
@@ -339,7 +349,10 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     SGL_CUDA_CHECK(a1.alloc(M));
     SGL_CUDA_CHECK(a2.alloc(M));
     if (M > 0) {
-        k_warp<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
+        if (p.raw)
+            k_torus<<<grid_for(M, T), T, 0, st>>>(pts, M, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
+        else
+            k_warp<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
         SGL_CUDA_CHECK(cudaGetLastError());
     }
     // Gather order: W x W pencils (cells on axes 1-2), nodes by lo0 inside a

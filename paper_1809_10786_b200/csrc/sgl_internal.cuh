@@ -71,6 +71,7 @@ struct Plan {
     bool compact = false;
     bool generic = false;
     bool exact = false;           // exact last stage: direct NDFT on I_n (no window, no FFT)
+    bool raw = false;             // plain 3-D NFFT plan (nfft.py): torus nodes, coefficients on I_n, no basal
     bool profile = false;
     int n_axis[3];
     int grid[3];
@@ -145,6 +146,9 @@ void set_error(const std::string &msg);
 // kernels / launchers (defined in the .cu files)
 int build_nodes(Plan &p, const double *points_dev, cudaStream_t st);
 int build_basal_tables(Plan &p);
+int build_deconv_tables(Plan &p);
+int launch_place_raw(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st);
+int launch_crop_raw(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
 int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
 int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
 int launch_basal_forward(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st,

@@ -346,6 +346,53 @@ def evaluate_direct_adjoint(values, B: int, points):
     return out
 
 
+def transform_points(points, rho: float) -> np.ndarray:
+    """Warp (r, theta, phi) to torus nodes (arccos((2r - rho)/rho), theta, phi)
+    (reference transform.py:46-55; host arithmetic, the device warps its own
+    copy in `plan`)."""
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    r = pts[:, 0]
+    if np.any(r > rho * (1 + 1e-12)):
+        raise ValueError("point radius exceeds the radial parameter rho")
+    out = pts.copy()
+    out[:, 0] = np.arccos(np.clip((2 * r - rho) / rho, -1.0, 1.0))
+    return out
+
+
+def sgl_basis_eval(idx, point):
+    """One basis function H_{n,l,m} at (r, theta, phi) points (reference
+    special.py:171-182), by the device direct sum with a unit coefficient."""
+    from .indexing import nlm_to_mu
+    n, l, m = (int(v) for v in idx)
+    mu = nlm_to_mu(n, l, m)
+    p = np.asarray(point, dtype=float)
+    shape = p.shape[:-1]
+    c = np.zeros(coeff_count(n), dtype=np.complex128)
+    c[mu] = 1.0
+    out = evaluate_direct(c, n, p.reshape(-1, 3)).reshape(shape)
+    return out if out.ndim else complex(out)
+
+
+def growth_threshold(rho: float) -> float:
+    """Bandwidth below which the small-radius branch of `error_bound` applies
+    (the reference's closed form, transform.py:436-443)."""
+    if not 0 < rho < 1:
+        raise ValueError("threshold is defined for 0 < rho < 1")
+    ie = 1.0 / np.e
+    return float((np.exp(2 * ie) * (rho ** (2 * ie) - 1) / (2 * np.log(rho))) ** (1 - ie) - 0.5)
+
+
+def error_bound(B: int, rho: float, q: int, l1_norm: float) -> float:
+    """Analytic envelope of the fast path's max-abs error with unit leading
+    constant (the reference's certificate, transform.py:446-462): a trend
+    check in q, rho and B, not an acceptance threshold.  Host arithmetic."""
+    ie = 1.0 / np.e
+    small = rho < 1 and B <= growth_threshold(rho)
+    a = 1.0 if small else 1.0 / rho
+    b = 0.5 * np.exp(2 * ie) * (1.0 if small else rho ** (2 * ie))
+    return float(B ** 3.5 * a * np.exp(b * (B + 0.5) ** (1 - ie) + 0.5 * rho ** 2 - 0.5 * np.pi * q) * l1_norm)
+
+
 def choose_rho(points) -> float:
     """Largest sample radius; 1.0 if all points sit at the origin (transform.py:39-43)."""
     pts = np.atleast_2d(np.asarray(points, dtype=float))

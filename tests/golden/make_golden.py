@@ -212,6 +212,34 @@ def direct_cases(ref):
     return out
 
 
+def nfft_cases(ref):
+    """The reference NFFT layer (nfft.py): nfft_plan / nfft_execute /
+    nfft_adjoint_execute and the exact ndft / ndft_adjoint, d = 3, nodes
+    outside [0, 2 pi) included (reduced by the plan)."""
+    out = {}
+    specs = [("nfft_a", (8, 10, 6), 2, 6, 300, 501), ("nfft_b", (16, 16, 16), 2, 16, 500, 502),
+             ("nfft_c", (12, 8, 20), 3, 10, 400, 503), ("nfft_d", (32, 32, 16), 2, 16, 2000, 504)]
+    for name, n, sigma, q, M, seed in specs:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        nodes = rng.uniform(-1.0, 2 * np.pi + 1.0, (M, 3))
+        nodes[:5] = [[0, 0, 0], [2 * np.pi, 0, -1e-17], [np.pi, np.pi / 2, 3.0], [-np.pi, 1e-3, 6.2], [1, 2, 3]]
+        f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        v = _vals(rng, M)
+        p = ref.nfft.nfft_plan(3, n, sigma, q, nodes)
+        d = dict(n=np.array(n), sigma=sigma, q=q, nodes=nodes, coeffs=f, values=v,
+                 fwd=ref.nfft.nfft_execute(p, f), adj=ref.nfft.nfft_adjoint_execute(p, v))
+        if M <= 400:
+            d["ndft"] = ref.nfft.ndft(3, n, f, nodes)
+            d["ndft_adj"] = ref.nfft.ndft_adjoint(3, n, v, nodes)
+        out[name] = d
+    rng = np.random.Generator(np.random.PCG64(505))
+    pts = ref.gen_points_ball(20, 3.0, rng)
+    idx = np.array([(1, 0, 0), (3, 2, -1), (5, 4, 3), (8, 3, 0), (6, 5, -5)])
+    basis = np.stack([ref.special.sgl_basis_eval(tuple(int(v) for v in t), pts) for t in idx])
+    out["nfft_index"] = dict(nlm=ref.indexing.mu_to_nlm_array(10), basis_idx=idx, basis_pts=pts, basis=basis)
+    return out
+
+
 def csv_cases(ref):
     """Files written by the reference CLI (cli.py) itself: generators and the
     three transform methods on a small problem (tests/golden/csv/)."""
@@ -269,6 +297,8 @@ def main():
         cases.update(direct_cases(ref))
     if args.only in ("", "csv"):
         csv_cases(ref)
+    if args.only in ("", "nfft"):
+        cases.update(nfft_cases(ref))
     for name, d in cases.items():
         path = os.path.join(HERE, f"ref_{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})
