@@ -262,6 +262,14 @@ def csv_cases(ref):
         ["adjoint", "--values", "f_naive.csv", "--points", "p_m40.csv", "-B", "5", "-q", "8", "--out", "a_fast.csv"],
         ["invert", "--values", "f_naive.csv", "--points", "p_m40.csv", "-B", "3", "--max-iter", "50",
          "--out", "inv_b3.csv"],
+        ["experiment", "error-vs-q", "-B", "5", "-M", "80", "--kappa", "3.0", "--q-list", "2,4,8,12,16",
+         "--repetitions", "3", "--seed", "11", "--out", "exp_q.csv"],
+        ["experiment", "error-vs-radius", "-B", "4", "-M", "60", "--kappa-list", "0.5,2,4", "-q", "10",
+         "--repetitions", "2", "--seed", "12", "--out", "exp_radius.csv"],
+        ["experiment", "error-vs-bandwidth", "--bandwidth-list", "3,6", "-M", "50", "--kappa", "2.5", "-q", "8",
+         "--repetitions", "2", "--seed", "13", "--exact-control", "--out", "exp_bw.csv"],
+        ["experiment", "inverse-convergence", "-B", "3", "-q", "8", "--grid-n-list", "6", "--kappa", "1.5",
+         "--max-iter", "12", "--seed", "14", "--out", "exp_inv.csv"],
     ]
     cwd = os.getcwd()
     os.chdir(tmp)

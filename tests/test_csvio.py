@@ -77,3 +77,25 @@ def test_coefficient_rows_follow_mu_order():
     np.testing.assert_array_equal(c, gen_coeffs(5, 7))
     t = nlm_table(3)
     assert t[0].tolist() == [1, 0, 0] and t[4].tolist() == [2, 1, 1] and t[5].tolist() == [3, 0, 0]
+
+
+def test_experiment_spec_validation_and_paper_scale():
+    from paper_1809_10786_b200.experiments import ExperimentSpec, paper_scale
+    for kind in ("error-vs-q", "error-vs-radius", "error-vs-bandwidth", "runtime", "inverse-convergence"):
+        with pytest.raises(ValueError):
+            ExperimentSpec(kind=kind).validate()   # empty sweep list
+    with pytest.raises(ValueError):
+        ExperimentSpec(kind="nope").validate()
+    with pytest.raises(ValueError):
+        ExperimentSpec(kind="error-vs-q", q_list=[4], repetitions=0).validate()
+    s = paper_scale(ExperimentSpec(kind="error-vs-bandwidth"))
+    assert s.B_list == [8, 16, 32, 64, 128] and s.M == 1000 and s.q == 12
+    s = paper_scale(ExperimentSpec(kind="inverse-convergence"))
+    assert s.grid_n_list == [25, 50, 100] and s.max_iter == 10_000 and s.q == 15
+
+
+def test_csv_table_render_matches_reference_layout():
+    t = csvio.CsvTable(["q", "err"], [[4, 0.5], [8, 1e-20]], {"kind": "x", "B": 3})
+    assert t.render() == "# sglnufft-csv v1 kind=x B=3\nq,err\n4,0.5\n8,9.9999999999999995e-21\n"
+    with pytest.raises(ValueError):
+        csvio.CsvTable(["a"], [[1, 2]]).render()
