@@ -60,7 +60,9 @@ enum {
     SGL_FLAG_COMPACT_K1 = 1u << 0,        /* compact_k1=True (transform.py:350)     */
     SGL_FLAG_EXACT_LAST_STAGE = 1u << 1,  /* exact_last_stage=True: direct NDFT      */
     SGL_FLAG_GENERIC_GRIDDING = 1u << 2,  /* force the per-node window kernels      */
-    SGL_FLAG_PROFILE = 1u << 3            /* record per-stage CUDA-event timings    */
+    SGL_FLAG_PROFILE = 1u << 3,           /* record per-stage CUDA-event timings    */
+    SGL_FLAG_PRECISE = 1u << 4            /* basal tables in 80-bit extended precision
+                                             (precise=True, recurrences.py:13)      */
 };
 
 typedef struct {

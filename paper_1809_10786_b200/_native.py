@@ -17,6 +17,7 @@ FLAG_COMPACT_K1 = 1 << 0
 FLAG_EXACT_LAST_STAGE = 1 << 1
 FLAG_GENERIC_GRIDDING = 1 << 2
 FLAG_PROFILE = 1 << 3
+FLAG_PRECISE = 1 << 4
 STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares

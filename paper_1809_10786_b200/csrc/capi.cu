@@ -257,6 +257,7 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->q = q;
     p->compact = flags & SGL_FLAG_COMPACT_K1;
     p->profile = flags & SGL_FLAG_PROFILE;
+    p->precise = flags & SGL_FLAG_PRECISE;
     p->exact = exact;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
     p->n_axis[0] = 4 * B;

@@ -71,7 +71,8 @@ struct Plan {
     bool compact = false;
     bool generic = false;
     bool exact = false;           // exact last stage: direct NDFT on I_n (no window, no FFT)
-    bool raw = false;             // plain 3-D NFFT plan (nfft.py): torus nodes, coefficients on I_n, no basal
+    bool raw = false;
+    bool precise = false;         // basal tables built in x87 extended precision (precise=True)             // plain 3-D NFFT plan (nfft.py): torus nodes, coefficients on I_n, no basal
     bool profile = false;
     int n_axis[3];
     int grid[3];

@@ -67,6 +67,9 @@ class SglPlan:
     device: int
     _handle: int = field(repr=False)
     _info: _native.PlanInfo = field(repr=False)
+    backend: str = "auto"
+    precise_tables: bool = False
+    _twin: object = field(default=None, repr=False)   # extended-precision twin for precise=True calls
 
     @property
     def m_points(self) -> int:
@@ -101,6 +104,9 @@ class SglPlan:
         return dict(zip(_native.STAGES, (float(x) for x in buf)))
 
     def close(self) -> None:
+        if self._twin is not None:
+            self._twin.close()
+            self._twin = None
         if self._handle:
             _native.lib().sgl_plan_destroy(self._handle)
             self._handle = 0
@@ -120,7 +126,8 @@ def _stream_ptr(x) -> int | None:
 
 def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
          exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
-         precompute: bool = True, device: int | None = None, profile: bool = False) -> SglPlan:
+         precompute: bool = True, device: int | None = None, profile: bool = False,
+         precise_tables: bool = False) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
     ``backend``: "auto" (tiled DMMA kernels for q <= 16, per-node kernels
@@ -171,6 +178,8 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_GENERIC_GRIDDING
     if profile:
         flags |= _native.FLAG_PROFILE
+    if precise_tables:
+        flags |= _native.FLAG_PRECISE
     h = ctypes.c_void_p(0)
     stream = _stream_ptr(pts)
     _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q or 0),
@@ -183,12 +192,21 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     return SglPlan(B=int(B), rho=float(info.rho), sigma=int(sigma), q=None if exact_last_stage else int(q),
                    exact=bool(exact_last_stage),
                    compact_k1=bool(compact_k1), points=points, n_axis=tuple(info.n_axis), nfft=nf,
-                   device=int(dev) if dev is not None else 0, _handle=h.value, _info=info)
+                   device=int(dev) if dev is not None else 0, _handle=h.value, _info=info, backend=backend,
+                   precise_tables=bool(precise_tables))
 
 
-def _check_precise(precise):
-    if precise:
-        raise ValueError("precise=True (80-bit recurrences) has no B200 equivalent")
+def _for_call(p: SglPlan, precise: bool) -> SglPlan:
+    """precise=True (the reference's 80-bit recurrences, recurrences.py:13):
+    run on a twin plan whose basal tables were built in x87 extended
+    precision (built on first use, cached on the plan)."""
+    if not precise or p.precise_tables:
+        return p
+    if p._twin is None:
+        p._twin = plan(p.B, p.points, sigma=p.sigma, q=p.q if not p.exact else 16, rho=p.rho,
+                       exact_last_stage=p.exact, compact_k1=p.compact_k1, backend=p.backend, device=p.device,
+                       precise_tables=True)
+    return p._twin
 
 
 def forward(p: SglPlan, coeffs, precise: bool = False):
@@ -196,7 +214,7 @@ def forward(p: SglPlan, coeffs, precise: bool = False):
 
     ``coeffs``: (count,) complex128, or (K, count) for K vectors on one plan
     (the batched forward).  Returns (M,) or (K, M)."""
-    _check_precise(precise)
+    p = _for_call(p, precise)
     cnt = p.count
     if _is_torch(coeffs):
         torch = _torch()
@@ -221,7 +239,7 @@ def forward(p: SglPlan, coeffs, precise: bool = False):
 
 def adjoint(p: SglPlan, values, precise: bool = False):
     """Apply the conjugate transpose of `forward` (transform.py:398-429)."""
-    _check_precise(precise)
+    p = _for_call(p, precise)
     if _is_torch(values):
         torch = _torch()
         v = values.to(torch.complex128).contiguous()

@@ -29,7 +29,7 @@ def golden_names(pattern="*"):
     return out
 
 
-SMALL = [n for n in golden_names() if not n.startswith(("cfg", "inv_", "direct_", "nfft_"))]
+SMALL = [n for n in golden_names() if not n.startswith(("cfg", "inv_", "direct_", "nfft_", "precise_"))]
 NFFT = [n for n in golden_names() if n.startswith("nfft_") and n != "nfft_index"]
 DIRECT = [n for n in golden_names() if n.startswith("direct_")]
 

@@ -240,6 +240,21 @@ def nfft_cases(ref):
     return out
 
 
+def precise_cases(ref):
+    """forward / adjoint with precise=True (80-bit recurrences, recurrences.py:13)."""
+    out = {}
+    for name, B, M, q, rad, seed in [("precise_b8", 8, 200, 16, 3.0, 601), ("precise_b24", 24, 300, 12, 5.0, 602)]:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        c = ref.gen_coeffs(B, rng)
+        pts = ref.gen_points_ball(M, rad, rng)
+        v = _vals(rng, M)
+        p = ref.plan(B, pts, q=q)
+        out[name] = dict(B=B, q=q, compact=False, points=pts, coeffs=c, values=v, rho=p.rho,
+                         fwd=ref.forward(p, c, precise=True), adj=ref.adjoint(p, v, precise=True),
+                         fwd_double=ref.forward(p, c), adj_double=ref.adjoint(p, v))
+    return out
+
+
 def csv_cases(ref):
     """Files written by the reference CLI (cli.py) itself: generators and the
     three transform methods on a small problem (tests/golden/csv/)."""
@@ -307,6 +322,8 @@ def main():
         csv_cases(ref)
     if args.only in ("", "nfft"):
         cases.update(nfft_cases(ref))
+    if args.only in ("", "precise"):
+        cases.update(precise_cases(ref))
     for name, d in cases.items():
         path = os.path.join(HERE, f"ref_{name}.npz")
         np.savez_compressed(path, **{k: np.asarray(v) for k, v in d.items()})

@@ -126,9 +126,23 @@ def test_linearity_zero_and_errors(sgl):
     with pytest.raises(ValueError):
         sgl.adjoint(p, np.zeros(31))
     with pytest.raises(ValueError):
-        sgl.forward(p, x, precise=True)
-    with pytest.raises(ValueError):
         sgl.plan(2, np.array([[2.1, 0, 0]]), q=4, rho=1.0)
+
+
+@pytest.mark.parametrize("name", ["precise_b8", "precise_b24"])
+def test_precise_matches_reference_precise(sgl, name):
+    # precise=True: basal tables in x87 extended precision on a cached twin
+    # plan; against the reference's own precise=True outputs
+    g = load_golden(name)
+    p = _plan(sgl, g)
+    f = sgl.forward(p, g["coeffs"], precise=True)
+    a = sgl.adjoint(p, g["values"], precise=True)
+    assert rel(f, g["fwd"]) <= TOL and rel(a, g["adj"]) <= TOL
+    assert p._twin is not None and p._twin.precise_tables
+    assert sgl.forward(p, g["coeffs"], precise=True).shape == f.shape   # the twin is reused
+    assert rel(sgl.forward(p, g["coeffs"]), g["fwd_double"]) <= TOL
+    p.close()
+    assert p._twin is None
 
 
 def test_compact_grid_agrees(sgl):
