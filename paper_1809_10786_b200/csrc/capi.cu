@@ -399,11 +399,11 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
 
 extern "C" {
 
-int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, int32_t sigma, int32_t q,
+int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, const int32_t *sigma, int32_t q,
                          uint32_t flags, void *stream, sgl_plan **out) {
     g_err.clear();
-    if (!out || !n_axis) {
-        set_error("NULL n_axis or output plan pointer");
+    if (!out || !n_axis || !sigma) {
+        set_error("NULL n_axis, sigma or output plan pointer");
         return SGL_EINVAL;
     }
     *out = nullptr;
@@ -427,24 +427,26 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
         while (g < v) g <<= 1;
         return g;
     };
+    int32_t sig[3] = {sigma[0], sigma[1], sigma[2]};
     if (!exact) {
-        if (sigma < 2) {
-            set_error("oversampling factor must be an integer >= 2");
-            return SGL_EINVAL;
-        }
+        for (int ax = 0; ax < 3; ++ax)
+            if (sig[ax] < 2) {
+                set_error("oversampling factor must be an integer >= 2");
+                return SGL_EINVAL;
+            }
         if (q < 1) {
             set_error("cutoff parameter must be >= 1");
             return SGL_EINVAL;
         }
         int64_t gmin = INT64_MAX;
-        for (int ax = 0; ax < 3; ++ax) gmin = std::min<int64_t>(gmin, pow2((int64_t)sigma * n_axis[ax]));
+        for (int ax = 0; ax < 3; ++ax) gmin = std::min<int64_t>(gmin, pow2((int64_t)sig[ax] * n_axis[ax]));
         if (q >= gmin) {
             set_error("cutoff q = " + std::to_string(q) + " must be below sigma*n = " + std::to_string(gmin));
             return SGL_EINVAL;
         }
     } else {
         q = 0;
-        sigma = 1;
+        sig[0] = sig[1] = sig[2] = 1;
     }
     auto t0 = std::chrono::steady_clock::now();
     Plan *p = new Plan();
@@ -453,7 +455,7 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
     p->B = 0;
     p->M = M;
     p->rho = 1.0;
-    p->sigma = sigma;
+    p->sigma = sig[0];
     p->q = q;
     p->profile = flags & SGL_FLAG_PROFILE;
     p->exact = exact;
@@ -461,8 +463,8 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
     p->count = (int64_t)n_axis[0] * n_axis[1] * n_axis[2];
     for (int ax = 0; ax < 3; ++ax) {   // nfft.py:174, 181-182 (no sigma escalation in the NFFT layer)
         p->n_axis[ax] = n_axis[ax];
-        p->sig_axes[ax] = sigma;
-        p->grid[ax] = exact ? n_axis[ax] : (int)pow2((int64_t)sigma * n_axis[ax]);
+        p->sig_axes[ax] = sig[ax];
+        p->grid[ax] = exact ? n_axis[ax] : (int)pow2((int64_t)sig[ax] * n_axis[ax]);
         p->s_eff[ax] = (double)p->grid[ax] / n_axis[ax];
         p->lam[ax] = exact ? 0.0 : p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
     }

@@ -13,7 +13,8 @@ stage): `sgl_nfft_plan_create` + `sgl_forward` / `sgl_adjoint`.
 
 `ndft` / `ndft_adjoint` are the exact sums on the device (an exact plan).
 `nfft_error_bound` is the reference's closed-form bound (host arithmetic).
-Deviation: only d = 3 (the dimension of the SGL transform); d = 1, 2 raise.
+Deviation: only d = 3 (the dimension of the SGL transform); d = 1, 2 raise
+(embedding them in 3-D would add window error on the dummy axes).
 """
 from __future__ import annotations
 
@@ -85,8 +86,8 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
               exact: bool = False) -> NfftPlan:
     """Plan the fast transform pair for one node set (nfft.py:147-207).
 
-    ``nodes`` (m, 3), reduced into [0, 2 pi).  ``sigma``: one integer >= 2
-    for all axes (the device plan has one oversampling factor).  ``backend``:
+    ``nodes`` (m, 3), reduced into [0, 2 pi).  ``sigma``: integer >= 2, or
+    one per axis.  ``backend``:
     "auto" / "tiled" / "generic" (the reference names "numba" / "numpy" are
     accepted as "auto").  ``precompute`` is accepted; windows are evaluated
     on the fly on the device.  ``exact=True`` plans the direct NDFT."""
@@ -97,13 +98,11 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
         raise ValueError("per-axis degree must be even and >= 2")
     if any(s < 2 for s in sig):
         raise ValueError("oversampling factor must be an integer >= 2")
-    if len(set(sig)) != 1:
-        raise ValueError("the device plan takes one oversampling factor for all axes")
     if q < 1:
         raise ValueError("cutoff parameter must be >= 1")
     if backend not in _BACKENDS:
         raise ValueError("backend must be 'auto', 'numba' or 'numpy'")
-    grid = tuple(1 << int(np.ceil(np.log2(sig[0] * n))) for n in n_axis)
+    grid = tuple(1 << int(np.ceil(np.log2(s * n))) for s, n in zip(sig, n_axis))
     if not exact and any(q >= g for g in grid):
         raise ValueError(f"cutoff q = {q} must be below sigma*n = {min(grid)}")
     torch_in = _is_torch(nodes)
@@ -124,8 +123,9 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
     if backend == "generic":
         flags |= _native.FLAG_GENERIC_GRIDDING
     n_arr = (ctypes.c_int32 * 3)(*n_axis)
+    s_arr = (ctypes.c_int32 * 3)(*sig)
     h = ctypes.c_void_p(0)
-    _native.check(_native.lib().sgl_nfft_plan_create(n_arr, M, ptr if M else None, int(sig[0]), int(q), flags,
+    _native.check(_native.lib().sgl_nfft_plan_create(n_arr, M, ptr if M else None, s_arr, int(q), flags,
                                                      _stream_ptr(pts), ctypes.byref(h)))
     info = _native.PlanInfo()
     _native.check(_native.lib().sgl_plan_get_info(h, ctypes.byref(info)))

@@ -218,7 +218,8 @@ def nfft_cases(ref):
     outside [0, 2 pi) included (reduced by the plan)."""
     out = {}
     specs = [("nfft_a", (8, 10, 6), 2, 6, 300, 501), ("nfft_b", (16, 16, 16), 2, 16, 500, 502),
-             ("nfft_c", (12, 8, 20), 3, 10, 400, 503), ("nfft_d", (32, 32, 16), 2, 16, 2000, 504)]
+             ("nfft_c", (12, 8, 20), 3, 10, 400, 503), ("nfft_d", (32, 32, 16), 2, 16, 2000, 504),
+             ("nfft_e", (10, 12, 8), (2, 4, 3), 8, 250, 506)]
     for name, n, sigma, q, M, seed in specs:
         rng = np.random.Generator(np.random.PCG64(seed))
         nodes = rng.uniform(-1.0, 2 * np.pi + 1.0, (M, 3))
@@ -226,7 +227,7 @@ def nfft_cases(ref):
         f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
         v = _vals(rng, M)
         p = ref.nfft.nfft_plan(3, n, sigma, q, nodes)
-        d = dict(n=np.array(n), sigma=sigma, q=q, nodes=nodes, coeffs=f, values=v,
+        d = dict(n=np.array(n), sigma=np.array(sigma), q=q, nodes=nodes, coeffs=f, values=v,
                  fwd=ref.nfft.nfft_execute(p, f), adj=ref.nfft.nfft_adjoint_execute(p, v))
         if M <= 400:
             d["ndft"] = ref.nfft.ndft(3, n, f, nodes)

@@ -49,7 +49,7 @@ def test_transform_points():
 
 @pytest.mark.parametrize("kw,msg", [
     (dict(d=2), "three-dimensional"), (dict(n_axis=(8, 9, 6)), "even"), (dict(sigma=1), "oversampling"),
-    (dict(q=0), "cutoff"), (dict(q=32, n_axis=(8, 8, 8)), "below sigma"), (dict(sigma=(2, 3, 2)), "one oversampling"),
+    (dict(q=0), "cutoff"), (dict(q=32, n_axis=(8, 8, 8)), "below sigma"), (dict(sigma=(2, 1, 2)), "oversampling"),
 ])
 def test_nfft_plan_argument_errors(kw, msg):
     args = dict(d=3, n_axis=(8, 10, 6), sigma=2, q=6, nodes=np.zeros((4, 3)))

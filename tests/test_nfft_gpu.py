@@ -24,8 +24,9 @@ def sgl():
 def test_nfft_matches_reference(sgl, name, backend):
     g = load_golden(name)
     n = tuple(int(v) for v in g["n"])
-    p = sgl.nfft_plan(3, n, int(g["sigma"]), int(g["q"]), g["nodes"], backend=backend)
-    assert p.grid_shape == tuple(1 << int(np.ceil(np.log2(int(g["sigma"]) * k))) for k in n)
+    sig = np.broadcast_to(g["sigma"], (3,))
+    p = sgl.nfft_plan(3, n, tuple(int(s) for s in sig), int(g["q"]), g["nodes"], backend=backend)
+    assert p.grid_shape == tuple(1 << int(np.ceil(np.log2(int(s) * k))) for s, k in zip(sig, n))
     assert rel(sgl.nfft_execute(p, g["coeffs"]), g["fwd"]) <= 1e-10
     assert rel(sgl.nfft_adjoint_execute(p, g["values"]), g["adj"]) <= 1e-10
 
