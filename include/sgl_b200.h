@@ -118,17 +118,18 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
 
 void sgl_plan_destroy(sgl_plan *plan);
 
-/* Plain 3-D NFFT on the torus (the reference's NFFT layer): trigonometric
- * polynomial coefficients on I_n = prod [-n_j/2, n_j/2) in the centred layout
- * (position p on axis j holds frequency p - n_j/2), nodes (M x 3) reduced
- * into [0, 2 pi).  n_axis[j] even >= 2; sigma[j] >= 2 per axis; oversampled
- * length pow2(sigma_j n_j);
- * q must be below every oversampled length (no escalation).  Use sgl_forward
- * (coefficients: n0*n1*n2, K vectors) and sgl_adjoint on the plan.
+/* Plain d-dimensional NFFT on the torus (the reference's NFFT layer, d <= 3):
+ * trigonometric polynomial coefficients on I_n = prod [-n_j/2, n_j/2) in the
+ * centred layout (position p on axis j holds frequency p - n_j/2), nodes
+ * (M x d) reduced into [0, 2 pi).  n_axis[j] even >= 2, sigma[j] >= 2
+ * (length-d arrays); oversampled length pow2(sigma_j n_j); q must be below
+ * every oversampled length (no escalation).  Use sgl_forward (coefficients:
+ * prod n_j per vector, K vectors) and sgl_adjoint on the plan.  d = 3 runs
+ * the tiled window kernels; d < 3 the per-node ones.
  * Flags: SGL_FLAG_EXACT_LAST_STAGE (direct NDFT), SGL_FLAG_GENERIC_GRIDDING,
  * SGL_FLAG_PROFILE. */
-int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, const int32_t *sigma, int32_t q,
-                         uint32_t flags, void *stream, sgl_plan **out);
+int sgl_nfft_plan_create(int32_t d, const int32_t *n_axis, int64_t M, const double *nodes, const int32_t *sigma,
+                         int32_t q, uint32_t flags, void *stream, sgl_plan **out);
 
 /* Direct summation of the expansion (no plan, O(M * count) FP64; the
  * reference's verification path and the CLI's --method naive).

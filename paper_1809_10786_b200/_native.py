@@ -74,7 +74,8 @@ def lib() -> ctypes.CDLL:
     L.sgl_forward.restype = ctypes.c_int
     L.sgl_adjoint.argtypes = [vp, vp, vp, vp]
     L.sgl_adjoint.restype = ctypes.c_int
-    L.sgl_nfft_plan_create.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_int32, ctypes.c_uint32, vp, vp]
+    L.sgl_nfft_plan_create.argtypes = [ctypes.c_int32, vp, ctypes.c_int64, vp, vp, ctypes.c_int32, ctypes.c_uint32,
+                                       vp, vp]
     L.sgl_nfft_plan_create.restype = ctypes.c_int
     L.sgl_forward_adjoint.argtypes = [vp, vp, vp, vp, vp, vp]
     L.sgl_forward_adjoint.restype = ctypes.c_int

@@ -320,6 +320,15 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         *cs[ax] = a / std::sqrt(kTwoPi * lam);                          // nfft.py:137
         *hs[ax] = ((kTwoPi / N) * (kTwoPi / N)) * (a * a) / (2.0 * lam);  // nfft.py:138
     }
+    int *qas[3] = {&wp.qa0, &wp.qa1, &wp.qa2};
+    for (int ax = 0; ax < 3; ++ax) {
+        *qas[ax] = q;
+        if (p->raw && ax < 3 - p->d) {   // dummy axis of a d < 3 NFFT: one tap of weight 1
+            *qas[ax] = 0;
+            *cs[ax] = 1.0;
+            *hs[ax] = 0.0;
+        }
+    }
     wp.r0_1 = std::exp(-2.0 * wp.h0);
     wp.r0_8 = std::exp(-2.0 * wp.h0 * 64.0);
     wp.r1_1 = std::exp(-2.0 * wp.h1);
@@ -330,8 +339,9 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     const double *dpts = points;
     double *owned = nullptr;
     if (M > 0 && !is_device_ptr(points)) {
-        if (cudaMalloc(&owned, sizeof(double) * 3 * M) != cudaSuccess ||
-            cudaMemcpyAsync(owned, points, sizeof(double) * 3 * M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        const int cols = p->raw ? p->d : 3;   // (M, d) torus nodes of an NFFT plan
+        if (cudaMalloc(&owned, sizeof(double) * cols * M) != cudaSuccess ||
+            cudaMemcpyAsync(owned, points, sizeof(double) * cols * M, cudaMemcpyHostToDevice, st) != cudaSuccess) {
             set_error("CUDA error while uploading points");
             rc = SGL_ECUDA;
         }
@@ -356,6 +366,8 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     if (rc == SGL_OK && !exact) {
         // transform the interior of the halo-padded grid in place
         // 64-bit plan: the padded grid exceeds 2^31 elements from B = 256 on
+        // rank d over the active (trailing) axes; the SGL transform is 3-D
+        const int rank = p->raw ? p->d : 3;
         long long n[3] = {p->grid[0], p->grid[1], p->grid[2]};
         long long emb[3] = {wp.N0, wp.N1p, wp.N2p};
         const long long dist = (long long)p->grid_elems;
@@ -363,7 +375,8 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         rc = fft_check(cufftCreate(&p->fft), "cufftCreate");
         if (rc == SGL_OK) {
             p->fft_ready = true;
-            rc = fft_check(cufftMakePlanMany64(p->fft, 3, n, emb, 1, dist, emb, 1, dist, CUFFT_Z2Z, 1, &work),
+            rc = fft_check(cufftMakePlanMany64(p->fft, rank, n + 3 - rank, emb + 3 - rank, 1, dist, emb + 3 - rank,
+                                               1, dist, CUFFT_Z2Z, 1, &work),
                            "cufftMakePlanMany64");
         }
     }
@@ -399,20 +412,28 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
 
 extern "C" {
 
-int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, const int32_t *sigma, int32_t q,
-                         uint32_t flags, void *stream, sgl_plan **out) {
+int sgl_nfft_plan_create(int32_t d, const int32_t *n_axis_d, int64_t M, const double *nodes,
+                         const int32_t *sigma_d, int32_t q, uint32_t flags, void *stream, sgl_plan **out) {
     g_err.clear();
-    if (!out || !n_axis || !sigma) {
+    if (!out || !n_axis_d || !sigma_d) {
         set_error("NULL n_axis, sigma or output plan pointer");
         return SGL_EINVAL;
     }
     *out = nullptr;
-    // nfft.py:164-176
-    for (int ax = 0; ax < 3; ++ax)
-        if (n_axis[ax] < 2 || n_axis[ax] % 2) {
+    if (d < 1 || d > 3) {
+        set_error("only d <= 3 supported");
+        return SGL_EINVAL;
+    }
+    // nfft.py:164-176; leading axes 0 .. 2-d are length-1 dummies
+    int32_t n_axis[3] = {1, 1, 1}, sigma[3] = {2, 2, 2};
+    for (int j = 0; j < d; ++j) {
+        n_axis[3 - d + j] = n_axis_d[j];
+        sigma[3 - d + j] = sigma_d[j];
+        if (n_axis_d[j] < 2 || n_axis_d[j] % 2) {
             set_error("per-axis degree must be even and >= 2");
             return SGL_EINVAL;
         }
+    }
     if (M < 0 || (M > 0 && !nodes)) {
         set_error("nodes must be (m, d)");
         return SGL_EINVAL;
@@ -439,7 +460,7 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
             return SGL_EINVAL;
         }
         int64_t gmin = INT64_MAX;
-        for (int ax = 0; ax < 3; ++ax) gmin = std::min<int64_t>(gmin, pow2((int64_t)sig[ax] * n_axis[ax]));
+        for (int ax = 3 - d; ax < 3; ++ax) gmin = std::min<int64_t>(gmin, pow2((int64_t)sig[ax] * n_axis[ax]));
         if (q >= gmin) {
             set_error("cutoff q = " + std::to_string(q) + " must be below sigma*n = " + std::to_string(gmin));
             return SGL_EINVAL;
@@ -452,6 +473,7 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
     Plan *p = new Plan();
     cudaGetDevice(&p->device);
     p->raw = true;
+    p->d = d;
     p->B = 0;
     p->M = M;
     p->rho = 1.0;
@@ -459,14 +481,15 @@ int sgl_nfft_plan_create(const int32_t *n_axis, int64_t M, const double *nodes, 
     p->q = q;
     p->profile = flags & SGL_FLAG_PROFILE;
     p->exact = exact;
-    p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
+    p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled || d < 3;
     p->count = (int64_t)n_axis[0] * n_axis[1] * n_axis[2];
     for (int ax = 0; ax < 3; ++ax) {   // nfft.py:174, 181-182 (no sigma escalation in the NFFT layer)
+        const bool dummy = ax < 3 - d;
         p->n_axis[ax] = n_axis[ax];
-        p->sig_axes[ax] = sig[ax];
-        p->grid[ax] = exact ? n_axis[ax] : (int)pow2((int64_t)sig[ax] * n_axis[ax]);
+        p->sig_axes[ax] = dummy ? 1 : sig[ax];
+        p->grid[ax] = (exact || dummy) ? n_axis[ax] : (int)pow2((int64_t)sig[ax] * n_axis[ax]);
         p->s_eff[ax] = (double)p->grid[ax] / n_axis[ax];
-        p->lam[ax] = exact ? 0.0 : p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
+        p->lam[ax] = (exact || dummy) ? 0.0 : p->s_eff[ax] * q / ((2 * p->s_eff[ax] - 1) * kPi);
     }
     return plan_finish(p, nodes, (cudaStream_t)stream, out, t0);
 }

@@ -504,30 +504,28 @@ __global__ void __launch_bounds__(NW_GEN * 32)
                      double2 *__restrict__ out) {
     extern __shared__ __align__(16) double gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P = 2 * wp.q + 1;
-    double *w0 = gsm + warp * 3 * P, *w1 = w0 + P, *w2 = w1 + P;
+    const int P0 = 2 * wp.qa0 + 1, P1 = 2 * wp.qa1 + 1, P2 = 2 * wp.qa2 + 1;
+    double *w0 = gsm + warp * (P0 + P1 + P2), *w1 = w0 + P0, *w2 = w1 + P1;
     const int64_t i = blockIdx.x * (int64_t)NW_GEN + warp;
     if (i >= M) return;
     const double u0 = nodes.u0[i], u1 = nodes.u1[i], u2 = nodes.u2[i];
     const int l0 = (int)floor(u0), l1 = (int)floor(u1), l2 = (int)floor(u2);
-    for (int o = lane; o < P; o += 32) {
-        w0[o] = wfun(u0, l0 - wp.q + o, wp.c0, wp.h0, wp.q);
-        w1[o] = wfun(u1, l1 - wp.q + o, wp.c1, wp.h1, wp.q);
-        w2[o] = wfun(u2, l2 - wp.q + o, wp.c2, wp.h2, wp.q);
-    }
+    for (int o = lane; o < P0; o += 32) w0[o] = wfun(u0, l0 - wp.qa0 + o, wp.c0, wp.h0, wp.qa0);
+    for (int o = lane; o < P1; o += 32) w1[o] = wfun(u1, l1 - wp.qa1 + o, wp.c1, wp.h1, wp.qa1);
+    for (int o = lane; o < P2; o += 32) w2[o] = wfun(u2, l2 - wp.qa2 + o, wp.c2, wp.h2, wp.qa2);
     __syncwarp();
     double ar = 0.0, ai = 0.0;
-    for (int a = 0; a < P; ++a) {
+    for (int a = 0; a < P0; ++a) {
         const double wa = w0[a];
         if (wa == 0.0) continue;
-        const int g0 = wrapi(l0 - wp.q + a, wp.N0);
-        for (int b = 0; b < P; ++b) {
+        const int g0 = wrapi(l0 - wp.qa0 + a, wp.N0);
+        for (int b = 0; b < P1; ++b) {
             const double wab = wa * w1[b];
-            const int g1 = wrapi(l1 - wp.q + b, wp.N1);
+            const int g1 = wrapi(l1 - wp.qa1 + b, wp.N1);
             const double2 *row = grid + ((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q;
             double sr = 0.0, si = 0.0;
-            for (int c = lane; c < P; c += 32) {
-                const double2 g = row[wrapi(l2 - wp.q + c, wp.N2)];
+            for (int c = lane; c < P2; c += 32) {
+                const double2 g = row[wrapi(l2 - wp.qa2 + c, wp.N2)];
                 sr = fma(w2[c], g.x, sr);
                 si = fma(w2[c], g.y, si);
             }
@@ -548,30 +546,28 @@ __global__ void __launch_bounds__(NW_GEN * 32)
                       double *__restrict__ grid) {
     extern __shared__ __align__(16) double gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P = 2 * wp.q + 1;
-    double *w0 = gsm + warp * 3 * P, *w1 = w0 + P, *w2 = w1 + P;
+    const int P0 = 2 * wp.qa0 + 1, P1 = 2 * wp.qa1 + 1, P2 = 2 * wp.qa2 + 1;
+    double *w0 = gsm + warp * (P0 + P1 + P2), *w1 = w0 + P0, *w2 = w1 + P1;
     const int64_t i = blockIdx.x * (int64_t)NW_GEN + warp;
     if (i >= M) return;
     const double u0 = nodes.u0[i], u1 = nodes.u1[i], u2 = nodes.u2[i];
     const int l0 = (int)floor(u0), l1 = (int)floor(u1), l2 = (int)floor(u2);
-    for (int o = lane; o < P; o += 32) {
-        w0[o] = wfun(u0, l0 - wp.q + o, wp.c0, wp.h0, wp.q);
-        w1[o] = wfun(u1, l1 - wp.q + o, wp.c1, wp.h1, wp.q);
-        w2[o] = wfun(u2, l2 - wp.q + o, wp.c2, wp.h2, wp.q);
-    }
+    for (int o = lane; o < P0; o += 32) w0[o] = wfun(u0, l0 - wp.qa0 + o, wp.c0, wp.h0, wp.qa0);
+    for (int o = lane; o < P1; o += 32) w1[o] = wfun(u1, l1 - wp.qa1 + o, wp.c1, wp.h1, wp.qa1);
+    for (int o = lane; o < P2; o += 32) w2[o] = wfun(u2, l2 - wp.qa2 + o, wp.c2, wp.h2, wp.qa2);
     __syncwarp();
     const double2 v = values[nodes.perm[i]];
-    for (int a = 0; a < P; ++a) {
+    for (int a = 0; a < P0; ++a) {
         const double wa = w0[a];
         if (wa == 0.0) continue;
-        const int g0 = wrapi(l0 - wp.q + a, wp.N0);
-        for (int b = 0; b < P; ++b) {
+        const int g0 = wrapi(l0 - wp.qa0 + a, wp.N0);
+        for (int b = 0; b < P1; ++b) {
             const double wab = wa * w1[b];
             const double tr = wab * v.x, tim = wab * v.y;
-            const int g1 = wrapi(l1 - wp.q + b, wp.N1);
+            const int g1 = wrapi(l1 - wp.qa1 + b, wp.N1);
             double *row = grid + 2 * (((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q);
-            for (int c = lane; c < P; c += 32) {
-                const int g2 = wrapi(l2 - wp.q + c, wp.N2);
+            for (int c = lane; c < P2; c += 32) {
+                const int g2 = wrapi(l2 - wp.qa2 + c, wp.N2);
                 red_add(row + 2 * g2, w2[c] * tr);
                 red_add(row + 2 * g2 + 1, w2[c] * tim);
             }
@@ -676,7 +672,7 @@ int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStrea
         if (blocks < 1) blocks = 1;
         k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
     } else {
-        const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);
+        const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_gather_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(p.M, p.nodes, p.wp,
                                                                                            grid, values);
@@ -742,7 +738,7 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
         k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.snodes, p.wp, values,
                                                           reinterpret_cast<double *>(grid));
     } else {
-        const size_t sm = (size_t)NW_GEN * 3 * (2 * p.q + 1) * sizeof(double);
+        const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_scatter_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(
             p.M, p.nodes, p.wp, values, reinterpret_cast<double *>(grid));

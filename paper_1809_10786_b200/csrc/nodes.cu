@@ -50,13 +50,20 @@ __device__ __forceinline__ void to_u(double tau, int N, double &u, int &lo) {
 }
 
 // plain NFFT nodes: already on the torus (nfft.py:177-178, 131-133)
-__global__ void k_torus(const double *pts, int64_t M, int N0, int N1, int N2, double *u0, double *u1, double *u2) {
+// (m, d) rows; the leading 3 - d axes are length-1 dummies at 0
+__global__ void k_torus(const double *pts, int64_t M, int d, int N0, int N1, int N2, double *u0, double *u1,
+                        double *u2) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= M) return;
-    int l;
-    to_u(reduce_2pi(pts[3 * i]), N0, u0[i], l);
-    to_u(reduce_2pi(pts[3 * i + 1]), N1, u1[i], l);
-    to_u(reduce_2pi(pts[3 * i + 2]), N2, u2[i], l);
+    double *us[3] = {u0, u1, u2};
+    const int Ns[3] = {N0, N1, N2};
+    for (int ax = 0; ax < 3; ++ax) {
+        int l;
+        if (ax < 3 - d)
+            us[ax][i] = 0.0;
+        else
+            to_u(reduce_2pi(pts[d * i + ax - (3 - d)]), Ns[ax], us[ax][i], l);
+    }
 }
 
 struct KeyGeom {
@@ -350,7 +357,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     SGL_CUDA_CHECK(a2.alloc(M));
     if (M > 0) {
         if (p.raw)
-            k_torus<<<grid_for(M, T), T, 0, st>>>(pts, M, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
+            k_torus<<<grid_for(M, T), T, 0, st>>>(pts, M, p.d, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
         else
             k_warp<<<grid_for(M, T), T, 0, st>>>(pts, M, p.rho, p.grid[0], p.grid[1], p.grid[2], a0.p, a1.p, a2.p);
         SGL_CUDA_CHECK(cudaGetLastError());

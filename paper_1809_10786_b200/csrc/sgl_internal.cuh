@@ -50,6 +50,8 @@ struct WindowParams {
     int32_t N0, N1, N2;
     int32_t N1p, N2p;
     int32_t q;
+    int32_t qa0, qa1, qa2;      // per-axis tap half-width of the generic kernels (0 on the
+                                // dummy axes of a d < 3 NFFT plan: one tap of weight 1)
     double c0, c1, c2;          // (N/2pi)/sqrt(2 pi lam)
     double h0, h1, h2;          // 1/(2 lam)
     // recurrence ratios e^{-2 h s^2} of the Gaussian walks (stride s in cells)
@@ -72,6 +74,7 @@ struct Plan {
     bool generic = false;
     bool exact = false;           // exact last stage: direct NDFT on I_n (no window, no FFT)
     bool raw = false;
+    int d = 3;                    // NFFT dimension (raw plans); axes 0 .. 2-d are length-1 dummies
     bool precise = false;         // basal tables built in x87 extended precision (precise=True)             // plain 3-D NFFT plan (nfft.py): torus nodes, coefficients on I_n, no basal
     bool profile = false;
     int n_axis[3];

@@ -1,6 +1,6 @@
 """The reference's NFFT layer (`sglnufft.nfft`, nfft.py:1-273) on the device.
 
-Three-dimensional non-equispaced FFTs on the torus,
+Non-equispaced FFTs on the torus in d <= 3 dimensions,
 
     p(t) = sum_{k in I_n} w_k e^{+i <k, t>},   c_k = sum_i v_i e^{-i <k, t_i>},
 
@@ -13,8 +13,9 @@ stage): `sgl_nfft_plan_create` + `sgl_forward` / `sgl_adjoint`.
 
 `ndft` / `ndft_adjoint` are the exact sums on the device (an exact plan).
 `nfft_error_bound` is the reference's closed-form bound (host arithmetic).
-Deviation: only d = 3 (the dimension of the SGL transform); d = 1, 2 raise
-(embedding them in 3-D would add window error on the dummy axes).
+d = 3 runs the tiled DMMA window kernels; d = 1, 2 are embedded as length-1
+leading axes with a single unit-weight tap (exact, no window on them) and run
+the per-node kernels.
 """
 from __future__ import annotations
 
@@ -41,8 +42,6 @@ def _as_axes(value, d: int, name: str) -> tuple:
 def _check_d(d: int) -> None:
     if d < 1 or d > 3:
         raise ValueError("only d <= 3 supported")
-    if d != 3:
-        raise ValueError("the B200 NFFT is three-dimensional (d = 3)")
 
 
 @dataclass
@@ -86,7 +85,7 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
               exact: bool = False) -> NfftPlan:
     """Plan the fast transform pair for one node set (nfft.py:147-207).
 
-    ``nodes`` (m, 3), reduced into [0, 2 pi).  ``sigma``: integer >= 2, or
+    ``nodes`` (m, d), reduced into [0, 2 pi).  ``sigma``: integer >= 2, or
     one per axis.  ``backend``:
     "auto" / "tiled" / "generic" (the reference names "numba" / "numpy" are
     accepted as "auto").  ``precompute`` is accepted; windows are evaluated
@@ -122,15 +121,15 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
         flags |= _native.FLAG_EXACT_LAST_STAGE
     if backend == "generic":
         flags |= _native.FLAG_GENERIC_GRIDDING
-    n_arr = (ctypes.c_int32 * 3)(*n_axis)
-    s_arr = (ctypes.c_int32 * 3)(*sig)
+    n_arr = (ctypes.c_int32 * d)(*n_axis)
+    s_arr = (ctypes.c_int32 * d)(*sig)
     h = ctypes.c_void_p(0)
-    _native.check(_native.lib().sgl_nfft_plan_create(n_arr, M, ptr if M else None, s_arr, int(q), flags,
+    _native.check(_native.lib().sgl_nfft_plan_create(int(d), n_arr, M, ptr if M else None, s_arr, int(q), flags,
                                                      _stream_ptr(pts), ctypes.byref(h)))
     info = _native.PlanInfo()
     _native.check(_native.lib().sgl_plan_get_info(h, ctypes.byref(info)))
-    return NfftPlan(d=d, n_axis=n_axis, sigma=sig, q=int(q), grid_shape=tuple(info.grid),
-                    sigma_eff=tuple(info.sigma_eff), lam=tuple(info.lam), nodes=pts,
+    return NfftPlan(d=d, n_axis=n_axis, sigma=sig, q=int(q), grid_shape=tuple(info.grid)[3 - d:],
+                    sigma_eff=tuple(info.sigma_eff)[3 - d:], lam=tuple(info.lam)[3 - d:], nodes=pts,
                     backend="generic" if info.generic else "tiled", exact=bool(exact), _handle=h.value)
 
 

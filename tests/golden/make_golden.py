@@ -233,6 +233,17 @@ def nfft_cases(ref):
             d["ndft"] = ref.nfft.ndft(3, n, f, nodes)
             d["ndft_adj"] = ref.nfft.ndft_adjoint(3, n, v, nodes)
         out[name] = d
+    for name, d, n, sigma, q, M, seed in [("nfft_d1", 1, (16,), 2, 8, 120, 507),
+                                          ("nfft_d2", 2, (12, 10), (2, 3), 6, 200, 508),
+                                          ("nfft_d2b", 2, (32, 16), 2, 16, 300, 509)]:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        nodes = rng.uniform(-1.0, 2 * np.pi + 1.0, (M, d))
+        f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        v = _vals(rng, M)
+        p = ref.nfft.nfft_plan(d, n, sigma, q, nodes)
+        out[name] = dict(d=d, n=np.array(n), sigma=np.array(sigma), q=q, nodes=nodes, coeffs=f, values=v,
+                         fwd=ref.nfft.nfft_execute(p, f), adj=ref.nfft.nfft_adjoint_execute(p, v),
+                         ndft=ref.nfft.ndft(d, n, f, nodes), ndft_adj=ref.nfft.ndft_adjoint(d, n, v, nodes))
     rng = np.random.Generator(np.random.PCG64(505))
     pts = ref.gen_points_ball(20, 3.0, rng)
     idx = np.array([(1, 0, 0), (3, 2, -1), (5, 4, 3), (8, 3, 0), (6, 5, -5)])

@@ -48,7 +48,7 @@ def test_transform_points():
 
 
 @pytest.mark.parametrize("kw,msg", [
-    (dict(d=2), "three-dimensional"), (dict(n_axis=(8, 9, 6)), "even"), (dict(sigma=1), "oversampling"),
+    (dict(d=4), "d <= 3"), (dict(n_axis=(8, 9, 6)), "even"), (dict(sigma=1), "oversampling"),
     (dict(q=0), "cutoff"), (dict(q=32, n_axis=(8, 8, 8)), "below sigma"), (dict(sigma=(2, 1, 2)), "oversampling"),
 ])
 def test_nfft_plan_argument_errors(kw, msg):

@@ -23,9 +23,10 @@ def sgl():
 @pytest.mark.parametrize("name", NFFT)
 def test_nfft_matches_reference(sgl, name, backend):
     g = load_golden(name)
+    d = int(g["d"]) if "d" in g else 3
     n = tuple(int(v) for v in g["n"])
-    sig = np.broadcast_to(g["sigma"], (3,))
-    p = sgl.nfft_plan(3, n, tuple(int(s) for s in sig), int(g["q"]), g["nodes"], backend=backend)
+    sig = np.broadcast_to(g["sigma"], (d,))
+    p = sgl.nfft_plan(d, n, tuple(int(s) for s in sig), int(g["q"]), g["nodes"], backend=backend)
     assert p.grid_shape == tuple(1 << int(np.ceil(np.log2(int(s) * k))) for s, k in zip(sig, n))
     assert rel(sgl.nfft_execute(p, g["coeffs"]), g["fwd"]) <= 1e-10
     assert rel(sgl.nfft_adjoint_execute(p, g["values"]), g["adj"]) <= 1e-10
@@ -34,9 +35,10 @@ def test_nfft_matches_reference(sgl, name, backend):
 @pytest.mark.parametrize("name", [n for n in NFFT if "ndft" in load_golden(n)])
 def test_ndft_matches_reference(sgl, name):
     g = load_golden(name)
+    d = int(g["d"]) if "d" in g else 3
     n = tuple(int(v) for v in g["n"])
-    assert rel(sgl.ndft(3, n, g["coeffs"], g["nodes"]), g["ndft"]) <= 1e-12
-    assert rel(sgl.ndft_adjoint(3, n, g["values"], g["nodes"]), g["ndft_adj"]) <= 1e-12
+    assert rel(sgl.ndft(d, n, g["coeffs"], g["nodes"]), g["ndft"]) <= 1e-12
+    assert rel(sgl.ndft_adjoint(d, n, g["values"], g["nodes"]), g["ndft_adj"]) <= 1e-12
 
 
 def test_nfft_pairing_torch_and_errors(sgl):
