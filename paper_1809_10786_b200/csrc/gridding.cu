@@ -166,27 +166,28 @@ __device__ __forceinline__ void consumers_sync() {
 // <= 32 columns (narrow pencils) and 9 otherwise.  W0[a, node] is folded
 // into the A fragments, so the NTMAX accumulators run over the whole tile
 // (K = slabs x columns) and W1 is applied once per tile.
-template <int NKS>
-__device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[KSMAX], double w0, int rb, int cc,
-                                            int part, double (&d)[NTMAX][2]) {
+template <int NKS, int NT>
+__device__ __forceinline__ void gather_slab(const double *sl, const double (&afr)[NT], double w0, int rb, int cc,
+                                            int part, double (&d)[NT][2]) {
     // B fragments double-buffered one k-step ahead, so no DMMA waits on the
     // shared-memory load feeding it
-    double bf[2][NTMAX];
+    double bf[2][NT];
 #pragma unroll
-    for (int nt = 0; nt < NTMAX; ++nt) bf[0][nt] = sl[((nt * 4 + rb) * SSTR + cc) * 2 + part];
+    for (int nt = 0; nt < NT; ++nt) bf[0][nt] = sl[((nt * 4 + rb) * SSTR + cc) * 2 + part];
 #pragma unroll
     for (int ks = 0; ks < NKS; ++ks) {
         if (ks + 1 < NKS) {
 #pragma unroll
-            for (int nt = 0; nt < NTMAX; ++nt)
+            for (int nt = 0; nt < NT; ++nt)
                 bf[(ks + 1) & 1][nt] = sl[((nt * 4 + rb) * SSTR + (ks + 1) * 4 + cc) * 2 + part];
         }
         const double a = w0 * afr[ks];
 #pragma unroll
-        for (int nt = 0; nt < NTMAX; ++nt) dmma(d[nt], a, bf[ks & 1][nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma(d[nt], a, bf[ks & 1][nt]);
     }
 }
 
+template <int NT>   // fragment tiles per slab axis: ceil(box / 4) of the plan's widest tile (9 at q = 16)
 __global__ void __launch_bounds__(GT, GCPS)
     k_gather_tiled(const __grid_constant__ CUtensorMap tmap, const Tile *__restrict__ tiles, int64_t ntiles,
                    NodeSet nodes, WindowParams wp, double2 *__restrict__ out) {
@@ -262,13 +263,13 @@ __global__ void __launch_bounds__(GT, GCPS)
         const double r0step = wp.r0_1;
         const int Mt = (t.e1 + 3) >> 2;
         const int KS = (t.e2 + 3) >> 2;
-        double afr[KSMAX];
-        wwalk<KSMAX, 4>(S.nu[2][node], t.o2 + cc, KS, wp.c2, wp.h2, wp.r2_4, wp.q, afr);
+        double afr[NT];
+        wwalk<NT, 4>(S.nu[2][node], t.o2 + cc, KS, wp.c2, wp.h2, wp.r2_4, wp.q, afr);
         consumers_sync();
         const bool col_live = warp * 8 < t.count;
-        double d[NTMAX][2];
+        double d[NT][2];
 #pragma unroll
-        for (int nt = 0; nt < NTMAX; ++nt) d[nt][0] = d[nt][1] = 0.0;
+        for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = 0.0;
         for (int a = 0; a < t.e0; ++a) {
             const uint32_t q = seq + a;
             const int buf = (int)(q % NST);
@@ -285,10 +286,10 @@ __global__ void __launch_bounds__(GT, GCPS)
             mbar_wait(&S.full[buf], (q / NST) & 1);
             if (col_live && __any_sync(0xffffffffu, w0 != 0.0)) {
                 const double *sl = reinterpret_cast<const double *>(S.slab[buf]);
-                if (KS <= KSMAX - 1)
-                    gather_slab<KSMAX - 1>(sl, afr, w0, rb, cc, part, d);
+                if (KS <= NT - 1)
+                    gather_slab<NT - 1, NT>(sl, afr, w0, rb, cc, part, d);
                 else
-                    gather_slab<KSMAX>(sl, afr, w0, rb, cc, part, d);
+                    gather_slab<NT, NT>(sl, afr, w0, rb, cc, part, d);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[buf]);
@@ -296,10 +297,10 @@ __global__ void __launch_bounds__(GT, GCPS)
         double acc_re = 0.0, acc_im = 0.0;
         {
             // W1 once per tile, evaluated here so it holds no registers in the slab loop
-            double w1[NTMAX];
-            wwalk<NTMAX, 4>(S.nu[1][node], t.o1 + cc, Mt, wp.c1, wp.h1, wp.r1_4, wp.q, w1);
+            double w1[NT];
+            wwalk<NT, 4>(S.nu[1][node], t.o1 + cc, Mt, wp.c1, wp.h1, wp.r1_4, wp.q, w1);
 #pragma unroll
-            for (int nt = 0; nt < NTMAX; ++nt) {
+            for (int nt = 0; nt < NT; ++nt) {
                 acc_re = fma(w1[nt], d[nt][0], acc_re);
                 acc_im = fma(w1[nt], d[nt][1], acc_im);
             }
@@ -354,32 +355,32 @@ struct ScatterSmem {
 // One group of SMT four-row M-tiles x NCT eight-column tiles of slab a,
 // accumulated over the active node k-steps, then reduced into the grid.
 // NCT is a template parameter so no runtime predicate sits around a DMMA.
-template <int NCT>
+template <int NCT, int G>
 __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double (*w0row)[WS], int mt0, int ks0, int ks1,
                                               int g0, const Tile &t, const WindowParams &wp, double *grid,
                                               int lane) {
     const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
-    double d[SMT][NCT][2];
+    double d[G][NCT][2];
 #pragma unroll
-    for (int i = 0; i < SMT; ++i)
+    for (int i = 0; i < G; ++i)
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) d[i][ct][0] = d[i][ct][1] = 0.0;
 #pragma unroll 2
     for (int ks = ks0; ks < ks1; ++ks) {
         const int n = ks * 4 + kk;
         const double wv = w0row[part][n];
-        double av[SMT];
+        double av[G];
 #pragma unroll
-        for (int i = 0; i < SMT; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
+        for (int i = 0; i < G; ++i) av[i] = wv * S.w1[(mt0 + i) * 4 + rb][n];
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) {
             const double bv = S.w2[ct * 8 + cr][n];
 #pragma unroll
-            for (int i = 0; i < SMT; ++i) dmma(d[i][ct], av[i], bv);
+            for (int i = 0; i < G; ++i) dmma(d[i][ct], av[i], bv);
         }
     }
 #pragma unroll
-    for (int i = 0; i < SMT; ++i) {
+    for (int i = 0; i < G; ++i) {
         const int b = (mt0 + i) * 4 + rb;
         if (b < t.e1) {
             // halo-padded grid: rows / columns of the box never wrap
@@ -394,6 +395,32 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
             }
         }
     }
+}
+
+// the group's column tiles (box width / 8) and M-tiles (<= SMT; fewer for the
+// last group of a short box) as template parameters: no DMMA on padding tiles
+__device__ __forceinline__ void scatter_group_any(int nct, int g, const ScatterSmem &S, const double (*w0row)[WS],
+                                                  int mt0, int ks0, int ks1, int g0, const Tile &t,
+                                                  const WindowParams &wp, double *grid, int lane) {
+#define SGL_SG(NC, GG) scatter_group<NC, GG>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane)
+    switch (nct * 4 + g) {
+    case 1 * 4 + 1: SGL_SG(1, 1); break;
+    case 1 * 4 + 2: SGL_SG(1, 2); break;
+    case 1 * 4 + 3: SGL_SG(1, 3); break;
+    case 2 * 4 + 1: SGL_SG(2, 1); break;
+    case 2 * 4 + 2: SGL_SG(2, 2); break;
+    case 2 * 4 + 3: SGL_SG(2, 3); break;
+    case 3 * 4 + 1: SGL_SG(3, 1); break;
+    case 3 * 4 + 2: SGL_SG(3, 2); break;
+    case 3 * 4 + 3: SGL_SG(3, 3); break;
+    case 4 * 4 + 1: SGL_SG(4, 1); break;
+    case 4 * 4 + 2: SGL_SG(4, 2); break;
+    case 4 * 4 + 3: SGL_SG(4, 3); break;
+    case 5 * 4 + 1: SGL_SG(5, 1); break;
+    case 5 * 4 + 2: SGL_SG(5, 2); break;
+    default: SGL_SG(5, 3); break;
+    }
+#undef SGL_SG
 }
 
 __global__ void __launch_bounds__(STH, 2)
@@ -483,12 +510,8 @@ __global__ void __launch_bounds__(STH, 2)
             if (klast < 0) continue;
             const int ks0 = kfirst, ks1 = min(nks, klast + 1);
             const int g0 = wrapi(t.o0 + a, wp.N0);
-            for (int mt0 = 0; mt0 < Mt; mt0 += SMT) {
-                if (CT == CTMAX)
-                    scatter_group<CTMAX>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
-                else
-                    scatter_group<CTMAX - 1>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
-            }
+            for (int mt0 = 0; mt0 < Mt; mt0 += SMT)
+                scatter_group_any(CT, min(SMT, Mt - mt0), S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
             __syncwarp();   // w0row is rewritten for the warp's next slab
         }
     }
@@ -663,14 +686,31 @@ int num_sms() {
 
 }  // namespace
 
+namespace {
+template <int NT>
+cudaError_t launch_gather_nt(const Plan &p, double2 *values, unsigned blocks, cudaStream_t st) {
+    const size_t sm = sizeof(GatherSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_gather_tiled<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_gather_tiled<NT><<<blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
+    return cudaGetLastError();
+}
+}  // namespace
+
 int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st) {
     if (p.M == 0) return SGL_OK;
     if (!p.generic) {
-        const size_t sm = sizeof(GatherSmem);
-        SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * GCPS);
         if (blocks < 1) blocks = 1;
-        k_gather_tiled<<<(unsigned)blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
+        switch (std::max(3, std::min(NTMAX, (p.tile_box + 3) / 4))) {
+        case 3: SGL_CUDA_CHECK(launch_gather_nt<3>(p, values, (unsigned)blocks, st)); break;
+        case 4: SGL_CUDA_CHECK(launch_gather_nt<4>(p, values, (unsigned)blocks, st)); break;
+        case 5: SGL_CUDA_CHECK(launch_gather_nt<5>(p, values, (unsigned)blocks, st)); break;
+        case 6: SGL_CUDA_CHECK(launch_gather_nt<6>(p, values, (unsigned)blocks, st)); break;
+        case 7: SGL_CUDA_CHECK(launch_gather_nt<7>(p, values, (unsigned)blocks, st)); break;
+        case 8: SGL_CUDA_CHECK(launch_gather_nt<8>(p, values, (unsigned)blocks, st)); break;
+        default: SGL_CUDA_CHECK(launch_gather_nt<NTMAX>(p, values, (unsigned)blocks, st)); break;
+        }
     } else {
         const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

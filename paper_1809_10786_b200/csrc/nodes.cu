@@ -407,8 +407,10 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     SGL_CUDA_CHECK(cudaMemcpyAsync(ht.data(), p.tiles, sizeof(Tile) * p.n_tiles, cudaMemcpyDeviceToHost, st));
     SGL_CUDA_CHECK(cudaStreamSynchronize(st));
     int64_t nodes = 0, dmma = 0;
+    int box = 1;
     for (const Tile &t : ht) {
         nodes += t.count;
+        box = std::max(box, std::max(t.e1, t.e2));
         int64_t mt = (t.e1 + 3) / 4, ks = (t.e2 + 3) / 4, nt = (t.count + 7) / 8;
         dmma += (int64_t)t.e0 * mt * ks * nt;
         if (t.e1 > kBoxMax || t.e2 > kBoxMax || t.e0 > kBox0Max) {
@@ -418,6 +420,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     }
     p.tile_nodes = nodes;
     p.tile_dmma = dmma;
+    p.tile_box = box;
     return SGL_OK;
 }
 

@@ -95,6 +95,7 @@ struct Plan {
     int64_t n_stiles = 0;
     int64_t tile_nodes = 0;
     int64_t tile_dmma = 0;
+    int tile_box = kBoxMax;       // widest gather-tile box on axes 1-2 (cells): fragment loop extent
     double plan_ms = 0;
     // per-node u (caller order) for the generic kernels
     double *gu0 = nullptr, *gu1 = nullptr, *gu2 = nullptr;
