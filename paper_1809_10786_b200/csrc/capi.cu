@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -52,6 +53,10 @@ void free_plan(Plan *p) {
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
+    if (p->pruned) {
+        cufftDestroy(p->fft2);
+        cufftDestroy(p->fft1);
+    }
     if (p->done) cudaEventDestroy(p->done);
     if (p->ev_a) cudaEventDestroy(p->ev_a);
     if (p->ev_b) cudaEventDestroy(p->ev_b);
@@ -125,6 +130,41 @@ cudaError_t ensure_side(Plan &p) {
     return e;
 }
 
+// The oversampled 3-D FFT of the padded interior (in place).  Pruned plans
+// skip the 2-D transforms of the axis-0 planes outside the n0 spectral
+// planes [0, n0/2) U [N0 - n0/2, N0): zero on input of the inverse
+// transform, not read after the forward one.
+int grid_fft(Plan &p, cudaStream_t st, int dir) {
+    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+    if (!p.pruned) {
+        int rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
+        if (rc) return rc;
+        return fft_check(cufftExecZ2Z(p.fft, interior, interior, dir), "cufftExecZ2Z");
+    }
+    const size_t plane = (size_t)p.wp.N1p * p.wp.N2p;
+    const int h = p.n_axis[0] / 2;
+    cufftDoubleComplex *all = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf);
+    int rc = fft_check(cufftSetStream(p.fft2, st), "cufftSetStream");
+    if (!rc) rc = fft_check(cufftSetStream(p.fft1, st), "cufftSetStream");
+    if (rc) return rc;
+    auto planes = [&]() {
+        int r = fft_check(cufftExecZ2Z(p.fft2, interior, interior, dir), "cufftExecZ2Z(2d)");
+        if (!r) {
+            cufftDoubleComplex *hi = interior + (size_t)(p.wp.N0 - h) * plane;
+            r = fft_check(cufftExecZ2Z(p.fft2, hi, hi, dir), "cufftExecZ2Z(2d)");
+        }
+        return r;
+    };
+    if (dir == CUFFT_INVERSE) {
+        rc = planes();
+        if (!rc) rc = fft_check(cufftExecZ2Z(p.fft1, all, all, dir), "cufftExecZ2Z(1d)");
+    } else {
+        rc = fft_check(cufftExecZ2Z(p.fft1, all, all, dir), "cufftExecZ2Z(1d)");
+        if (!rc) rc = planes();
+    }
+    return rc;
+}
+
 int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRec *rec) {
     auto mark = [&](int s) {
         if (rec) rec->mark(s);
@@ -137,10 +177,7 @@ int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRe
         return launch_exact_forward(p, p.grid_buf, v, st);
     }
     mark(SGL_STAGE_FFT);
-    rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-    if (rc) return rc;
-    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-    rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_INVERSE), "cufftExecZ2Z(inverse)");
+    rc = grid_fft(p, st, CUFFT_INVERSE);
     if (rc) return rc;
     rc = launch_halo_fill(p, p.grid_buf, st);
     if (rc) return rc;
@@ -162,13 +199,9 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
         rc = launch_scatter(p, v, p.grid_buf, st);
         if (rc) return rc;
         mark(SGL_STAGE_FFT);
-        rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
-        if (rc) return rc;
         rc = launch_halo_fold(p, p.grid_buf, st);
         if (rc) return rc;
-        cufftDoubleComplex *interior =
-            reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
-        rc = fft_check(cufftExecZ2Z(p.fft, interior, interior, CUFFT_FORWARD), "cufftExecZ2Z(forward)");
+        rc = grid_fft(p, st, CUFFT_FORWARD);
         if (rc) return rc;
     }
     mark(SGL_STAGE_BASAL);
@@ -378,6 +411,25 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
             rc = fft_check(cufftMakePlanMany64(p->fft, rank, n + 3 - rank, emb + 3 - rank, 1, dist, emb + 3 - rank,
                                                1, dist, CUFFT_Z2Z, 1, &work),
                            "cufftMakePlanMany64");
+        }
+        // pruned variant when at most half the axis-0 planes carry the spectrum
+        const char *fe = getenv("SGL_FFT");
+        const bool want = rank == 3 && 2 * p->n_axis[0] <= p->grid[0] && !(fe && !strcmp(fe, "full"));
+        if (rc == SGL_OK && want) {
+            long long n2[2] = {p->grid[1], p->grid[2]}, e2[2] = {wp.N1p, wp.N2p};
+            const long long pl = (long long)wp.N1p * wp.N2p;
+            long long n1[1] = {p->grid[0]}, e1[1] = {p->grid[0]};
+            size_t w2 = 0, w1 = 0;
+            bool ok = cufftCreate(&p->fft2) == CUFFT_SUCCESS;
+            ok = ok && cufftCreate(&p->fft1) == CUFFT_SUCCESS;
+            ok = ok && cufftMakePlanMany64(p->fft2, 2, n2, e2, 1, pl, e2, 1, pl, CUFFT_Z2Z, p->n_axis[0] / 2, &w2) ==
+                           CUFFT_SUCCESS;
+            ok = ok && cufftMakePlanMany64(p->fft1, 1, n1, e1, pl, 1, e1, pl, 1, CUFFT_Z2Z, pl, &w1) == CUFFT_SUCCESS;
+            p->pruned = ok;
+            if (!ok) {
+                cufftDestroy(p->fft2);
+                cufftDestroy(p->fft1);
+            }
         }
     }
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);

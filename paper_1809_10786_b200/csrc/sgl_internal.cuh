@@ -118,6 +118,10 @@ struct Plan {
     size_t grid_elems = 0;
     cufftHandle fft = 0;
     bool fft_ready = false;
+    // pruned 3-D FFT: 2-D transforms over the planes that hold (forward) or
+    // receive (adjoint) the n0 spectral planes, 1-D transforms along axis 0
+    cufftHandle fft2 = 0, fft1 = 0;
+    bool pruned = false;
 
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
