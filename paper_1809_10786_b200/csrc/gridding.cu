@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+
 #include "sgl_internal.cuh"
 
 namespace sgl {
@@ -672,16 +674,19 @@ __global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
     fold_cell(wp, grid, blockIdx.y, i1, i2);
 }
 
-int g_num_sms = 0;
-
+// SM count of the current device (cached per device; benign concurrent fill)
 int num_sms() {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n <= 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        cache[dev].store(n, std::memory_order_relaxed);
     }
-    return g_num_sms;
+    return n;
 }
 
 }  // namespace
@@ -723,16 +728,19 @@ int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStrea
 
 int make_grid_tmap(Plan &p) {
     // FLOAT64 view of the padded grid: dims {2 N2p, N1p, N0}; one box = one slab
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    // driver entry point, looked up once (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult qr;
         void *fn = nullptr;
-        SGL_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
-        if (qr != cudaDriverEntryPointSuccess || !fn) {
-            set_error("cuTensorMapEncodeTiled is unavailable");
-            return SGL_ECUDA;
-        }
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) {
+        cudaGetLastError();
+        set_error("cuTensorMapEncodeTiled is unavailable");
+        return SGL_ECUDA;
     }
     const WindowParams &w = p.wp;
     cuuint64_t dims[3] = {(cuuint64_t)2 * w.N2p, (cuuint64_t)w.N1p, (cuuint64_t)w.N0};
