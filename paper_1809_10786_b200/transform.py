@@ -88,6 +88,13 @@ class SglPlan:
         return out
 
     @property
+    def r_nodes(self) -> np.ndarray:
+        """Radial Chebyshev nodes rho (1 + cos w_j) / 2, w_j = (2j+1) pi / 4B
+        (transform.py:365); the device folds them into its radial matrices."""
+        w = (2 * np.arange(2 * self.B) + 1) * np.pi / (4 * self.B)
+        return self.rho * (1 + np.cos(w)) / 2
+
+    @property
     def tiles(self) -> int:
         return int(self._info.n_tiles)
 
