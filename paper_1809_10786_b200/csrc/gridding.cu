@@ -256,6 +256,9 @@ __global__ void __launch_bounds__(GT, GCPS)
         // truncation |delta| <= q is applied exactly
         const double u0n = S.nu[0][node];
         const int a_first = max(0, (int)ceil(u0n - wp.q) - t.o0);
+        // last in-window slab: |u0 - cell| <= q <=> ceil(u0 - q) <= cell <= floor(u0 + q),
+        // both bounds exact (a double minus a small integer is exact)
+        const int a_last = (int)floor(u0n + wp.q) - t.o0;
         double w0r, r0r;
         {
             const double d = u0n - (double)(t.o0 + a_first);
@@ -277,8 +280,7 @@ __global__ void __launch_bounds__(GT, GCPS)
             const int buf = (int)(q % NST);
             double w0 = 0.0;
             if (a >= a_first) {
-                const double dl = u0n - (double)(t.o0 + a);
-                w0 = (fabs(dl) <= (double)wp.q) ? w0r : 0.0;
+                w0 = (a <= a_last) ? w0r : 0.0;
                 w0r *= r0r;
                 r0r *= r0step;
             }
