@@ -71,14 +71,23 @@ void free_plan(Plan *p) {
 }
 
 struct PlanGuard {
+    // Serialises calls on one plan: host threads by the mutex, streams by
+    // waiting on the previous call's completion event.  Inside a CUDA-graph
+    // capture the graph's own dependencies order the work, and an event
+    // recorded outside the capture may not be waited on, so the event is
+    // left alone there.
     Plan &p;
     cudaStream_t st;
     std::lock_guard<std::mutex> lock;
+    bool capturing = false;
     PlanGuard(Plan &pl, cudaStream_t s) : p(pl), st(s), lock(pl.mu) {
-        if (p.done) cudaStreamWaitEvent(st, p.done, 0);
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) cudaGetLastError();
+        capturing = cs != cudaStreamCaptureStatusNone;
+        if (p.done && !capturing) cudaStreamWaitEvent(st, p.done, 0);
     }
     ~PlanGuard() {
-        if (p.done) cudaEventRecord(p.done, st);
+        if (p.done && !capturing) cudaEventRecord(p.done, st);
     }
 };
 

@@ -346,3 +346,31 @@ def test_plan_shared_across_threads(sgl):
     assert not errs
     for k in range(4):
         assert rel(res[("f", k)], g["fwd"]) <= TOL and rel(res[("a", k)], g["adj"]) <= TOL
+
+
+def test_cuda_graph_capture(sgl):
+    """forward / adjoint on device tensors can be captured into a CUDA graph
+    and replayed (e.g. a CG loop); replays match eager calls."""
+    import torch
+    g = load_golden("b12_q12")
+    dev = torch.device("cuda", 0)
+    p = sgl.plan(12, g["points"], q=12, rho=float(g["rho"]))
+    c = torch.as_tensor(g["coeffs"], device=dev)
+    v = torch.as_tensor(g["values"], device=dev)
+    f0, a0 = sgl.forward(p, c).clone(), sgl.adjoint(p, v).clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        sgl.forward(p, c)
+        sgl.adjoint(p, v)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fo = sgl.forward(p, c)
+        ao = sgl.adjoint(p, v)
+    c.mul_(2.0)   # replays read the captured buffers' current contents
+    graph.replay()
+    torch.cuda.synchronize()
+    assert rel(fo.cpu().numpy(), 2.0 * f0.cpu().numpy()) <= 1e-13
+    assert rel(ao.cpu().numpy(), a0.cpu().numpy()) <= 1e-13
+    assert rel(fo.cpu().numpy(), 2.0 * g["fwd"]) <= TOL
