@@ -57,6 +57,7 @@ void free_plan(Plan *p) {
         cufftDestroy(p->fft2);
         cufftDestroy(p->fft1);
     }
+    if (p->fft_work) cudaFree(p->fft_work);
     if (p->done) cudaEventDestroy(p->done);
     if (p->ev_a) cudaEventDestroy(p->ev_a);
     if (p->ev_b) cudaEventDestroy(p->ev_b);
@@ -410,34 +411,50 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         // 64-bit plan: the padded grid exceeds 2^31 elements from B = 256 on
         // rank d over the active (trailing) axes; the SGL transform is 3-D
         const int rank = p->raw ? p->d : 3;
-        long long n[3] = {p->grid[0], p->grid[1], p->grid[2]};
-        long long emb[3] = {wp.N0, wp.N1p, wp.N2p};
-        const long long dist = (long long)p->grid_elems;
-        size_t work = 0;
-        rc = fft_check(cufftCreate(&p->fft), "cufftCreate");
-        if (rc == SGL_OK) {
-            p->fft_ready = true;
-            rc = fft_check(cufftMakePlanMany64(p->fft, rank, n + 3 - rank, emb + 3 - rank, 1, dist, emb + 3 - rank,
-                                               1, dist, CUFFT_Z2Z, 1, &work),
-                           "cufftMakePlanMany64");
-        }
-        // pruned variant when at most half the axis-0 planes carry the spectrum
+        // Pruned FFT when at most half the axis-0 planes carry the spectrum:
+        // a batched 2-D plan and a 1-D plan sharing one work area; otherwise
+        // (or if those plans fail) a single rank-d plan
         const char *fe = getenv("SGL_FFT");
         const bool want = rank == 3 && 2 * p->n_axis[0] <= p->grid[0] && !(fe && !strcmp(fe, "full"));
-        if (rc == SGL_OK && want) {
+        if (want) {
             long long n2[2] = {p->grid[1], p->grid[2]}, e2[2] = {wp.N1p, wp.N2p};
             const long long pl = (long long)wp.N1p * wp.N2p;
             long long n1[1] = {p->grid[0]}, e1[1] = {p->grid[0]};
             size_t w2 = 0, w1 = 0;
+            bool made2 = false, made1 = false;
             bool ok = cufftCreate(&p->fft2) == CUFFT_SUCCESS;
+            made2 = ok;
             ok = ok && cufftCreate(&p->fft1) == CUFFT_SUCCESS;
+            made1 = ok;
+            ok = ok && cufftSetAutoAllocation(p->fft2, 0) == CUFFT_SUCCESS &&
+                 cufftSetAutoAllocation(p->fft1, 0) == CUFFT_SUCCESS;
             ok = ok && cufftMakePlanMany64(p->fft2, 2, n2, e2, 1, pl, e2, 1, pl, CUFFT_Z2Z, p->n_axis[0] / 2, &w2) ==
                            CUFFT_SUCCESS;
             ok = ok && cufftMakePlanMany64(p->fft1, 1, n1, e1, pl, 1, e1, pl, 1, CUFFT_Z2Z, pl, &w1) == CUFFT_SUCCESS;
+            const size_t wmax = std::max(w2, w1);
+            ok = ok && (wmax == 0 || cudaMalloc(&p->fft_work, wmax) == cudaSuccess);
+            ok = ok && cufftSetWorkArea(p->fft2, p->fft_work) == CUFFT_SUCCESS &&
+                 cufftSetWorkArea(p->fft1, p->fft_work) == CUFFT_SUCCESS;
             p->pruned = ok;
             if (!ok) {
-                cufftDestroy(p->fft2);
-                cufftDestroy(p->fft1);
+                cudaGetLastError();
+                if (made2) cufftDestroy(p->fft2);
+                if (made1) cufftDestroy(p->fft1);
+                if (p->fft_work) cudaFree(p->fft_work);
+                p->fft_work = nullptr;
+            }
+        }
+        if (!p->pruned) {
+            long long n[3] = {p->grid[0], p->grid[1], p->grid[2]};
+            long long emb[3] = {wp.N0, wp.N1p, wp.N2p};
+            const long long dist = (long long)p->grid_elems;
+            size_t work = 0;
+            rc = fft_check(cufftCreate(&p->fft), "cufftCreate");
+            if (rc == SGL_OK) {
+                p->fft_ready = true;
+                rc = fft_check(cufftMakePlanMany64(p->fft, rank, n + 3 - rank, emb + 3 - rank, 1, dist,
+                                                   emb + 3 - rank, 1, dist, CUFFT_Z2Z, 1, &work),
+                               "cufftMakePlanMany64");
             }
         }
     }

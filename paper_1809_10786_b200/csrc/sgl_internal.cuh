@@ -122,6 +122,7 @@ struct Plan {
     // receive (adjoint) the n0 spectral planes, 1-D transforms along axis 0
     cufftHandle fft2 = 0, fft1 = 0;
     bool pruned = false;
+    void *fft_work = nullptr;       // shared cuFFT work area of fft2 / fft1
 
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
