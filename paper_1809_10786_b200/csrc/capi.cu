@@ -350,9 +350,10 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     wp.N2p = wp.N2 + 2 * q;
     wp.q = q;
     p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
-    // planes smaller than the TMA slab box (kBoxMax^2 cells) also take the tiled
-    // kernels: the box reads past the padded plane come back as zeros (TMA
-    // out-of-bounds fill) and meet zero window weights
+    // the TMA slab box (kBoxMax^2 cells) must fit the padded plane; smaller
+    // grids use the per-node kernels (a box larger than the tensor gave wrong
+    // slabs for windows that wrap more than once: tools/soak.py)
+    if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         if (exact) {

@@ -42,21 +42,24 @@ __device__ __forceinline__ double wfun(double u, int cell, double c, double h, i
     return (fabs(d) <= (double)q) ? c * exp(-d * d * h) : 0.0;
 }
 
-// w(j) = wfun(u, o + s j) for j = 0 .. N-1 (j < n live, 0 beyond) by the
-// Gaussian's two-term recurrence w(j+1) = w(j) r(j), r(j+1) = r(j) e^{-2 h s^2},
-// seeded exactly at the first j inside the window; d = u - (o + s j) is formed
-// exactly as wfun forms it, so the truncation |d| <= q is bit-identical and
-// the values differ from wfun's by a few ulps.  3 exps instead of N.
+// w(j) = wfun(u, o + S j) for j = 0 .. N-1 (j < n live, 0 beyond) by the
+// Gaussian's two-term recurrence w(j+1) = w(j) r(j), r(j+1) = r(j) e^{-2 h S^2},
+// seeded at the first cell of the node's window (window_cells: the
+// reference's own tap rule, decided on fl(u - cell)); values differ from
+// wfun's by a few ulps.  3 exps instead of N.
 template <int N, int S>
 __device__ __forceinline__ void wwalk(double u, int o, int n, double c, double h, double rs, int q, double (&w)[N]) {
-    const double base = u - (double)o;
-    const int j0 = max(0, (int)ceil((base - q) / S));
-    const double d0 = base - (double)(S * j0);
+    int c_lo, c_hi;
+    window_cells(u, q, c_lo, c_hi);
+    // first j with o + S j >= c_lo (integer ceiling; c_lo - o may be negative)
+    const int num = c_lo - o;
+    const int j0 = num <= 0 ? 0 : (num + S - 1) / S;
+    const double d0 = u - (double)(o + S * j0);
     double cur = c * exp(-d0 * d0 * h), r = exp(h * (2.0 * S * d0 - (double)(S * S)));
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-        const double d = base - (double)(S * j);
-        w[j] = (j >= j0 && j < n && fabs(d) <= (double)q) ? cur : 0.0;
+        const int cell = o + S * j;
+        w[j] = (j >= j0 && j < n && cell >= c_lo && cell <= c_hi) ? cur : 0.0;
         if (j >= j0) {
             cur *= r;
             r *= rs;
@@ -255,10 +258,9 @@ __global__ void __launch_bounds__(GT, GCPS)
         // node's first in-window slab (relative drift <= e0 ulps); the
         // truncation |delta| <= q is applied exactly
         const double u0n = S.nu[0][node];
-        const int a_first = max(0, (int)ceil(u0n - wp.q) - t.o0);
-        // last in-window slab: |u0 - cell| <= q <=> ceil(u0 - q) <= cell <= floor(u0 + q),
-        // both bounds exact (a double minus a small integer is exact)
-        const int a_last = (int)floor(u0n + wp.q) - t.o0;
+        int c_lo0, c_hi0;
+        window_cells(u0n, wp.q, c_lo0, c_hi0);
+        const int a_first = max(0, c_lo0 - t.o0), a_last = c_hi0 - t.o0;
         double w0r, r0r;
         {
             const double d = u0n - (double)(t.o0 + a_first);
@@ -353,6 +355,7 @@ struct ScatterSmem {
                                       // (pitch WS: the re and im rows sit in different banks)
     double2 v[SN];
     double nu[3][SN];
+    int clo0[SN], chi0[SN];           // axis-0 window cells per node (window_cells)
     Tile t;
 };
 
@@ -447,6 +450,10 @@ __global__ void __launch_bounds__(STH, 2)
             S.nu[1][tid] = ok ? nodes.u1[s] : -1e9;
             S.nu[2][tid] = ok ? nodes.u2[s] : -1e9;
             S.v[tid] = ok ? values[nodes.perm[s]] : make_double2(0.0, 0.0);
+            int clo = 1 << 30, chi = -(1 << 30);   // no window for a padding node
+            if (ok) window_cells(nodes.u0[s], wp.q, clo, chi);
+            S.clo0[tid] = clo;
+            S.chi0[tid] = chi;
         }
         __syncthreads();
         const int Mt = (t.e1 + 3) >> 2;
@@ -483,10 +490,10 @@ __global__ void __launch_bounds__(STH, 2)
         const double r0step = wp.r0_8;
 #pragma unroll
         for (int j = 0; j < SN / 32; ++j) {
-            const double F = S.nu[0][32 * j + lane] - (double)t.o0;
-            const int k0 = max(0, (int)ceil((ceil(F - wp.q) - warp) / (double)SW));
+            const int clo = S.clo0[32 * j + lane] - t.o0;           // first in-window slab
+            const int k0 = clo > warp ? (clo - warp + SW - 1) / SW : 0;
             a0s[j] = warp + SW * k0;
-            const double df = F - (double)a0s[j];
+            const double df = S.nu[0][32 * j + lane] - (double)(t.o0 + a0s[j]);
             w0s[j] = wp.c0 * exp(-df * df * wp.h0);
             r0s[j] = exp(wp.h0 * (2.0 * SW * df - (double)(SW * SW)));
         }
@@ -495,8 +502,7 @@ __global__ void __launch_bounds__(STH, 2)
             int kfirst = SKS, klast = -1;
 #pragma unroll
             for (int j = 0; j < SN / 32; ++j) {
-                const double dl = S.nu[0][32 * j + lane] - (double)(t.o0 + a);
-                const double w = (a >= a0s[j] && fabs(dl) <= (double)wp.q) ? w0s[j] : 0.0;
+                const double w = (a >= a0s[j] && a + t.o0 <= S.chi0[32 * j + lane]) ? w0s[j] : 0.0;
                 if (a >= a0s[j]) {
                     w0s[j] *= r0s[j];
                     r0s[j] *= r0step;

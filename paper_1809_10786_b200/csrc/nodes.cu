@@ -69,6 +69,7 @@ __global__ void k_torus(const double *pts, int64_t M, int d, int N0, int N1, int
 struct KeyGeom {
     int N0, N1, N2, W1, W2, P2;   // pencils of W1 x W2 cells on axes 1-2, P2 per row
     uint64_t line_base;           // first key of the grid-line nodes (see k_key)
+    int q;                        // window half-width (grid-line test)
 };
 
 __global__ void k_warp(const double *pts, int64_t M, double rho, int N0, int N1, int N2, double *u0,
@@ -97,12 +98,15 @@ __global__ void k_key(const double *u0, const double *u1, const double *u2, int6
     if (i >= M) return;
     const double v1 = u1[i], v2 = u2[i];
     const int l0 = (int)floor(u0[i]), l1 = (int)floor(v1), l2 = (int)floor(v2);
-    // A node exactly on a grid line of axis 1 or 2 has 2q+1 taps there, so in
+    // A node on (or within rounding of) a grid line of axis 1 or 2 has 2q+1 taps there, so in
     // a W-wide pencil its box would exceed the device slab and cut the tile
     // short (structured inputs: config 2's lattice puts ~2 % of its nodes on
     // the phi = k pi/2 and theta = pi/2 planes).  Such nodes get their own
     // single-cell pencils after all regular ones.
-    if (g.line_base && (v1 == (double)l1 || v2 == (double)l2)) {
+    int c1lo, c1hi, c2lo, c2hi;
+    window_cells(v1, g.q, c1lo, c1hi);
+    window_cells(v2, g.q, c2lo, c2hi);
+    if (g.line_base && (c1hi - c1lo == 2 * g.q || c2hi - c2lo == 2 * g.q)) {
         key[i] = g.line_base + ((uint64_t)l1 * (uint64_t)g.N2 + (uint64_t)l2) * (uint64_t)g.N0 + (uint64_t)l0;
     } else {
         const uint64_t pencil = (uint64_t)(l1 / g.W1) * (uint64_t)g.P2 + (uint64_t)(l2 / g.W2);
@@ -165,10 +169,10 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
             int tmn[3], tmx[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                int lo = lo_of(uu[d]);
-                int lower = lo - g.q + ((uu[d] > (double)lo) ? 1 : 0);   // a node on a grid line has 2q+1 taps
-                tmn[d] = min(mn[d], lower);
-                tmx[d] = max(mx[d], lo + g.q);
+                int c_lo, c_hi;   // the reference's taps: 2q+1 on (or within rounding of) a grid line, else 2q
+                window_cells(uu[d], g.q, c_lo, c_hi);
+                tmn[d] = min(mn[d], c_lo);
+                tmx[d] = max(mx[d], c_hi);
             }
             // the box must fit the device slab (axes 1, 2) and the slab-count limit (axis 0)
             if (j > i && (tmx[1] - tmn[1] + 1 > kBoxMax || tmx[2] - tmn[2] + 1 > kBoxMax ||
@@ -225,7 +229,7 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
         SGL_CUDA_CHECK(cudaMalloc(&ns.perm, sizeof(int32_t) * (M ? M : 1)));
     }
     if (M == 0) return SGL_OK;
-    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2, 0};
+    KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2, 0, p.q};
     const uint64_t regular = (uint64_t)((p.grid[1] + W1 - 1) / W1) * kg.P2 * (uint64_t)p.grid[0];
     if (W1 > 1 || W2 > 1) kg.line_base = regular;
     DevBuf<uint64_t> key, key_s;

@@ -60,6 +60,18 @@ struct WindowParams {
     double r2_1, r2_4;          // axis 2
 };
 
+// The cells a node's window covers on one axis, exactly as the reference
+// decides them (nfft.py:131-141): the 2q+1 offsets lo-q .. lo+q, lo = floor(u),
+// minus those with |fl(u - cell)| > q.  Only the first offset can drop out
+// (u - (lo+q) = frac(u) - q >= -q always); it stays in when u sits on, or
+// within rounding of, a grid line.  [c_lo, c_hi] inclusive.
+__host__ __device__ inline void window_cells(double u, int q, int &c_lo, int &c_hi) {
+    const double f = floor(u);
+    const int lo = (int)f;
+    c_lo = lo - q + ((u - (double)(lo - q) <= (double)q) ? 0 : 1);
+    c_hi = lo + q;
+}
+
 struct StageTimer {
     cudaEvent_t ev[SGL_STAGE_COUNT + 1];
     bool ready = false;

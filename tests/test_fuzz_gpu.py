@@ -52,3 +52,38 @@ def test_random_plan_matches_oracle(seed):
         assert p.nfft.grid_shape == tuple(op.grid)
         assert rel(sgl.forward(p, c), f_ref) <= 1e-10, (backend, B, sigma, q, compact)
         assert rel(sgl.adjoint(p, v), a_ref) <= 1e-10, (backend, B, sigma, q, compact)
+
+
+def _soak_case(seed):
+    # tools/soak.py's generator: lattice nodes put u within rounding of grid
+    # lines, where the reference keeps the edge tap (|fl(u - cell)| <= q)
+    rng = np.random.default_rng(10_000 + seed)
+    B = int(rng.integers(1, 33))
+    sigma = int(rng.choice([2, 2, 2, 3]))
+    q = int(rng.integers(2, 17))
+    if q >= 4 * sigma * B:
+        q = max(1, 4 * sigma * B - 1)
+    M = int(rng.choice([1, 7, 100, 3000, 50_000, 200_000]))
+    kind = int(rng.integers(0, 4))
+    assert kind == 2
+    import paper_1809_10786_b200 as sgl
+    pts = sgl.gen_grid(max(2, int(round(M ** (1 / 3)))), float(rng.uniform(1.0, 6.0)))
+    compact = bool(rng.random() < 0.2)
+    return B, sigma, q, compact, pts, sgl.gen_coeffs(B, rng), rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(
+        -1, 1, len(pts))
+
+
+@pytest.mark.parametrize("seed", [578, 702, 892, 1634, 2311])
+def test_grid_line_edge_taps(seed):
+    """Regression (tools/soak.py): nodes within rounding of a grid line keep
+    the 2q+1-th tap exactly when the reference does (window_cells), in the
+    tiled tiles, fragments, tables and slab ranges; tiny grids."""
+    import paper_1809_10786_b200 as sgl
+    from oracle import sgl_oracle as o
+    B, sigma, q, compact, pts, c, v = _soak_case(seed)
+    op = o.oracle_plan(B, pts, sigma=sigma, q=q, compact_k1=compact)
+    f_ref, a_ref = o.oracle_forward(op, c), o.oracle_adjoint(op, v)
+    for backend in ("auto", "generic"):
+        p = sgl.plan(B, pts, sigma=sigma, q=q, compact_k1=compact, backend=backend)
+        assert rel(sgl.forward(p, c), f_ref) <= 1e-12, backend
+        assert rel(sgl.adjoint(p, v), a_ref) <= 1e-12, backend
