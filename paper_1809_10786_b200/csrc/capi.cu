@@ -145,7 +145,7 @@ cudaError_t ensure_side(Plan &p) {
 // planes [0, n0/2) U [N0 - n0/2, N0): zero on input of the inverse
 // transform, not read after the forward one.
 int grid_fft(Plan &p, cudaStream_t st, int dir) {
-    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.q * p.wp.N2p + p.q);
+    cufftDoubleComplex *interior = reinterpret_cast<cufftDoubleComplex *>(p.grid_buf + (size_t)p.wp.pad * p.wp.N2p + p.wp.pad);
     if (!p.pruned) {
         int rc = fft_check(cufftSetStream(p.fft, st), "cufftSetStream");
         if (rc) return rc;
@@ -346,14 +346,17 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     wp.N0 = p->grid[0];
     wp.N1 = p->grid[1];
     wp.N2 = p->grid[2];
-    wp.N1p = wp.N1 + 2 * q;
-    wp.N2p = wp.N2 + 2 * q;
+    // halo width: q, widened on grids whose padded plane would be smaller than
+    // the TMA slab box (kBoxMax^2) so that the box always fits the plane
+    int pad = q;
+    if (!exact && q > 0 && std::min(wp.N1, wp.N2) + 2 * q < kBoxMax)
+        pad = (kBoxMax - std::min(wp.N1, wp.N2) + 1) / 2;
+    wp.N1p = wp.N1 + 2 * pad;
+    wp.N2p = wp.N2 + 2 * pad;
     wp.q = q;
+    wp.pad = pad;
     p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
-    // the TMA slab box (kBoxMax^2 cells) must fit the padded plane; smaller
-    // grids use the per-node kernels (a box larger than the tensor gave wrong
-    // slabs for windows that wrap more than once: tools/soak.py)
-    if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;
+    if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;   // (not reached: pad widens the plane)
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         if (exact) {

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(GT, GCPS)
             uint32_t q = 0;
             for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
                 const Tile t = tiles[ti];
-                const int c0 = 2 * (t.o2 + wp.q), c1 = t.o1 + wp.q;
+                const int c0 = 2 * (t.o2 + wp.pad), c1 = t.o1 + wp.pad;
                 for (int a = 0; a < t.e0; ++a, ++q) {
                     const int buf = (int)(q % NST);
                     const uint32_t use = q / NST;
@@ -391,7 +391,7 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
         const int b = (mt0 + i) * 4 + rb;
         if (b < t.e1) {
             // halo-padded grid: rows / columns of the box never wrap
-            double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.q)) * wp.N2p + (t.o2 + wp.q));
+            double *row = grid + 2 * (((size_t)g0 * wp.N1p + (t.o1 + b + wp.pad)) * wp.N2p + (t.o2 + wp.pad));
 #pragma unroll
             for (int ct = 0; ct < NCT; ++ct) {
 #pragma unroll
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(NW_GEN * 32)
         for (int b = 0; b < P1; ++b) {
             const double wab = wa * w1[b];
             const int g1 = wrapi(l1 - wp.qa1 + b, wp.N1);
-            const double2 *row = grid + ((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q;
+            const double2 *row = grid + ((size_t)g0 * wp.N1p + g1 + wp.pad) * wp.N2p + wp.pad;
             double sr = 0.0, si = 0.0;
             for (int c = lane; c < P2; c += 32) {
                 const double2 g = row[wrapi(l2 - wp.qa2 + c, wp.N2)];
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(NW_GEN * 32)
             const double wab = wa * w1[b];
             const double tr = wab * v.x, tim = wab * v.y;
             const int g1 = wrapi(l1 - wp.qa1 + b, wp.N1);
-            double *row = grid + 2 * (((size_t)g0 * wp.N1p + g1 + wp.q) * wp.N2p + wp.q);
+            double *row = grid + 2 * (((size_t)g0 * wp.N1p + g1 + wp.pad) * wp.N2p + wp.pad);
             for (int c = lane; c < P2; c += 32) {
                 const int g2 = wrapi(l2 - wp.qa2 + c, wp.N2);
                 red_add(row + 2 * g2, w2[c] * tr);
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(NW_GEN * 32)
 // and below the interior (full padded width) and the q-column strips beside
 // it; 32-bit index math, no pass over the interior.
 __global__ void k_halo_fill(WindowParams wp, double2 *__restrict__ grid) {
-    const int q = wp.q, band = 2 * q * wp.N2p, per_plane = band + 2 * q * wp.N1;
+    const int q = wp.pad, band = 2 * q * wp.N2p, per_plane = band + 2 * q * wp.N1;
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= per_plane) return;
     int p1, p2;
@@ -643,9 +643,9 @@ __device__ __forceinline__ void fold_cell(const WindowParams &wp, double2 *grid,
     double2 acc = make_double2(0.0, 0.0);
     bool any = false;
     // every padded position p = i + q + k N inside [0, N + 2q), except k = 0 on both axes
-    for (int p1 = (i1 + wp.q) % wp.N1; p1 < wp.N1p; p1 += wp.N1) {
-        for (int p2 = (i2 + wp.q) % wp.N2; p2 < wp.N2p; p2 += wp.N2) {
-            if (p1 == i1 + wp.q && p2 == i2 + wp.q) continue;
+    for (int p1 = (i1 + wp.pad) % wp.N1; p1 < wp.N1p; p1 += wp.N1) {
+        for (int p2 = (i2 + wp.pad) % wp.N2; p2 < wp.N2p; p2 += wp.N2) {
+            if (p1 == i1 + wp.pad && p2 == i2 + wp.pad) continue;
             const double2 v = grid[((size_t)g0 * wp.N1p + p1) * wp.N2p + p2];
             acc.x += v.x;
             acc.y += v.y;
@@ -653,7 +653,7 @@ __device__ __forceinline__ void fold_cell(const WindowParams &wp, double2 *grid,
         }
     }
     if (any) {
-        double2 &dst = grid[((size_t)g0 * wp.N1p + i1 + wp.q) * wp.N2p + i2 + wp.q];
+        double2 &dst = grid[((size_t)g0 * wp.N1p + i1 + wp.pad) * wp.N2p + i2 + wp.pad];
         dst.x += acc.x;
         dst.y += acc.y;
     }
@@ -661,7 +661,7 @@ __device__ __forceinline__ void fold_cell(const WindowParams &wp, double2 *grid,
 
 __global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
     // blockIdx.y = axis-0 plane; 32-bit index math within the plane
-    const int q1 = min(wp.q, wp.N1), q2 = min(wp.q, wp.N2);
+    const int q1 = min(wp.pad, wp.N1), q2 = min(wp.pad, wp.N2);
     const int band_rows = min(wp.N1, 2 * q1);              // rows [0,q) and [N1-q, N1)
     const int strip = min(wp.N2, 2 * q2);                   // columns [0,q) and [N2-q, N2)
     const int per_plane = band_rows * wp.N2 + (wp.N1 - band_rows) * strip;
@@ -767,16 +767,16 @@ int make_grid_tmap(Plan &p) {
 }
 
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st) {
-    if (p.wp.q == 0) return SGL_OK;
-    const int per_plane = 2 * p.wp.q * p.wp.N2p + 2 * p.wp.q * p.wp.N1;
+    if (p.wp.pad == 0) return SGL_OK;
+    const int per_plane = 2 * p.wp.pad * p.wp.N2p + 2 * p.wp.pad * p.wp.N1;
     k_halo_fill<<<dim3((per_plane + 255) / 256, p.wp.N0), 256, 0, st>>>(p.wp, grid);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
 
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st) {
-    if (p.wp.q == 0) return SGL_OK;
-    const int q1 = std::min(p.wp.q, p.wp.N1), q2 = std::min(p.wp.q, p.wp.N2);
+    if (p.wp.pad == 0) return SGL_OK;
+    const int q1 = std::min(p.wp.pad, p.wp.N1), q2 = std::min(p.wp.pad, p.wp.N2);
     const int band_rows = std::min(p.wp.N1, 2 * q1), strip = std::min(p.wp.N2, 2 * q2);
     const int per_plane = band_rows * p.wp.N2 + (p.wp.N1 - band_rows) * strip;
     k_halo_fold<<<dim3((per_plane + 255) / 256, p.wp.N0), 256, 0, st>>>(p.wp, grid);

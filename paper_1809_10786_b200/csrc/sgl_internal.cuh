@@ -50,6 +50,7 @@ struct WindowParams {
     int32_t N0, N1, N2;
     int32_t N1p, N2p;
     int32_t q;
+    int32_t pad;                // halo width on axes 1-2 (>= q; wider on grids smaller than the TMA box)
     int32_t qa0, qa1, qa2;      // per-axis tap half-width of the generic kernels (0 on the
                                 // dummy axes of a d < 3 NFFT plan: one tap of weight 1)
     double c0, c1, c2;          // (N/2pi)/sqrt(2 pi lam)
