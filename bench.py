@@ -88,6 +88,9 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t_end = time.time() + 1.0   # short timed regions: wait for the first sample (<= 1 s)
+        while not any(r and r[0].replace(".", "").isdigit() for r in self.rows) and time.time() < t_end:
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)

@@ -36,3 +36,12 @@ def test_reference_arm_other_ranks_are_silent():
     r = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--config", "1", "--points", "3000"],
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_metric_names():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.metric_name(3, "both", 64, 1) == "NFSGLFT nodes/sec fwd+adj at B=64"
+    assert bench.metric_name(1, "fwd", 16, 1) == "NFSGLFT nodes/sec fwd at B=16"
+    assert bench.metric_name(4, "adj", 128, 1) == "NFSGLFT nodes/sec adj at B=128"
+    assert "64 vectors" in bench.metric_name(5, "fwd", 48, 64)
