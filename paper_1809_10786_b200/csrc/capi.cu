@@ -49,7 +49,8 @@ void free_plan(Plan *p) {
     void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->snodes.u0, p->snodes.u1, p->snodes.u2,
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
-                    p->coef_buf, p->val_buf};
+                    p->coef_buf, p->val_buf, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
+                    p->itiles, p->digits, p->gmax};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
@@ -192,7 +193,7 @@ int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRe
     rc = launch_halo_fill(p, p.grid_buf, st);
     if (rc) return rc;
     mark(SGL_STAGE_WINDOW);
-    return launch_gather(p, p.grid_buf, v, st);
+    return p.i8 ? launch_gather_i8(p, p.grid_buf, v, st) : launch_gather(p, p.grid_buf, v, st);
 }
 
 int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRec *rec) {
@@ -303,6 +304,10 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->precise = flags & SGL_FLAG_PRECISE;
     p->exact = exact;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
+    {
+        const char *ge = getenv("SGL_GATHER");   // "i8": int8 tensor-core gather (experimental)
+        p->i8 = !p->generic && ge && !strcmp(ge, "i8");
+    }
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
     p->n_axis[2] = 2 * B;
@@ -357,6 +362,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     wp.pad = pad;
     p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
     if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;   // (not reached: pad widens the plane)
+    if (wp.N1p < kI8Box1 || pad != q) p->i8 = false;   // digit TMA box within the plane; aligned K ranges
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         if (exact) {
@@ -463,6 +469,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         }
     }
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
+    if (rc == SGL_OK && p->i8) rc = setup_i8(*p);
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");
         rc = SGL_ECUDA;

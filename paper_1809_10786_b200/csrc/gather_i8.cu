@@ -1,0 +1,488 @@
+// Gaussian-window gather (forward NFFT interpolation, _gridding.py:53-74) on
+// the int8 tensor cores (tcgen05.mma kind::i8), reproducing FP64 results by an
+// exact integer digit split (Ozaki scheme).  sm_100a.
+//
+// Per tile of <= 128 sorted nodes (one 8 x 16 pencil of cells on axes 1-2,
+// consecutive in lo0) and its box of e0 x 40 x 48 cells, the window sum
+//     out[n] = sum_b w1[n,b] sum_{a,c} w0[n,a] w2[n,c] G[a,b,c]
+// is a GEMM with M = nodes, N = (b, re|im) = 80 and K = (a, c) = e0 x 48:
+//     D[n, (b,ri)] = sum_k A[n,k] G_ri[k,b],  A[n,(a,c)] = w0[n,a] w2[n,c].
+// Both operands are scaled to fixed point and split into 6 bytes:
+//     A * 2^sA = sum_p a_p 256^p   (a_p unsigned: the weights are >= 0)
+//     G * 2^sG = sum_q g_q 256^q   (g_q signed, balanced digits)
+// so A G = 2^-(sA+sG) sum_{p,q} 256^(p+q) (a_p . g_q), every a_p . g_q an
+// exact int32 dot product.  The 21 digit pairs with p + q >= 5 are kept
+// (dropped pairs are below 2^-45 of the product scale); pairs with equal
+// p + q share one int32 TMEM accumulator (6 "diagonals" x 80 columns = 480
+// of the 512 TMEM columns), and one MMA multiplies A digit p with up to
+// three consecutive B digits stacked along N (N = 240), 9 MMAs per K-step of
+// 32.  The epilogue converts the diagonals to FP64, applies the scale and the
+// axis-1 weights w1[n,b] and writes the node values in caller order.
+//
+// Grid digits are produced once per forward (k_slice_grid, after the halo
+// fill) as planes [a][digit][b][re|im][c] and reach shared memory by TMA
+// (one 6-digit x 80-row x 16-cell box per K-chunk).  The weight digits are
+// built per tile by 8 generator warps directly in the UMMA K-major layout.
+//
+// CTA (one per SM, persistent over tiles): warp 0 TMA producer, warp 1 MMA
+// issuer (one lane), warps 2-9 weight-digit generators, warps 10-13 epilogue
+// (TMEM lane quarters).  4-stage smem ring (full / empty mbarriers), TMEM
+// full / empty mbarriers between the MMA issuer and the epilogue.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "sgl_internal.cuh"
+#include "umma.cuh"
+
+namespace sgl {
+namespace {
+
+constexpr int ND = 6;                     // byte digits per operand
+constexpr int DMIN = 5;                   // kept digit diagonals p + q = DMIN .. 2 ND - 2
+constexpr int NBLK = 2 * ND - 1 - DMIN;   // 6 TMEM accumulators
+constexpr int IM = kI8Nodes;              // MMA M (nodes)
+constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
+constexpr int CHUNKS = kI8Box2 / 16;      // 16-cell K-chunks per slab
+constexpr int NSTG = 4;                   // smem ring depth (K-steps of 32)
+constexpr int A_DIGIT = IM * 16;          // one K-chunk of one weight digit (2048 B)
+constexpr int A_CHUNK = ND * A_DIGIT;
+constexpr int A_STAGE = 2 * A_CHUNK;
+constexpr int B_DIGIT = ROWS * 16;        // one K-chunk of one grid digit (1280 B)
+constexpr int B_CHUNK = ND * B_DIGIT;     // one TMA box
+constexpr int B_STAGE = 2 * B_CHUNK;
+constexpr int NGW = 8;                    // generator warps (2 K-chunks x 128 nodes)
+constexpr int NEW = 4;                    // epilogue warps
+constexpr int IT = (2 + NGW + NEW) * 32;
+constexpr uint32_t TCOLS = 512;
+constexpr double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, y, MAGIC) rounds x y to an integer
+static_assert(NBLK * ROWS <= (int)TCOLS, "diagonal accumulators must fit TMEM");
+static_assert(CHUNKS == 3, "K-chunk bookkeeping assumes 48-cell slabs");
+
+struct I8Smem {
+    uint8_t a[NSTG][A_STAGE];     // weight digits, [chunk][digit][node][16 cells]
+    uint8_t b[NSTG][B_STAGE];     // grid digits,   [chunk][digit][b][re|im][16 cells]
+    double w2[kI8Box2][IM];       // axis-2 weights of the tile, scaled by 2^s2
+    uint64_t fullA[NSTG], fullB[NSTG], empty[NSTG];
+    uint64_t tfull, tempty;
+    uint32_t tbase;
+};
+
+// MMA schedule of one K-step (SGL_I8_OP list in the issuer): A digit p times
+// B digits q0 .. q0+nq-1 (stacked along N) into the diagonal accumulators
+// p+q0-DMIN .. ; 21 digit pairs with p + q >= DMIN in 9 MMAs.
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+    i %= n;
+    return i < 0 ? i + n : i;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(umma::smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(umma::smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int tag = 0) {
+    uint32_t ok = 0, spins = 0;
+    for (;;) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(umma::smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (++spins == (1u << 26)) __trap();   // lost phase: trap instead of hanging the GPU
+    }
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];\n" ::"r"(umma::smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(umma::smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NGW * 32) : "memory"); }
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+    return r;
+}
+
+// scale of the grid digits from the device max: |G| 2^sG < 2^46
+__device__ __forceinline__ int grid_shift(const unsigned long long *gmax) {
+    const double m = __longlong_as_double((long long)*gmax);
+    if (!(m > 0.0) || !isfinite(m)) return 0;
+    int ex;
+    frexp(m, &ex);   // m < 2^ex
+    return 46 - ex;
+}
+
+// First padded axis-2 cell of a slab's K range: the TMA box start of the
+// innermost dimension must be 16-byte aligned (measured: unaligned starts
+// fault with an illegal instruction), so the 48-cell K range starts at the
+// 16-aligned cell at or below the box origin; 16-aligned pencils with
+// pad == q <= 16 keep every window inside it (checked at plan time).
+__host__ __device__ __forceinline__ int kstart2(const Tile &t, const WindowParams &wp) {
+    return (t.o2 + wp.pad) & ~15;
+}
+
+__device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * t.e0 + 1) >> 1; }
+
+__global__ void __launch_bounds__(IT, 1)
+    k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
+                NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
+                const unsigned long long *__restrict__ gmax, double2 *__restrict__ out, int dbg) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    I8Smem &S = *reinterpret_cast<I8Smem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTG; ++s) {
+            mbar_init(&S.fullA[s], NGW);
+            mbar_init(&S.fullB[s], 1);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.tfull, 1);
+        mbar_init(&S.tempty, NEW);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 1) umma::tmem_alloc(&S.tbase, TCOLS);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tbase = S.tbase;
+
+    if (warp == 0) {
+        // ---- TMA producer: grid digits, two 16-cell K-chunks per stage
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&dmap) : "memory");
+            uint32_t g = 0;
+            for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+                const Tile t = tiles[ti];
+                const int ns = (int)tile_steps(t);
+                const int cb = kstart2(t, wp), bb = t.o1 + wp.pad;   // TMA rows are (b, re|im) pairs
+                for (int s = 0; s < ns; ++s, ++g) {
+                    const int stg = (int)(g % NSTG);
+                    const uint32_t use = g / NSTG;
+                    if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 1);
+                    mbar_expect_tx(&S.fullB[stg], B_STAGE);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int kc = 2 * s + h, al = kc / CHUNKS, cc = kc - CHUNKS * al;
+                        tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, cb + 16 * cc, 2 * bb, 0, wrapi(t.o0 + al, wp.N0),
+                                    &S.fullB[stg]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer: the warp waits, one elected lane issues.  The 9
+        // MMAs of a K-step use compile-time digit offsets and instruction
+        // descriptors on top of two per-stage base descriptors.
+        const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), A_CHUNK, 128);
+        const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_CHUNK, 128);
+        uint32_t g = 0, tc = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tc) {
+            const int ns = (int)tile_steps(tiles[ti]);
+            if (tc) mbar_wait(&S.tempty, (tc - 1) & 1, 2);
+            umma::fence_after();
+            for (int s = 0; s < ns; ++s, ++g) {
+                const int stg = (int)(g % NSTG);
+                const uint32_t par = (g / NSTG) & 1;
+                mbar_wait(&S.fullB[stg], par, 3);
+                mbar_wait(&S.fullA[stg], par, 4);
+                umma::fence_after();
+                if (umma::elect_one()) {
+                    const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
+                    const uint64_t bd = b0 + (uint64_t)(stg * (B_STAGE >> 4));
+                    const bool acc = s > 0;
+                    {
+#define SGL_I8_OP(P, Q0, NQ, ACC)                                                                              \
+    umma::mma_i8(tbase + (uint32_t)(((P) + (Q0)-DMIN) * ROWS), ad + (uint64_t)((P)*A_DIGIT >> 4),             \
+                 bd + (uint64_t)((Q0)*B_DIGIT >> 4), umma::idesc_i8(IM, (NQ)*ROWS, false, true), ACC)
+                        // the two p = 5 MMAs cover every accumulator and carry the per-tile reset
+                        SGL_I8_OP(5, 0, 3, acc);
+                        SGL_I8_OP(5, 3, 3, acc);
+                        SGL_I8_OP(4, 1, 3, true);
+                        SGL_I8_OP(4, 4, 2, true);
+                        SGL_I8_OP(3, 2, 3, true);
+                        SGL_I8_OP(3, 5, 1, true);
+                        SGL_I8_OP(2, 3, 3, true);
+                        SGL_I8_OP(1, 4, 2, true);
+                        SGL_I8_OP(0, 5, 1, true);
+#undef SGL_I8_OP
+                    }
+                    umma::commit(&S.empty[stg]);
+                }
+                __syncwarp();
+            }
+            if (umma::elect_one()) umma::commit(&S.tfull);
+            __syncwarp();
+        }
+    } else if (warp < 2 + NGW) {
+        // ---- weight-digit generators: thread = (node n, K-chunk parity h)
+        const int gt = tid - 64, n = gt & (IM - 1), h = gt >> 7;
+        uint32_t g = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile t = tiles[ti];
+            const bool live = n < t.count;
+            const int64_t si = (int64_t)t.start + n;
+            const double u0 = live ? nodes.u0[si] : -1e9, u2 = live ? nodes.u2[si] : -1e9;
+            int lo0, hi0, lo2, hi2;
+            window_cells(u0, wp.q, lo0, hi0);
+            window_cells(u2, wp.q, lo2, hi2);
+            gen_sync();   // the previous tile's readers of S.w2 are done
+            const int c2base = kstart2(t, wp) - wp.pad;   // cell of K column 0 of a slab
+            for (int c = h * (kI8Box2 / 2); c < (h + 1) * (kI8Box2 / 2); ++c) {
+                const int cell = c2base + c;
+                const double d = u2 - (double)cell;
+                S.w2[c][n] = (live && cell >= lo2 && cell <= hi2) ? s2 * (wp.c2 * exp(-d * d * wp.h2)) : 0.0;
+            }
+            gen_sync();
+            const int ns = (int)tile_steps(t);
+            for (int s = 0; s < ns; ++s, ++g) {
+                const int stg = (int)(g % NSTG);
+                const uint32_t use = g / NSTG;
+                const int kc = 2 * s + h, al = kc / CHUNKS, c16 = (kc - CHUNKS * al) * 16;
+                const int cell0 = t.o0 + al;
+                const double d0 = u0 - (double)cell0;
+                const double w0 = (live && cell0 >= lo0 && cell0 <= hi0) ? s0 * (wp.c0 * exp(-d0 * d0 * wp.h0)) : 0.0;
+                uint32_t dw[ND][4];
+#pragma unroll
+                for (int grp = 0; grp < 4; ++grp) {
+                    uint32_t L[4], H[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const double y = fma(w0, S.w2[c16 + grp * 4 + e][n], MAGIC);
+                        L[e] = (uint32_t)__double2loint(y);
+                        H[e] = (uint32_t)__double2hiint(y);
+                    }
+                    const uint32_t t0 = prmt(L[0], L[1], 0x5140), t1 = prmt(L[2], L[3], 0x5140);
+                    const uint32_t t2 = prmt(L[0], L[1], 0x7362), t3 = prmt(L[2], L[3], 0x7362);
+                    const uint32_t h0 = prmt(H[0], H[1], 0x5140), h1 = prmt(H[2], H[3], 0x5140);
+                    dw[0][grp] = prmt(t0, t1, 0x5410);
+                    dw[1][grp] = prmt(t0, t1, 0x7632);
+                    dw[2][grp] = prmt(t2, t3, 0x5410);
+                    dw[3][grp] = prmt(t2, t3, 0x7632);
+                    dw[4][grp] = prmt(h0, h1, 0x5410);
+                    dw[5][grp] = prmt(h0, h1, 0x7632);
+                }
+                if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 5);
+                uint8_t *dst = S.a[stg] + h * A_CHUNK + n * 16;
+#pragma unroll
+                for (int p = 0; p < ND; ++p)
+                    *reinterpret_cast<uint4 *>(dst + p * A_DIGIT) = make_uint4(dw[p][0], dw[p][1], dw[p][2], dw[p][3]);
+                umma::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.fullA[stg]);
+            }
+        }
+    } else {
+        // ---- epilogue: thread = node = TMEM lane
+        const int quarter = warp & 3, n = quarter * 32 + lane;
+        const int sG = grid_shift(gmax);
+        double f[NBLK];
+#pragma unroll
+        for (int k = 0; k < NBLK; ++k) f[k] = ldexp(1.0, 8 * (k + DMIN) - sA - sG);
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
+        uint32_t tc = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tc) {
+            const Tile t = tiles[ti];
+            const bool live = n < t.count;
+            const int64_t si = (int64_t)t.start + n;
+            const double u1 = live ? nodes.u1[si] : -1e9;
+            int lo1, hi1;
+            window_cells(u1, wp.q, lo1, hi1);
+            mbar_wait(&S.tfull, tc & 1, 6);
+            umma::fence_after();
+            double acc_re = 0.0, acc_im = 0.0;
+#pragma unroll 1
+            for (int cb = 0; cb < ROWS / 8; ++cb) {   // 8 columns = 4 axis-1 cells (re, im)
+                int32_t D[NBLK][8];
+                __syncwarp();   // tcgen05.ld is .sync.aligned: the warp must be converged
+#pragma unroll
+                for (int k = 0; k < NBLK; ++k) umma::tmem_ld8(tl + (uint32_t)(k * ROWS + cb * 8), D[k]);
+                umma::tmem_ld_wait();
+                double v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    double x = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NBLK; ++k) x = fma((double)D[k][j], f[k], x);
+                    v[j] = x;
+                }
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb) {
+                    const int cell = t.o1 + cb * 4 + jb;
+                    const double d = u1 - (double)cell;
+                    const double w = (live && cell >= lo1 && cell <= hi1) ? wp.c1 * exp(-d * d * wp.h1) : 0.0;
+                    acc_re = fma(w, v[2 * jb], acc_re);
+                    acc_im = fma(w, v[2 * jb + 1], acc_im);
+                }
+            }
+            umma::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.tempty);
+            if (live) out[nodes.perm[si]] = make_double2(acc_re, acc_im);
+        }
+    }
+
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        umma::fence_after();
+        umma::tmem_free(tbase, TCOLS);
+    }
+}
+
+// max(|Re G|, |Im G|) over the padded grid (bits of a non-negative double
+// order like the double)
+__global__ void k_grid_absmax(const double2 *__restrict__ g, size_t n, unsigned long long *out) {
+    double m = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double2 v = g[i];
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// Grid -> balanced byte digits: G 2^sG = sum_j d_j 256^j, d_j in [-128, 127],
+// planes [a][j][b][re|im][c] (row pitch P2 bytes, zero beyond N2p).  Thread =
+// 4 consecutive cells of one row.
+__global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int P2,
+                             const unsigned long long *__restrict__ gmax, uint8_t *__restrict__ dig) {
+    const int sG = grid_shift(gmax);
+    const double sc = ldexp(1.0, sG);
+    const int64_t per_row = P2 / 4, rows = (int64_t)wp.N0 * wp.N1p;
+    const int64_t total = rows * per_row;
+    const size_t plane = (size_t)wp.N1p * 2 * P2;   // one digit of one slab
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / per_row;
+        const int c4 = (int)(i - row * per_row) * 4;
+        const int a = (int)(row / wp.N1p), b = (int)(row - (int64_t)a * wp.N1p);
+        uint32_t w[ND][2] = {};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = c4 + e;
+            double2 v = make_double2(0.0, 0.0);
+            if (c < wp.N2p) v = g[(size_t)row * wp.N2p + c];
+#pragma unroll
+            for (int ri = 0; ri < 2; ++ri) {
+                const double y = fma(ri ? v.y : v.x, sc, MAGIC);
+                long long f = __double_as_longlong(y) - __double_as_longlong(MAGIC);   // rint(x 2^sG)
+#pragma unroll
+                for (int j = 0; j < ND; ++j) {
+                    const long long d = (long long)(int8_t)(f & 0xff);   // balanced digit
+                    w[j][ri] |= ((uint32_t)(uint8_t)d) << (8 * e);
+                    f = (f - d) >> 8;
+                }
+            }
+        }
+        uint8_t *base = dig + (size_t)a * ND * plane + (size_t)b * 2 * P2 + c4;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+            *reinterpret_cast<uint32_t *>(base + j * plane) = w[j][0];
+            *reinterpret_cast<uint32_t *>(base + j * plane + P2) = w[j][1];
+        }
+    }
+}
+
+void i8_scales(const Plan &p, double &s0, double &s2, int &sA) {
+    // A 2^sA = w0 w2 2^sA <= c0 c2 2^sA < 2^47 (6 unsigned bytes with room)
+    const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
+    sA = 47 - e;
+    const int a0 = sA / 2;
+    s0 = std::ldexp(1.0, a0);
+    s2 = std::ldexp(1.0, sA - a0);
+}
+
+}  // namespace
+
+int setup_i8(Plan &p) {
+    const WindowParams &w = p.wp;
+    if (p.n_itiles > 0) {
+        std::vector<Tile> ht(p.n_itiles);
+        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.itiles, sizeof(Tile) * p.n_itiles, cudaMemcpyDeviceToHost));
+        for (const Tile &t : ht) {
+            const int k0 = kstart2(t, w);
+            if (t.o2 + w.pad < k0 || t.o2 + w.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 || t.e0 > kBox0Max ||
+                t.count > kI8Nodes) {
+                set_error("internal: int8 gather tile outside its K range");
+                return SGL_ECUDA;
+            }
+        }
+    }
+    p.P2 = (w.N2p + 15) / 16 * 16;
+    const size_t bytes = (size_t)w.N0 * ND * w.N1p * 2 * p.P2;
+    if (cudaMalloc(&p.digits, bytes) != cudaSuccess || cudaMalloc(&p.gmax, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("out of device memory for the int8 grid digits");
+        return SGL_ENOMEM;
+    }
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+        cudaDriverEntryPointQueryResult qr;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) {
+        cudaGetLastError();
+        set_error("cuTensorMapEncodeTiled is unavailable");
+        return SGL_ECUDA;
+    }
+    // dims (innermost first): c, row = (b, re|im), digit, a
+    cuuint64_t dims[4] = {(cuuint64_t)p.P2, (cuuint64_t)2 * w.N1p, (cuuint64_t)ND, (cuuint64_t)w.N0};
+    cuuint64_t strides[3] = {(cuuint64_t)p.P2, (cuuint64_t)2 * p.P2 * w.N1p, (cuuint64_t)ND * 2 * p.P2 * w.N1p};
+    cuuint32_t box[4] = {16, (cuuint32_t)(2 * kI8Box1), (cuuint32_t)ND, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&p.dmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, p.digits, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (digits) failed: " + std::to_string((int)r));
+        return SGL_ECUDA;
+    }
+    return SGL_OK;
+}
+
+int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st) {
+    if (p.M == 0) return SGL_OK;
+    const int sms = num_sms();
+    SGL_CUDA_CHECK(cudaMemsetAsync(p.gmax, 0, sizeof(unsigned long long), st));
+    k_grid_absmax<<<sms * 8, 256, 0, st>>>(grid, p.grid_elems, reinterpret_cast<unsigned long long *>(p.gmax));
+    SGL_CUDA_CHECK(cudaGetLastError());
+    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, reinterpret_cast<const unsigned long long *>(p.gmax),
+                                           p.digits);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    double s0, s2;
+    int sA;
+    i8_scales(p, s0, s2, sA);
+    const size_t sm = sizeof(I8Smem);
+    SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
+    k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA,
+                                                  reinterpret_cast<const unsigned long long *>(p.gmax), values,
+                                                  getenv("SGL_I8_DEBUG") ? atoi(getenv("SGL_I8_DEBUG")) : 0);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+}  // namespace sgl

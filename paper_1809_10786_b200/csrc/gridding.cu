@@ -682,6 +682,8 @@ __global__ void k_halo_fold(WindowParams wp, double2 *__restrict__ grid) {
     fold_cell(wp, grid, blockIdx.y, i1, i2);
 }
 
+}  // namespace
+
 // SM count of the current device (cached per device; benign concurrent fill)
 int num_sms() {
     static std::atomic<int> cache[64];
@@ -696,6 +698,8 @@ int num_sms() {
     }
     return n;
 }
+
+namespace {
 
 }  // namespace
 

@@ -142,6 +142,7 @@ struct TileGeom {
     int span0;      // max lo0 span inside a tile
     int max_nodes;  // nodes per tile
     int box0;       // max box extent on axis 0
+    int box1 = kBoxMax, box2 = kBoxMax;   // max box extents on axes 1-2
 };
 
 __device__ __forceinline__ int lo_of(double u) { return (int)floor(u); }
@@ -175,7 +176,7 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
                 tmx[d] = max(mx[d], c_hi);
             }
             // the box must fit the device slab (axes 1, 2) and the slab-count limit (axis 0)
-            if (j > i && (tmx[1] - tmn[1] + 1 > kBoxMax || tmx[2] - tmn[2] + 1 > kBoxMax ||
+            if (j > i && (tmx[1] - tmn[1] + 1 > g.box1 || tmx[2] - tmn[2] + 1 > g.box2 ||
                           tmx[0] - tmn[0] + 1 > g.box0))
                 break;
 #pragma unroll
@@ -375,6 +376,17 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     int rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max},
                             p.nodes, &p.tiles, &p.n_tiles, !p.generic, st);
     if (rc || p.generic) return rc;
+    if (p.i8) {
+        // int8 tensor-core gather: 8 x 16 pencils (box 40 x 48 = MMA N x 3 K-chunks per slab), 128-node tiles
+        TileGeom ig{p.q, kBox0Max - 2 * p.q - 1, kI8Nodes, kBox0Max};
+        ig.box1 = kI8Box1;
+        ig.box2 = kI8Box2;
+        rc = order_and_tile(p, a0.p, a1.p, a2.p, kI8Box1 - 32, kI8Box2 - 32, ig, p.inodes, &p.itiles, &p.n_itiles,
+                            true, st);
+        if (rc) return rc;
+        rc = reorder_tiles(p.itiles, p.n_itiles, st);
+        if (rc) return rc;
+    }
     // Scatter order: with dense nodes, W x W2 pencils whose axis-2 box is a
     // multiple of 8 (exact 8-column DMMA tiles, ~17 % fewer DMMAs; warps own
     // whole slabs, so a long lo0 span costs nothing); sparse node sets keep

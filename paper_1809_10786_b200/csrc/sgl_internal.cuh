@@ -28,6 +28,11 @@ constexpr int kSTileNodes = 128; // scatter tiles: GEMM K-dim (more nodes per RE
 constexpr int kSBox0Max = 96;    // scatter: max box extent on axis 0 (no smem cost)
 constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
 
+// int8 tensor-core gather tiles (gather_i8.cu)
+constexpr int kI8Nodes = 128;    // tcgen05 M
+constexpr int kI8Box1 = 40;      // axis-1 box (80 re|im rows per digit = MMA N)
+constexpr int kI8Box2 = 48;      // axis-2 box (3 K-chunks of 16 cells per slab)
+
 struct Tile {
     int32_t start;    // first sorted node
     int32_t count;    // nodes in tile (1..kTileNodes)
@@ -137,6 +142,18 @@ struct Plan {
     bool pruned = false;
     void *fft_work = nullptr;       // shared cuFFT work area of fft2 / fft1
 
+    // int8 tensor-core window stage (gather_i8.cu): FP64 reproduced from
+    // byte digits of the window weights and of the grid (Ozaki split) on
+    // tcgen05.mma kind::i8; own node order / tiles (8 x 16 pencils, 128 nodes)
+    bool i8 = false;
+    NodeSet inodes;
+    Tile *itiles = nullptr;
+    int64_t n_itiles = 0;
+    uint8_t *digits = nullptr;     // N0 x 6 x N1p x 2 x P2 signed bytes
+    int P2 = 0;                    // byte pitch of a digit row (>= N2p, multiple of 16)
+    uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
+    alignas(64) CUtensorMap dmap;  // TMA descriptor of the digit planes
+
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
 
@@ -185,5 +202,8 @@ int launch_direct_adjoint(int B, int64_t M, const double *pts, const double2 *v,
                           cudaStream_t st);
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
+int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
+int setup_i8(Plan &p);
+int num_sms();
 
 }  // namespace sgl
