@@ -252,32 +252,48 @@ __global__ void __launch_bounds__(IT, 1)
             }
             gen_sync();
             const int ns = (int)tile_steps(t);
+            // W0 along the slabs by the Gaussian two-term recurrence, seeded at
+            // the node's first window slab (the slab index of this thread's
+            // chunks advances by 0 or 1 per K-step); the window limits are exact
+            const int a_first = max(0, lo0 - t.o0), a_last = hi0 - t.o0;
+            int acur = -1;
+            double wcur = 0.0, rcur = 0.0;
             for (int s = 0; s < ns; ++s, ++g) {
                 const int stg = (int)(g % NSTG);
                 const uint32_t use = g / NSTG;
                 const int kc = 2 * s + h, al = kc / CHUNKS, c16 = (kc - CHUNKS * al) * 16;
-                const int cell0 = t.o0 + al;
-                const double d0 = u0 - (double)cell0;
-                const double w0 = (live && cell0 >= lo0 && cell0 <= hi0) ? s0 * (wp.c0 * exp(-d0 * d0 * wp.h0)) : 0.0;
+                if (al != acur) {
+                    acur = al;
+                    if (al == a_first) {
+                        const double d0 = u0 - (double)(t.o0 + al);
+                        wcur = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                        rcur = exp(wp.h0 * (2.0 * d0 - 1.0));
+                    } else if (al > a_first) {
+                        wcur *= rcur;
+                        rcur *= wp.r0_1;
+                    }
+                }
+                const double w0 = (live && al >= a_first && al <= a_last) ? wcur : 0.0;
                 uint32_t dw[ND][4];
 #pragma unroll
-                for (int grp = 0; grp < 4; ++grp) {
+                for (int q4 = 0; q4 < 4; ++q4) {
                     uint32_t L[4], H[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const double y = fma(w0, S.w2[c16 + grp * 4 + e][n], MAGIC);
+                        const double y = fma(w0, S.w2[c16 + q4 * 4 + e][n], MAGIC);
                         L[e] = (uint32_t)__double2loint(y);
                         H[e] = (uint32_t)__double2hiint(y);
                     }
+                    // byte transpose: digit p of the 4 entries -> one word
                     const uint32_t t0 = prmt(L[0], L[1], 0x5140), t1 = prmt(L[2], L[3], 0x5140);
                     const uint32_t t2 = prmt(L[0], L[1], 0x7362), t3 = prmt(L[2], L[3], 0x7362);
                     const uint32_t h0 = prmt(H[0], H[1], 0x5140), h1 = prmt(H[2], H[3], 0x5140);
-                    dw[0][grp] = prmt(t0, t1, 0x5410);
-                    dw[1][grp] = prmt(t0, t1, 0x7632);
-                    dw[2][grp] = prmt(t2, t3, 0x5410);
-                    dw[3][grp] = prmt(t2, t3, 0x7632);
-                    dw[4][grp] = prmt(h0, h1, 0x5410);
-                    dw[5][grp] = prmt(h0, h1, 0x7632);
+                    dw[0][q4] = prmt(t0, t1, 0x5410);
+                    dw[1][q4] = prmt(t0, t1, 0x7632);
+                    dw[2][q4] = prmt(t2, t3, 0x5410);
+                    dw[3][q4] = prmt(t2, t3, 0x7632);
+                    dw[4][q4] = prmt(h0, h1, 0x5410);
+                    dw[5][q4] = prmt(h0, h1, 0x7632);
                 }
                 if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 5);
                 uint8_t *dst = S.a[stg] + h * A_CHUNK + n * 16;
