@@ -7,12 +7,16 @@
 //     out[n] = sum_b w1[n,b] sum_{a,c} w0[n,a] w2[n,c] G[a,b,c]
 // is a GEMM with M = nodes, N = (b, re|im) = 80 and K = (a, c) = e0 x 48:
 //     D[n, (b,ri)] = sum_k A[n,k] G_ri[k,b],  A[n,(a,c)] = w0[n,a] w2[n,c].
-// Both operands are scaled to fixed point and split into 6 bytes:
-//     A * 2^sA = sum_p a_p 256^p   (a_p unsigned: the weights are >= 0)
-//     G * 2^sG = sum_q g_q 256^q   (g_q signed, balanced digits)
+// Both operands are scaled to fixed point and split into 6 balanced signed
+// bytes (digits in [-128, 127]: zero-mean truncation error):
+//     A * 2^sA = sum_p a_p 256^p,   G * 2^sG(a) = sum_q g_q 256^q,
 // so A G = 2^-(sA+sG) sum_{p,q} 256^(p+q) (a_p . g_q), every a_p . g_q an
-// exact int32 dot product.  The 21 digit pairs with p + q >= 5 are kept
-// (dropped pairs are below 2^-45 of the product scale); pairs with equal
+// exact int32 dot product.  The grid scale is per slab (sG(a), from the slab's
+// max |G|: the slab envelope spans up to 1e15 at B = 64); a tile works at the
+// scale of its largest slab, sG_t = min_a sG(a), and the weight digits absorb
+// the slab factor, A'[n,(a,c)] = A 2^(sG_t - sG(a)) <= A.  The 21 digit pairs
+// with p + q >= 5 are kept (tools/ozaki_sim.py: ~1e-12 relative on the
+// reference goldens, the dropped pairs being the leading error); pairs with equal
 // p + q share one int32 TMEM accumulator (6 "diagonals" x 80 columns = 480
 // of the 512 TMEM columns), and one MMA multiplies A digit p with up to
 // three consecutive B digits stacked along N (N = 240), 9 MMAs per K-step of
@@ -60,6 +64,10 @@ constexpr int NEW = 4;                    // epilogue warps
 constexpr int IT = (2 + NGW + NEW) * 32;
 constexpr uint32_t TCOLS = 512;
 constexpr double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, y, MAGIC) rounds x y to an integer
+// + 128 in each of the 6 digit bytes: the bytes of fma(x, y, MAGIC_BAL) are
+// the balanced digits of rint(x y) (< 2^46) offset by 128 (undone by ^ 0x80)
+constexpr double MAGIC_BAL = 6755399441055744.0 + 141289400074368.0;
+constexpr int NOSLAB = 4096;   // shift of an all-zero slab (never the tile minimum)
 static_assert(NBLK * ROWS <= (int)TCOLS, "diagonal accumulators must fit TMEM");
 static_assert(CHUNKS == 3, "K-chunk bookkeeping assumes 48-cell slabs");
 
@@ -120,13 +128,25 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     return r;
 }
 
-// scale of the grid digits from the device max: |G| 2^sG < 2^46
-__device__ __forceinline__ int grid_shift(const unsigned long long *gmax) {
-    const double m = __longlong_as_double((long long)*gmax);
-    if (!(m > 0.0) || !isfinite(m)) return 0;
+// digit shift of a slab from its max |G| (bits of a non-negative double):
+// |G| 2^sG < 2^46
+__device__ __forceinline__ int slab_shift(unsigned long long bits) {
+    const double m = __longlong_as_double((long long)bits);
+    if (!(m > 0.0) || !isfinite(m)) return NOSLAB;
     int ex;
     frexp(m, &ex);   // m < 2^ex
     return 46 - ex;
+}
+
+// 2^e for e <= 0 (0 below 2^-1022)
+__device__ __forceinline__ double pow2n(int e) {
+    return e < -1022 ? 0.0 : __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// slab index modulo N0 for boxes that start at most one period out
+__device__ __forceinline__ int wrap1(int a, int n) {
+    a += a < 0 ? n : 0;
+    return a >= n ? a - n : a;
 }
 
 // First padded axis-2 cell of a slab's K range: the TMA box start of the
@@ -143,7 +163,7 @@ __device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * 
 __global__ void __launch_bounds__(IT, 1)
     k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
                 NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
-                const unsigned long long *__restrict__ gmax, double2 *__restrict__ out, int dbg) {
+                const int *__restrict__ gsh, const int *__restrict__ tsh, double2 *__restrict__ out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     I8Smem &S = *reinterpret_cast<I8Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -181,7 +201,7 @@ __global__ void __launch_bounds__(IT, 1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int kc = 2 * s + h, al = kc / CHUNKS, cc = kc - CHUNKS * al;
-                        tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, cb + 16 * cc, 2 * bb, 0, wrapi(t.o0 + al, wp.N0),
+                        tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, cb + 16 * cc, 2 * bb, 0, wrap1(t.o0 + al, wp.N0),
                                     &S.fullB[stg]);
                     }
                 }
@@ -211,7 +231,7 @@ __global__ void __launch_bounds__(IT, 1)
                     {
 #define SGL_I8_OP(P, Q0, NQ, ACC)                                                                              \
     umma::mma_i8(tbase + (uint32_t)(((P) + (Q0)-DMIN) * ROWS), ad + (uint64_t)((P)*A_DIGIT >> 4),             \
-                 bd + (uint64_t)((Q0)*B_DIGIT >> 4), umma::idesc_i8(IM, (NQ)*ROWS, false, true), ACC)
+                 bd + (uint64_t)((Q0)*B_DIGIT >> 4), umma::idesc_i8(IM, (NQ)*ROWS, true, true), ACC)
                         // the two p = 5 MMAs cover every accumulator and carry the per-tile reset
                         SGL_I8_OP(5, 0, 3, acc);
                         SGL_I8_OP(5, 3, 3, acc);
@@ -245,10 +265,25 @@ __global__ void __launch_bounds__(IT, 1)
             window_cells(u2, wp.q, lo2, hi2);
             gen_sync();   // the previous tile's readers of S.w2 are done
             const int c2base = kstart2(t, wp) - wp.pad;   // cell of K column 0 of a slab
-            for (int c = h * (kI8Box2 / 2); c < (h + 1) * (kI8Box2 / 2); ++c) {
-                const int cell = c2base + c;
-                const double d = u2 - (double)cell;
-                S.w2[c][n] = (live && cell >= lo2 && cell <= hi2) ? s2 * (wp.c2 * exp(-d * d * wp.h2)) : 0.0;
+            {
+                // this thread's 24 columns by the Gaussian recurrence, seeded at
+                // its first in-window column (2 exps instead of 24)
+                const int cb = h * (kI8Box2 / 2), ce = cb + kI8Box2 / 2;
+                const int cfirst = max(cb, lo2 - c2base);
+                double w = 0.0, r = 0.0;
+                if (cfirst < ce) {
+                    const double d = u2 - (double)(c2base + cfirst);
+                    w = s2 * (wp.c2 * exp(-d * d * wp.h2));
+                    r = exp(wp.h2 * (2.0 * d - 1.0));
+                }
+                for (int c = cb; c < ce; ++c) {
+                    const int cell = c2base + c;
+                    S.w2[c][n] = (live && c >= cfirst && cell <= hi2) ? w : 0.0;
+                    if (c >= cfirst) {
+                        w *= r;
+                        r *= wp.r2_1;
+                    }
+                }
             }
             gen_sync();
             const int ns = (int)tile_steps(t);
@@ -256,14 +291,16 @@ __global__ void __launch_bounds__(IT, 1)
             // the node's first window slab (the slab index of this thread's
             // chunks advances by 0 or 1 per K-step); the window limits are exact
             const int a_first = max(0, lo0 - t.o0), a_last = hi0 - t.o0;
+            const int sGt = __ldg(tsh + ti);
             int acur = -1;
-            double wcur = 0.0, rcur = 0.0;
+            double wcur = 0.0, rcur = 0.0, fslab = 0.0;
             for (int s = 0; s < ns; ++s, ++g) {
                 const int stg = (int)(g % NSTG);
                 const uint32_t use = g / NSTG;
                 const int kc = 2 * s + h, al = kc / CHUNKS, c16 = (kc - CHUNKS * al) * 16;
                 if (al != acur) {
                     acur = al;
+                    fslab = pow2n(sGt - __ldg(gsh + wrap1(t.o0 + al, wp.N0)));   // slab scale -> tile scale
                     if (al == a_first) {
                         const double d0 = u0 - (double)(t.o0 + al);
                         wcur = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
@@ -273,14 +310,14 @@ __global__ void __launch_bounds__(IT, 1)
                         rcur *= wp.r0_1;
                     }
                 }
-                const double w0 = (live && al >= a_first && al <= a_last) ? wcur : 0.0;
+                const double w0 = (live && al >= a_first && al <= a_last) ? wcur * fslab : 0.0;
                 uint32_t dw[ND][4];
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     uint32_t L[4], H[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const double y = fma(w0, S.w2[c16 + q4 * 4 + e][n], MAGIC);
+                        const double y = fma(w0, S.w2[c16 + q4 * 4 + e][n], MAGIC_BAL);
                         L[e] = (uint32_t)__double2loint(y);
                         H[e] = (uint32_t)__double2hiint(y);
                     }
@@ -288,12 +325,12 @@ __global__ void __launch_bounds__(IT, 1)
                     const uint32_t t0 = prmt(L[0], L[1], 0x5140), t1 = prmt(L[2], L[3], 0x5140);
                     const uint32_t t2 = prmt(L[0], L[1], 0x7362), t3 = prmt(L[2], L[3], 0x7362);
                     const uint32_t h0 = prmt(H[0], H[1], 0x5140), h1 = prmt(H[2], H[3], 0x5140);
-                    dw[0][q4] = prmt(t0, t1, 0x5410);
-                    dw[1][q4] = prmt(t0, t1, 0x7632);
-                    dw[2][q4] = prmt(t2, t3, 0x5410);
-                    dw[3][q4] = prmt(t2, t3, 0x7632);
-                    dw[4][q4] = prmt(h0, h1, 0x5410);
-                    dw[5][q4] = prmt(h0, h1, 0x7632);
+                    dw[0][q4] = prmt(t0, t1, 0x5410) ^ 0x80808080u;   // offset bytes -> balanced digits
+                    dw[1][q4] = prmt(t0, t1, 0x7632) ^ 0x80808080u;
+                    dw[2][q4] = prmt(t2, t3, 0x5410) ^ 0x80808080u;
+                    dw[3][q4] = prmt(t2, t3, 0x7632) ^ 0x80808080u;
+                    dw[4][q4] = prmt(h0, h1, 0x5410) ^ 0x80808080u;
+                    dw[5][q4] = prmt(h0, h1, 0x7632) ^ 0x80808080u;
                 }
                 if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 5);
                 uint8_t *dst = S.a[stg] + h * A_CHUNK + n * 16;
@@ -308,10 +345,6 @@ __global__ void __launch_bounds__(IT, 1)
     } else {
         // ---- epilogue: thread = node = TMEM lane
         const int quarter = warp & 3, n = quarter * 32 + lane;
-        const int sG = grid_shift(gmax);
-        double f[NBLK];
-#pragma unroll
-        for (int k = 0; k < NBLK; ++k) f[k] = ldexp(1.0, 8 * (k + DMIN) - sA - sG);
         const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
         uint32_t tc = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tc) {
@@ -321,6 +354,16 @@ __global__ void __launch_bounds__(IT, 1)
             const double u1 = live ? nodes.u1[si] : -1e9;
             int lo1, hi1;
             window_cells(u1, wp.q, lo1, hi1);
+            const int sGt = __ldg(tsh + ti);
+            const double unit = ldexp(1.0, 8 * DMIN - sA - sGt);   // value of diagonal DMIN
+            // W1 along axis 1 by the Gaussian recurrence, seeded before the wait
+            const int bfirst = max(0, lo1 - t.o1), blast = hi1 - t.o1;
+            double w1 = 0.0, r1 = 0.0;
+            {
+                const double d = u1 - (double)(t.o1 + bfirst);
+                w1 = wp.c1 * exp(-d * d * wp.h1);
+                r1 = exp(wp.h1 * (2.0 * d - 1.0));
+            }
             mbar_wait(&S.tfull, tc & 1, 6);
             umma::fence_after();
             double acc_re = 0.0, acc_im = 0.0;
@@ -334,16 +377,20 @@ __global__ void __launch_bounds__(IT, 1)
                 double v[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    double x = 0.0;
-#pragma unroll
-                    for (int k = 0; k < NBLK; ++k) x = fma((double)D[k][j], f[k], x);
-                    v[j] = x;
+                    // sum_k D_k 256^k exactly in two int64 halves, then two conversions
+                    const long long lo = (long long)D[0][j] + (long long)D[1][j] * 256 + (long long)D[2][j] * 65536 +
+                                         (long long)D[3][j] * 16777216;
+                    const long long hi = (long long)D[4][j] + (long long)D[5][j] * 256;
+                    v[j] = fma((double)hi, 4294967296.0 * unit, (double)lo * unit);
                 }
 #pragma unroll
                 for (int jb = 0; jb < 4; ++jb) {
-                    const int cell = t.o1 + cb * 4 + jb;
-                    const double d = u1 - (double)cell;
-                    const double w = (live && cell >= lo1 && cell <= hi1) ? wp.c1 * exp(-d * d * wp.h1) : 0.0;
+                    const int b = cb * 4 + jb;
+                    const double w = (live && b >= bfirst && b <= blast) ? w1 : 0.0;
+                    if (b >= bfirst) {
+                        w1 *= r1;
+                        r1 *= wp.r1_1;
+                    }
                     acc_re = fma(w, v[2 * jb], acc_re);
                     acc_im = fma(w, v[2 * jb + 1], acc_im);
                 }
@@ -364,26 +411,41 @@ __global__ void __launch_bounds__(IT, 1)
     }
 }
 
-// max(|Re G|, |Im G|) over the padded grid (bits of a non-negative double
-// order like the double)
-__global__ void k_grid_absmax(const double2 *__restrict__ g, size_t n, unsigned long long *out) {
+// per slab a: max(|Re G|, |Im G|) (bits of a non-negative double order like
+// the double); grid = (N0 slabs) x (blocks per slab)
+__global__ void k_slab_absmax(const double2 *__restrict__ g, size_t per_slab, unsigned long long *out) {
+    const double2 *s = g + (size_t)blockIdx.y * per_slab;
     double m = 0.0;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const double2 v = g[i];
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slab; i += (size_t)gridDim.x * blockDim.x) {
+        const double2 v = s[i];
         m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + blockIdx.y, (unsigned long long)__double_as_longlong(m));
 }
 
-// Grid -> balanced byte digits: G 2^sG = sum_j d_j 256^j, d_j in [-128, 127],
+// per tile: the shift of its largest slab (the tile's fixed-point reference)
+__global__ void k_tile_shift(const Tile *__restrict__ tiles, int64_t n, WindowParams wp, const int *__restrict__ gsh,
+                             int *__restrict__ tsh) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Tile t = tiles[i];
+    int m = NOSLAB;
+    for (int a = 0; a < t.e0; ++a) m = min(m, gsh[wrap1(t.o0 + a, wp.N0)]);
+    tsh[i] = m;
+}
+
+__global__ void k_slab_shift(const unsigned long long *__restrict__ mx, int n, int *__restrict__ sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) sh[i] = slab_shift(mx[i]);
+}
+
+// Grid -> balanced byte digits: G 2^sG(a) = sum_j d_j 256^j, d_j in [-128, 127],
 // planes [a][j][b][re|im][c] (row pitch P2 bytes, zero beyond N2p).  Thread =
 // 4 consecutive cells of one row.
-__global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int P2,
-                             const unsigned long long *__restrict__ gmax, uint8_t *__restrict__ dig) {
-    const int sG = grid_shift(gmax);
-    const double sc = ldexp(1.0, sG);
+__global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int P2, const int *__restrict__ gsh,
+                             uint8_t *__restrict__ dig) {
     const int64_t per_row = P2 / 4, rows = (int64_t)wp.N0 * wp.N1p;
     const int64_t total = rows * per_row;
     const size_t plane = (size_t)wp.N1p * 2 * P2;   // one digit of one slab
@@ -392,6 +454,8 @@ __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int
         const int64_t row = i / per_row;
         const int c4 = (int)(i - row * per_row) * 4;
         const int a = (int)(row / wp.N1p), b = (int)(row - (int64_t)a * wp.N1p);
+        const int sh = gsh[a];
+        const double sc = sh == NOSLAB ? 0.0 : ldexp(1.0, sh);
         uint32_t w[ND][2] = {};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -420,9 +484,9 @@ __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int
 }
 
 void i8_scales(const Plan &p, double &s0, double &s2, int &sA) {
-    // A 2^sA = w0 w2 2^sA <= c0 c2 2^sA < 2^47 (6 unsigned bytes with room)
+    // A 2^sA = w0 w2 2^sA <= c0 c2 2^sA <= 2^46 (6 balanced bytes)
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
-    sA = 47 - e;
+    sA = 46 - e;
     const int a0 = sA / 2;
     s0 = std::ldexp(1.0, a0);
     s2 = std::ldexp(1.0, sA - a0);
@@ -446,7 +510,10 @@ int setup_i8(Plan &p) {
     }
     p.P2 = (w.N2p + 15) / 16 * 16;
     const size_t bytes = (size_t)w.N0 * ND * w.N1p * 2 * p.P2;
-    if (cudaMalloc(&p.digits, bytes) != cudaSuccess || cudaMalloc(&p.gmax, sizeof(unsigned long long)) != cudaSuccess) {
+    // per slab: max bits (N0 x u64), shift (N0 x int); per tile: shift (n_itiles x int)
+    if (cudaMalloc(&p.digits, bytes) != cudaSuccess ||
+        cudaMalloc(&p.gmax, (sizeof(unsigned long long) + sizeof(int)) * w.N0 + sizeof(int) * (p.n_itiles + 1)) !=
+            cudaSuccess) {
         cudaGetLastError();
         set_error("out of device memory for the int8 grid digits");
         return SGL_ENOMEM;
@@ -482,11 +549,19 @@ int setup_i8(Plan &p) {
 int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st) {
     if (p.M == 0) return SGL_OK;
     const int sms = num_sms();
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.gmax, 0, sizeof(unsigned long long), st));
-    k_grid_absmax<<<sms * 8, 256, 0, st>>>(grid, p.grid_elems, reinterpret_cast<unsigned long long *>(p.gmax));
+    unsigned long long *mx = reinterpret_cast<unsigned long long *>(p.gmax);
+    int *gsh = reinterpret_cast<int *>(mx + p.wp.N0);
+    SGL_CUDA_CHECK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * p.wp.N0, st));
+    const size_t per_slab = (size_t)p.wp.N1p * p.wp.N2p;
+    const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (per_slab + 8191) / 8192));
+    k_slab_absmax<<<dim3(bx, p.wp.N0), 256, 0, st>>>(grid, per_slab, mx);
     SGL_CUDA_CHECK(cudaGetLastError());
-    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, reinterpret_cast<const unsigned long long *>(p.gmax),
-                                           p.digits);
+    k_slab_shift<<<(p.wp.N0 + 255) / 256, 256, 0, st>>>(mx, p.wp.N0, gsh);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.digits);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    int *tsh = gsh + p.wp.N0;
+    k_tile_shift<<<(unsigned)((p.n_itiles + 255) / 256), 256, 0, st>>>(p.itiles, p.n_itiles, p.wp, gsh, tsh);
     SGL_CUDA_CHECK(cudaGetLastError());
     double s0, s2;
     int sA;
@@ -494,9 +569,8 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     const size_t sm = sizeof(I8Smem);
     SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
-    k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA,
-                                                  reinterpret_cast<const unsigned long long *>(p.gmax), values,
-                                                  getenv("SGL_I8_DEBUG") ? atoi(getenv("SGL_I8_DEBUG")) : 0);
+    k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA, gsh,
+                                                  tsh, values);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
