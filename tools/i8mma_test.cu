@@ -120,6 +120,63 @@ __global__ void k_rate(int K, int N, int iters, int32_t *sink) {
     if (warp == 0) umma::tmem_free(td, 512);
 }
 
+// rate with a given descriptor layout: lay 0 = interleave (LBO = M*16), 1 = interleave with LBO + 16,
+// 2 = SW128 K-major (SBO 1024, K advance 32 B), 3 = SW32 K-major (SBO 256)
+__global__ void k_rate2(int N, int iters, int lay, int32_t *sink) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 96 * 1024; i += blockDim.x) sm[i] = (uint8_t)(i * 7);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) umma::tmem_alloc(&tbase, 512);
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t td = tbase;
+    const uint32_t sa = umma::smem_addr(sm), sb = umma::smem_addr(sm + 32768);
+    if (tid == 0) {
+        const uint32_t id = umma::idesc_i8(128, N, true, true);
+        uint64_t da, db;
+        uint32_t kadv_a, kadv_b;
+        if (lay == 0 || lay == 1) {
+            const uint32_t ex = lay == 1 ? 16 : 0;
+            da = umma::desc_kmajor(sa, 128 * 16 + ex, 128);
+            db = umma::desc_kmajor(sb, N * 16 + ex, 128);
+            kadv_a = 2 * (128 * 16 + ex);
+            kadv_b = 2 * (N * 16 + ex);
+        } else if (lay == 2) {
+            da = umma::desc_kmajor(sa, 16, 1024) | ((uint64_t)2 << 61);
+            db = umma::desc_kmajor(sb, 16, 1024) | ((uint64_t)2 << 61);
+            kadv_a = kadv_b = 32;
+        } else {
+            da = umma::desc_kmajor(sa, 16, 256) | ((uint64_t)6 << 61);
+            db = umma::desc_kmajor(sb, 16, 256) | ((uint64_t)6 << 61);
+            kadv_a = 128 * 32;
+            kadv_b = N * 32;
+        }
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb)
+                umma::mma_i8(td + (it & 1) * 256, da + ((kb * kadv_a) >> 4), db + ((kb * kadv_b) >> 4), id, true);
+        umma::commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    umma::fence_after();
+    int32_t v[16];
+    umma::tmem_ld16(td + ((uint32_t)(warp * 32) << 16), v);
+    umma::tmem_ld_wait();
+    if (v[0] == 12345) sink[tid] = v[1];
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(td, 512);
+}
+
 int main() {
     int bad = 0;
     const int K = 96;
@@ -186,6 +243,21 @@ int main() {
             double ops = 2.0 * 128 * N * Kr * (double)iters * sms;
             printf("rate M=128 N=%d K/issue-block=%d: %.1f int8 TOPS (%.3f ms) %s\n", N, Kr, ops / ms / 1e9, ms,
                    cudaGetErrorString(cudaGetLastError()));
+        }
+    for (int lay = 0; lay < 4; ++lay)
+        for (int N : {80, 160, 240, 256}) {
+            cudaFuncSetAttribute(k_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            const int iters = 5000;
+            k_rate2<<<sms, 128, 96 * 1024>>>(N, 100, lay, sink);
+            cudaEventRecord(e0);
+            k_rate2<<<sms, 128, 96 * 1024>>>(N, iters, lay, sink);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double mmas = 4.0 * iters;
+            printf("layout %d N=%d: %.1f cycles/MMA at 1.9 GHz, %.0f TOPS %s\n", lay, N, ms * 1e-3 * 1.9e9 / mmas,
+                   2.0 * 128 * N * 32 * mmas * sms / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
         }
     printf(bad ? "FAIL\n" : "PASS\n");
     return bad;
