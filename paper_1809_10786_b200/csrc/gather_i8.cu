@@ -29,14 +29,15 @@
 // built per tile by 8 generator warps directly in the UMMA K-major layout.
 //
 // CTA (one per SM, persistent over tiles): warp 0 TMA producer, warp 1 MMA
-// issuer (one lane), warps 2-9 weight-digit generators, warps 10-13 epilogue
-// (TMEM lane quarters).  4-stage smem ring (full / empty mbarriers), TMEM
+// issuer (one lane), warps 2-13 weight-digit generators, warps 14-17 epilogue
+// (TMEM lane quarters).  5-stage smem ring (full / empty mbarriers), TMEM
 // full / empty mbarriers between the MMA issuer and the epilogue.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -52,14 +53,14 @@ constexpr int NBLK = 2 * ND - 1 - DMIN;   // 6 TMEM accumulators
 constexpr int IM = kI8Nodes;              // MMA M (nodes)
 constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
 constexpr int CHUNKS = kI8Box2 / 16;      // 16-cell K-chunks per slab
-constexpr int NSTG = 4;                   // smem ring depth (K-steps of 32)
+constexpr int NSTG = 5;                   // smem ring depth (K-steps of 32)
 constexpr int A_DIGIT = IM * 16;          // one K-chunk of one weight digit (2048 B)
 constexpr int A_CHUNK = ND * A_DIGIT;
 constexpr int A_STAGE = 2 * A_CHUNK;
 constexpr int B_DIGIT = ROWS * 16;        // one K-chunk of one grid digit (1280 B)
 constexpr int B_CHUNK = ND * B_DIGIT;     // one TMA box
 constexpr int B_STAGE = 2 * B_CHUNK;
-constexpr int NGW = 8;                    // generator warps (2 K-chunks x 128 nodes)
+constexpr int NGW = 12;                   // generator warps (3 chunk columns x 128 nodes)
 constexpr int NEW = 4;                    // epilogue warps
 constexpr int IT = (2 + NGW + NEW) * 32;
 constexpr uint32_t TCOLS = 512;
@@ -74,7 +75,6 @@ static_assert(CHUNKS == 3, "K-chunk bookkeeping assumes 48-cell slabs");
 struct I8Smem {
     uint8_t a[NSTG][A_STAGE];     // weight digits, [chunk][digit][node][16 cells]
     uint8_t b[NSTG][B_STAGE];     // grid digits,   [chunk][digit][b][re|im][16 cells]
-    double w2[kI8Box2][IM];       // axis-2 weights of the tile, scaled by 2^s2
     uint64_t fullA[NSTG], fullB[NSTG], empty[NSTG];
     uint64_t tfull, tempty;
     uint32_t tbase;
@@ -120,7 +120,6 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, i
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(umma::smem_addr(bar))
         : "memory");
 }
-__device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NGW * 32) : "memory"); }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
     uint32_t r;
@@ -163,14 +162,15 @@ __device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * 
 __global__ void __launch_bounds__(IT, 1)
     k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
                 NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
-                const int *__restrict__ gsh, const int *__restrict__ tsh, double2 *__restrict__ out) {
+                const int *__restrict__ gsh, const int *__restrict__ tsh, double2 *__restrict__ out,
+                unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     I8Smem &S = *reinterpret_cast<I8Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
         for (int s = 0; s < NSTG; ++s) {
-            mbar_init(&S.fullA[s], NGW);
+            mbar_init(&S.fullA[s], 8);   // 2 chunks x 4 warps per K-step
             mbar_init(&S.fullB[s], 1);
             mbar_init(&S.empty[s], 1);
         }
@@ -214,15 +214,24 @@ __global__ void __launch_bounds__(IT, 1)
         const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), A_CHUNK, 128);
         const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_CHUNK, 128);
         uint32_t g = 0, tc = 0;
+        long long pw_a = 0, pw_b = 0, pw_e = 0, pt0 = clock64();
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tc) {
             const int ns = (int)tile_steps(tiles[ti]);
+            long long t0 = clock64();
             if (tc) mbar_wait(&S.tempty, (tc - 1) & 1, 2);
             umma::fence_after();
+            long long t1 = clock64();
+            pw_e += t1 - t0;
             for (int s = 0; s < ns; ++s, ++g) {
                 const int stg = (int)(g % NSTG);
                 const uint32_t par = (g / NSTG) & 1;
+                t0 = clock64();
                 mbar_wait(&S.fullB[stg], par, 3);
+                t1 = clock64();
                 mbar_wait(&S.fullA[stg], par, 4);
+                long long t2 = clock64();
+                pw_b += t1 - t0;
+                pw_a += t2 - t1;
                 umma::fence_after();
                 if (umma::elect_one()) {
                     const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
@@ -251,10 +260,19 @@ __global__ void __launch_bounds__(IT, 1)
             if (umma::elect_one()) umma::commit(&S.tfull);
             __syncwarp();
         }
+        if (prof && lane == 0) {
+            prof[blockIdx.x * 4 + 0] = clock64() - pt0;
+            prof[blockIdx.x * 4 + 1] = pw_a;
+            prof[blockIdx.x * 4 + 2] = pw_b;
+            prof[blockIdx.x * 4 + 3] = pw_e;
+        }
     } else if (warp < 2 + NGW) {
-        // ---- weight-digit generators: thread = (node n, K-chunk parity h)
-        const int gt = tid - 64, n = gt & (IM - 1), h = gt >> 7;
-        uint32_t g = 0;
+        // ---- weight-digit generators: thread = (node n, chunk column cc of a
+        // slab): its 16 W2 values stay in registers for the whole tile and its
+        // chunks kc = cc, cc + 3, ... visit the slabs one by one (W0 by the
+        // Gaussian recurrence); chunk kc goes to half kc % 2 of K-step kc / 2
+        const int gt = tid - 64, n = gt % IM, cc = gt / IM;
+        uint32_t g = 0;   // K-steps of the previous tiles
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
             const bool live = n < t.count;
@@ -263,61 +281,47 @@ __global__ void __launch_bounds__(IT, 1)
             int lo0, hi0, lo2, hi2;
             window_cells(u0, wp.q, lo0, hi0);
             window_cells(u2, wp.q, lo2, hi2);
-            gen_sync();   // the previous tile's readers of S.w2 are done
-            const int c2base = kstart2(t, wp) - wp.pad;   // cell of K column 0 of a slab
+            const int cell2 = kstart2(t, wp) - wp.pad + 16 * cc;   // cell of this thread's first column
+            double w2[16];
             {
-                // this thread's 24 columns by the Gaussian recurrence, seeded at
-                // its first in-window column (2 exps instead of 24)
-                const int cb = h * (kI8Box2 / 2), ce = cb + kI8Box2 / 2;
-                const int cfirst = max(cb, lo2 - c2base);
-                double w = 0.0, r = 0.0;
-                if (cfirst < ce) {
-                    const double d = u2 - (double)(c2base + cfirst);
-                    w = s2 * (wp.c2 * exp(-d * d * wp.h2));
-                    r = exp(wp.h2 * (2.0 * d - 1.0));
-                }
-                for (int c = cb; c < ce; ++c) {
-                    const int cell = c2base + c;
-                    S.w2[c][n] = (live && c >= cfirst && cell <= hi2) ? w : 0.0;
-                    if (c >= cfirst) {
+                const int efirst = max(0, lo2 - cell2);
+                const double d = u2 - (double)(cell2 + efirst);
+                double w = s2 * (wp.c2 * exp(-d * d * wp.h2)), r = exp(wp.h2 * (2.0 * d - 1.0));
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    w2[e] = (live && e >= efirst && cell2 + e <= hi2) ? w : 0.0;
+                    if (e >= efirst) {
                         w *= r;
                         r *= wp.r2_1;
                     }
                 }
             }
-            gen_sync();
             const int ns = (int)tile_steps(t);
-            // W0 along the slabs by the Gaussian two-term recurrence, seeded at
-            // the node's first window slab (the slab index of this thread's
-            // chunks advances by 0 or 1 per K-step); the window limits are exact
             const int a_first = max(0, lo0 - t.o0), a_last = hi0 - t.o0;
             const int sGt = __ldg(tsh + ti);
-            int acur = -1;
-            double wcur = 0.0, rcur = 0.0, fslab = 0.0;
-            for (int s = 0; s < ns; ++s, ++g) {
-                const int stg = (int)(g % NSTG);
-                const uint32_t use = g / NSTG;
-                const int kc = 2 * s + h, al = kc / CHUNKS, c16 = (kc - CHUNKS * al) * 16;
-                if (al != acur) {
-                    acur = al;
-                    fslab = pow2n(sGt - __ldg(gsh + wrap1(t.o0 + al, wp.N0)));   // slab scale -> tile scale
-                    if (al == a_first) {
-                        const double d0 = u0 - (double)(t.o0 + al);
-                        wcur = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
-                        rcur = exp(wp.h0 * (2.0 * d0 - 1.0));
-                    } else if (al > a_first) {
-                        wcur *= rcur;
-                        rcur *= wp.r0_1;
-                    }
+            double wcur = 0.0, rcur = 0.0;
+            for (int kc = cc, al = 0; kc < 2 * ns; kc += CHUNKS, ++al) {
+                // W0 of slab al (recurrence from the node's first window slab)
+                if (al == a_first) {
+                    const double d0 = u0 - (double)(t.o0 + al);
+                    wcur = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                    rcur = exp(wp.h0 * (2.0 * d0 - 1.0));
+                } else if (al > a_first) {
+                    wcur *= rcur;
+                    rcur *= wp.r0_1;
                 }
+                const double fslab = pow2n(sGt - __ldg(gsh + wrap1(t.o0 + al, wp.N0)));   // slab -> tile scale
                 const double w0 = (live && al >= a_first && al <= a_last) ? wcur * fslab : 0.0;
+                const uint32_t gs = g + (uint32_t)(kc >> 1);
+                const int stg = (int)(gs % NSTG), h = kc & 1;
+                const uint32_t use = gs / NSTG;
                 uint32_t dw[ND][4];
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     uint32_t L[4], H[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const double y = fma(w0, S.w2[c16 + q4 * 4 + e][n], MAGIC_BAL);
+                        const double y = fma(w0, w2[q4 * 4 + e], MAGIC_BAL);
                         L[e] = (uint32_t)__double2loint(y);
                         H[e] = (uint32_t)__double2hiint(y);
                     }
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(IT, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.fullA[stg]);
             }
+            g += (uint32_t)ns;
         }
     } else {
         // ---- epilogue: thread = node = TMEM lane
@@ -569,8 +574,25 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     const size_t sm = sizeof(I8Smem);
     SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
+    static unsigned long long *prof = nullptr;
+    const bool want_prof = getenv("SGL_I8_PROF") != nullptr;
+    if (want_prof && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 4 * 1024);
     k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA, gsh,
-                                                  tsh, values);
+                                                  tsh, values, want_prof ? prof : nullptr);
+    if (want_prof) {
+        unsigned long long h[4 * 1024];
+        cudaMemcpyAsync(h, prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        double tot = 0, a = 0, b = 0, e = 0;
+        for (int i = 0; i < blocks; ++i) {
+            tot += h[4 * i];
+            a += h[4 * i + 1];
+            b += h[4 * i + 2];
+            e += h[4 * i + 3];
+        }
+        fprintf(stderr, "i8 MMA warp: total %.0f cycles/CTA, wait fullA %.1f%%, fullB %.1f%%, tempty %.1f%%\n",
+                tot / blocks, 100 * a / tot, 100 * b / tot, 100 * e / tot);
+    }
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
