@@ -24,13 +24,13 @@
 // axis-1 weights w1[n,b] and writes the node values in caller order.
 //
 // Grid digits are produced once per forward (k_slice_grid, after the halo
-// fill) as planes [a][digit][b][re|im][c] and reach shared memory by TMA
-// (one 6-digit x 80-row x 16-cell box per K-chunk).  The weight digits are
+// fill) as [a][c/16][digit][b][re|im][c%16] and reach shared memory by TMA
+// (one 6-digit x 1280-byte box per K-chunk).  The weight digits are
 // built per tile by 8 generator warps directly in the UMMA K-major layout.
 //
 // CTA (one per SM, persistent over tiles): warp 0 TMA producer, warp 1 MMA
 // issuer (one lane), warps 2-13 weight-digit generators, warps 14-17 epilogue
-// (TMEM lane quarters).  5-stage smem ring (full / empty mbarriers), TMEM
+// (TMEM lane quarters).  5-stage weight-digit ring and 7-stage grid-digit ring (full / empty mbarriers), TMEM
 // full / empty mbarriers between the MMA issuer and the epilogue.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -53,7 +53,8 @@ constexpr int NBLK = 2 * ND - 1 - DMIN;   // 6 TMEM accumulators
 constexpr int IM = kI8Nodes;              // MMA M (nodes)
 constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
 constexpr int CHUNKS = kI8Box2 / 16;      // 16-cell K-chunks per slab
-constexpr int NSTG = 5;                   // smem ring depth (K-steps of 32)
+constexpr int NSTG = 5;                   // weight-digit ring depth (K-steps of 32)
+constexpr int NSTGB = 7;                  // grid-digit (TMA) ring depth: hides the L2 latency
 constexpr int A_DIGIT = IM * 16;          // one K-chunk of one weight digit (2048 B)
 constexpr int A_CHUNK = ND * A_DIGIT;
 constexpr int A_STAGE = 2 * A_CHUNK;
@@ -74,8 +75,8 @@ static_assert(CHUNKS == 3, "K-chunk bookkeeping assumes 48-cell slabs");
 
 struct I8Smem {
     uint8_t a[NSTG][A_STAGE];     // weight digits, [chunk][digit][node][16 cells]
-    uint8_t b[NSTG][B_STAGE];     // grid digits,   [chunk][digit][b][re|im][16 cells]
-    uint64_t fullA[NSTG], fullB[NSTG], empty[NSTG];
+    uint8_t b[NSTGB][B_STAGE];    // grid digits,   [chunk][digit][b][re|im][16 cells]
+    uint64_t fullA[NSTG], empty[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
     uint32_t tbase;
 };
@@ -171,8 +172,11 @@ __global__ void __launch_bounds__(IT, 1)
     if (tid == 0) {
         for (int s = 0; s < NSTG; ++s) {
             mbar_init(&S.fullA[s], 8);   // 2 chunks x 4 warps per K-step
-            mbar_init(&S.fullB[s], 1);
             mbar_init(&S.empty[s], 1);
+        }
+        for (int s = 0; s < NSTGB; ++s) {
+            mbar_init(&S.fullB[s], 1);
+            mbar_init(&S.emptyB[s], 1);
         }
         mbar_init(&S.tfull, 1);
         mbar_init(&S.tempty, NEW);
@@ -194,14 +198,14 @@ __global__ void __launch_bounds__(IT, 1)
                 const int ns = (int)tile_steps(t);
                 const int cb = kstart2(t, wp), bb = t.o1 + wp.pad;   // TMA rows are (b, re|im) pairs
                 for (int s = 0; s < ns; ++s, ++g) {
-                    const int stg = (int)(g % NSTG);
-                    const uint32_t use = g / NSTG;
-                    if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 1);
+                    const int stg = (int)(g % NSTGB);
+                    const uint32_t use = g / NSTGB;
+                    if (use) mbar_wait(&S.emptyB[stg], (use - 1) & 1, 1);
                     mbar_expect_tx(&S.fullB[stg], B_STAGE);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int kc = 2 * s + h, al = kc / CHUNKS, cc = kc - CHUNKS * al;
-                        tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, cb + 16 * cc, 2 * bb, 0, wrap1(t.o0 + al, wp.N0),
+                        tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, 4 * bb, 0, (cb >> 4) + cc, wrap1(t.o0 + al, wp.N0),
                                     &S.fullB[stg]);
                     }
                 }
@@ -223,19 +227,18 @@ __global__ void __launch_bounds__(IT, 1)
             long long t1 = clock64();
             pw_e += t1 - t0;
             for (int s = 0; s < ns; ++s, ++g) {
-                const int stg = (int)(g % NSTG);
-                const uint32_t par = (g / NSTG) & 1;
+                const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
                 t0 = clock64();
-                mbar_wait(&S.fullB[stg], par, 3);
+                mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1, 3);
                 t1 = clock64();
-                mbar_wait(&S.fullA[stg], par, 4);
+                mbar_wait(&S.fullA[stg], (g / NSTG) & 1, 4);
                 long long t2 = clock64();
                 pw_b += t1 - t0;
                 pw_a += t2 - t1;
                 umma::fence_after();
                 if (umma::elect_one()) {
                     const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
-                    const uint64_t bd = b0 + (uint64_t)(stg * (B_STAGE >> 4));
+                    const uint64_t bd = b0 + (uint64_t)(stgb * (B_STAGE >> 4));
                     const bool acc = s > 0;
                     {
 #define SGL_I8_OP(P, Q0, NQ, ACC)                                                                              \
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(IT, 1)
 #undef SGL_I8_OP
                     }
                     umma::commit(&S.empty[stg]);
+                    umma::commit(&S.emptyB[stgb]);
                 }
                 __syncwarp();
             }
@@ -447,26 +451,30 @@ __global__ void k_slab_shift(const unsigned long long *__restrict__ mx, int n, i
 }
 
 // Grid -> balanced byte digits: G 2^sG(a) = sum_j d_j 256^j, d_j in [-128, 127],
-// planes [a][j][b][re|im][c] (row pitch P2 bytes, zero beyond N2p).  Thread =
-// 4 consecutive cells of one row.
-__global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int P2, const int *__restrict__ gsh,
+// layout [a][c / 16][j][b][re|im][c % 16] (zero beyond N2p): one K-chunk of one
+// digit for a tile's 40 axis-1 cells is 1280 contiguous bytes, so a TMA box
+// row is 1280 B (6 rows per box) instead of 480 rows of 16 B.  Thread = 4
+// consecutive cells.
+__global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int ncb, const int *__restrict__ gsh,
                              uint8_t *__restrict__ dig) {
-    const int64_t per_row = P2 / 4, rows = (int64_t)wp.N0 * wp.N1p;
-    const int64_t total = rows * per_row;
-    const size_t plane = (size_t)wp.N1p * 2 * P2;   // one digit of one slab
+    const int64_t total = (int64_t)wp.N0 * ncb * wp.N1p * 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / per_row;
-        const int c4 = (int)(i - row * per_row) * 4;
-        const int a = (int)(row / wp.N1p), b = (int)(row - (int64_t)a * wp.N1p);
+        const int c4 = (int)(i & 3);
+        int64_t r = i >> 2;
+        const int b = (int)(r % wp.N1p);
+        r /= wp.N1p;
+        const int cb = (int)(r % ncb);
+        const int a = (int)(r / ncb);
         const int sh = gsh[a];
         const double sc = sh == NOSLAB ? 0.0 : ldexp(1.0, sh);
+        const double2 *row = g + ((size_t)a * wp.N1p + b) * wp.N2p;
         uint32_t w[ND][2] = {};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const int c = c4 + e;
+            const int c = cb * 16 + c4 * 4 + e;
             double2 v = make_double2(0.0, 0.0);
-            if (c < wp.N2p) v = g[(size_t)row * wp.N2p + c];
+            if (c < wp.N2p) v = row[c];
 #pragma unroll
             for (int ri = 0; ri < 2; ++ri) {
                 const double y = fma(ri ? v.y : v.x, sc, MAGIC);
@@ -479,11 +487,11 @@ __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int
                 }
             }
         }
-        uint8_t *base = dig + (size_t)a * ND * plane + (size_t)b * 2 * P2 + c4;
+        uint8_t *base = dig + (((size_t)a * ncb + cb) * ND * wp.N1p + b) * 32 + c4 * 4;
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
-            *reinterpret_cast<uint32_t *>(base + j * plane) = w[j][0];
-            *reinterpret_cast<uint32_t *>(base + j * plane + P2) = w[j][1];
+            *reinterpret_cast<uint32_t *>(base + (size_t)j * wp.N1p * 32) = w[j][0];
+            *reinterpret_cast<uint32_t *>(base + (size_t)j * wp.N1p * 32 + 16) = w[j][1];
         }
     }
 }
@@ -513,8 +521,8 @@ int setup_i8(Plan &p) {
             }
         }
     }
-    p.P2 = (w.N2p + 15) / 16 * 16;
-    const size_t bytes = (size_t)w.N0 * ND * w.N1p * 2 * p.P2;
+    p.P2 = (w.N2p + 15) / 16;   // 16-cell column blocks per row
+    const size_t bytes = (size_t)w.N0 * p.P2 * ND * w.N1p * 32;
     // per slab: max bits (N0 x u64), shift (N0 x int); per tile: shift (n_itiles x int)
     if (cudaMalloc(&p.digits, bytes) != cudaSuccess ||
         cudaMalloc(&p.gmax, (sizeof(unsigned long long) + sizeof(int)) * w.N0 + sizeof(int) * (p.n_itiles + 1)) !=
@@ -536,12 +544,13 @@ int setup_i8(Plan &p) {
         set_error("cuTensorMapEncodeTiled is unavailable");
         return SGL_ECUDA;
     }
-    // dims (innermost first): c, row = (b, re|im), digit, a
-    cuuint64_t dims[4] = {(cuuint64_t)p.P2, (cuuint64_t)2 * w.N1p, (cuuint64_t)ND, (cuuint64_t)w.N0};
-    cuuint64_t strides[3] = {(cuuint64_t)p.P2, (cuuint64_t)2 * p.P2 * w.N1p, (cuuint64_t)ND * 2 * p.P2 * w.N1p};
-    cuuint32_t box[4] = {16, (cuuint32_t)(2 * kI8Box1), (cuuint32_t)ND, 1};
+    // 8-byte elements; dims (innermost first): (b, re|im, c % 16), digit, c / 16, a
+    cuuint64_t dims[4] = {(cuuint64_t)4 * w.N1p, (cuuint64_t)ND, (cuuint64_t)p.P2, (cuuint64_t)w.N0};
+    cuuint64_t strides[3] = {(cuuint64_t)32 * w.N1p, (cuuint64_t)ND * 32 * w.N1p,
+                             (cuuint64_t)p.P2 * ND * 32 * w.N1p};
+    cuuint32_t box[4] = {(cuuint32_t)(ROWS * 2), (cuuint32_t)ND, 1, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(&p.dmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, p.digits, dims, strides, box, estr,
+    CUresult r = encode(&p.dmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, p.digits, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -563,7 +572,7 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     SGL_CUDA_CHECK(cudaGetLastError());
     k_slab_shift<<<(p.wp.N0 + 255) / 256, 256, 0, st>>>(mx, p.wp.N0, gsh);
     SGL_CUDA_CHECK(cudaGetLastError());
-    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.digits);
+    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.digits);   // P2 = column blocks
     SGL_CUDA_CHECK(cudaGetLastError());
     int *tsh = gsh + p.wp.N0;
     k_tile_shift<<<(unsigned)((p.n_itiles + 255) / 256), 256, 0, st>>>(p.itiles, p.n_itiles, p.wp, gsh, tsh);

@@ -149,8 +149,8 @@ struct Plan {
     NodeSet inodes;
     Tile *itiles = nullptr;
     int64_t n_itiles = 0;
-    uint8_t *digits = nullptr;     // N0 x 6 x N1p x 2 x P2 signed bytes
-    int P2 = 0;                    // byte pitch of a digit row (>= N2p, multiple of 16)
+    uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
+    int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
     alignas(64) CUtensorMap dmap;  // TMA descriptor of the digit planes
 
