@@ -61,8 +61,11 @@ enum {
     SGL_FLAG_EXACT_LAST_STAGE = 1u << 1,  /* exact_last_stage=True: direct NDFT      */
     SGL_FLAG_GENERIC_GRIDDING = 1u << 2,  /* force the per-node window kernels      */
     SGL_FLAG_PROFILE = 1u << 3,           /* record per-stage CUDA-event timings    */
-    SGL_FLAG_PRECISE = 1u << 4            /* basal tables in 80-bit extended precision
+    SGL_FLAG_PRECISE = 1u << 4,           /* basal tables in 80-bit extended precision
                                              (precise=True, recurrences.py:13)      */
+    SGL_FLAG_FP64_WINDOW = 1u << 5        /* forward window stage on the FP64 DMMA
+                                             kernel instead of the int8 tensor-core
+                                             (digit-split) gather                   */
 };
 
 typedef struct {
@@ -83,6 +86,9 @@ typedef struct {
     int32_t generic;          /* 1 if the per-node window kernels are used     */
     int32_t exact;            /* 1 for exact_last_stage plans (direct NDFT)    */
     double plan_ms;           /* device time of plan construction              */
+    int32_t i8_gather;        /* 1 if the forward window stage runs on the int8
+                                 tensor cores (tcgen05, FP64 by digit split)   */
+    int64_t i8_tiles;         /* its 128-node tiles                            */
 } sgl_plan_info;
 
 /* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */

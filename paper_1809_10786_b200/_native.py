@@ -18,6 +18,7 @@ FLAG_EXACT_LAST_STAGE = 1 << 1
 FLAG_GENERIC_GRIDDING = 1 << 2
 FLAG_PROFILE = 1 << 3
 FLAG_PRECISE = 1 << 4
+FLAG_FP64_WINDOW = 1 << 5
 STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares
@@ -47,6 +48,8 @@ class PlanInfo(ctypes.Structure):
         ("generic", ctypes.c_int32),
         ("exact", ctypes.c_int32),
         ("plan_ms", ctypes.c_double),
+        ("i8_gather", ctypes.c_int32),
+        ("i8_tiles", ctypes.c_int64),
     ]
 
 

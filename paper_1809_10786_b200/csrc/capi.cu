@@ -305,8 +305,9 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->exact = exact;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
     {
-        const char *ge = getenv("SGL_GATHER");   // "i8": int8 tensor-core gather (experimental)
-        p->i8 = !p->generic && ge && !strcmp(ge, "i8");
+        // int8 tensor-core gather unless FP64 is asked for (flag, or SGL_GATHER=fp64 for experiments)
+        const char *ge = getenv("SGL_GATHER");
+        p->i8 = !p->generic && !(flags & SGL_FLAG_FP64_WINDOW) && !(ge && !strcmp(ge, "fp64"));
     }
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
@@ -610,6 +611,8 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->generic = p.generic ? 1 : 0;
     info->exact = p.exact ? 1 : 0;
     info->plan_ms = p.plan_ms;
+    info->i8_gather = p.i8 ? 1 : 0;
+    info->i8_tiles = p.n_itiles;
     return SGL_OK;
 }
 

@@ -102,7 +102,8 @@ class SglPlan:
     def stats(self) -> dict:
         i = self._info
         return {"n_tiles": int(i.n_tiles), "tile_nodes": int(i.tile_nodes), "tile_dmma": int(i.tile_dmma),
-                "generic": bool(i.generic), "plan_ms": float(i.plan_ms)}
+                "generic": bool(i.generic), "plan_ms": float(i.plan_ms), "i8_gather": bool(i.i8_gather),
+                "i8_tiles": int(i.i8_tiles)}
 
     def stage_ms(self, direction: str = "forward") -> dict:
         """Per-stage device ms of the last call (plan(..., profile=True))."""
@@ -137,8 +138,10 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
          precise_tables: bool = False) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
-    ``backend``: "auto" (tiled DMMA kernels for q <= 16, per-node kernels
-    otherwise), "tiled", "generic" (per-node kernels).  The reference names
+    ``backend``: "auto" (q <= 16: the int8 tensor-core gather for the
+    forward window stage (FP64 results by digit split) and the tiled FP64 DMMA
+    scatter; per-node kernels otherwise), "tiled" (FP64 DMMA kernels in both
+    directions), "generic" (per-node kernels).  The reference names
     "numba" / "numpy" are accepted as aliases of "auto".  ``precompute`` is
     accepted for compatibility: window weights are always evaluated on the
     fly on the device.  ``exact_last_stage=True`` replaces the window
@@ -183,6 +186,8 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_COMPACT_K1
     if backend == "generic":
         flags |= _native.FLAG_GENERIC_GRIDDING
+    if backend == "tiled":
+        flags |= _native.FLAG_FP64_WINDOW
     if profile:
         flags |= _native.FLAG_PROFILE
     if precise_tables:
@@ -195,7 +200,7 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     _native.check(L.sgl_plan_get_info(h, ctypes.byref(info)))
     nf = None if exact_last_stage else NfftInfo(
         3, tuple(info.n_axis), tuple(info.sigma_axes), int(q), tuple(info.grid), tuple(info.sigma_eff),
-        tuple(info.lam), "generic" if info.generic else "tiled")
+        tuple(info.lam), "generic" if info.generic else ("i8" if info.i8_gather else "tiled"))
     return SglPlan(B=int(B), rho=float(info.rho), sigma=int(sigma), q=None if exact_last_stage else int(q),
                    exact=bool(exact_last_stage),
                    compact_k1=bool(compact_k1), points=points, n_axis=tuple(info.n_axis), nfft=nf,

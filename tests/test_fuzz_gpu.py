@@ -47,7 +47,9 @@ def test_random_plan_matches_oracle(seed):
     v = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
     op = o.oracle_plan(B, pts, sigma=sigma, q=q, rho=rho, compact_k1=compact)
     f_ref, a_ref = o.oracle_forward(op, c), o.oracle_adjoint(op, v)
-    for backend in ("auto", "generic"):
+    for backend in ("auto", "tiled", "generic"):
+        if backend == "tiled" and q > 16:
+            continue
         p = sgl.plan(B, pts, sigma=sigma, q=q, rho=rho, compact_k1=compact, backend=backend)
         assert p.nfft.grid_shape == tuple(op.grid)
         assert rel(sgl.forward(p, c), f_ref) <= 1e-10, (backend, B, sigma, q, compact)
@@ -83,7 +85,9 @@ def test_grid_line_edge_taps(seed):
     B, sigma, q, compact, pts, c, v = _soak_case(seed)
     op = o.oracle_plan(B, pts, sigma=sigma, q=q, compact_k1=compact)
     f_ref, a_ref = o.oracle_forward(op, c), o.oracle_adjoint(op, v)
-    for backend in ("auto", "generic"):
+    for backend in ("auto", "tiled", "generic"):
         p = sgl.plan(B, pts, sigma=sigma, q=q, compact_k1=compact, backend=backend)
-        assert rel(sgl.forward(p, c), f_ref) <= 1e-12, backend
+        # the int8 gather (digit split, ~1e-13) is held to 1e-11, the FP64 kernels to 1e-12
+        tol_f = 1e-11 if p.stats["i8_gather"] else 1e-12
+        assert rel(sgl.forward(p, c), f_ref) <= tol_f, backend
         assert rel(sgl.adjoint(p, v), a_ref) <= 1e-12, backend

@@ -1,0 +1,90 @@
+"""The int8 tensor-core gather (csrc/gather_i8.cu): FP64 window sums
+reproduced from byte digits of the weights and the grid on tcgen05.mma
+kind::i8.  Checked against the FP64 DMMA gather, the oracle and the
+reference goldens; dynamic range, zero input and plan selection."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+TOL_I8 = 1e-11   # measured 5e-14 .. 5e-13 on the goldens (FP64 kernels: 1e-15 .. 1e-13)
+
+
+def rel(x, ref):
+    return float(np.max(np.abs(np.asarray(x) - ref)) / np.max(np.abs(ref)))
+
+
+@pytest.fixture(scope="module")
+def sgl():
+    import paper_1809_10786_b200 as m
+    return m
+
+
+def test_default_plan_selects_int8_gather(sgl):
+    rng = np.random.default_rng(3)
+    pts = sgl.gen_points_ball(2000, 3.0, rng)
+    assert sgl.plan(16, pts).stats["i8_gather"]
+    assert sgl.plan(16, pts).nfft.backend == "i8"
+    assert not sgl.plan(16, pts, backend="tiled").stats["i8_gather"]
+    assert not sgl.plan(16, pts, backend="generic").stats["i8_gather"]
+    assert not sgl.plan(16, pts, q=20).stats["i8_gather"]   # q > 16: per-node kernels
+    assert sgl.plan(16, pts).stats["i8_tiles"] > 0
+
+
+@pytest.mark.parametrize("name", ["b8_q16", "b12_q12", "cfg1", "cfg3_sub600", "cfg5_sub400", "edges_b8_q16",
+                                  "edges_b4_q5"])
+def test_int8_gather_matches_fp64_and_reference(sgl, name):
+    g = load_golden(name)
+    kw = dict(q=int(g["q"]), rho=float(g["rho"]), compact_k1=bool(g["compact"]))
+    p8 = sgl.plan(int(g["B"]), g["points"], **kw)
+    p64 = sgl.plan(int(g["B"]), g["points"], backend="tiled", **kw)
+    c = g["coeffs"] if g["coeffs"].ndim == 1 else g["coeffs"][0]
+    fref = g["fwd"] if g["fwd"].ndim == 1 else g["fwd"][0]
+    f8, f64 = sgl.forward(p8, c), sgl.forward(p64, c)
+    assert rel(f8, f64) <= TOL_I8, rel(f8, f64)
+    assert rel(f8, fref) <= TOL_I8, rel(f8, fref)
+
+
+@pytest.mark.parametrize("scale", [1e-250, 1e-30, 1.0, 1e30, 1e250])
+def test_dynamic_range(sgl, scale):
+    # per-slab grid scales: the digit split is scale-free over the FP64 range
+    rng = np.random.default_rng(9)
+    pts = sgl.gen_points_ball(3000, 4.0, rng)
+    c = sgl.gen_coeffs(16, rng) * scale
+    p8, p64 = sgl.plan(16, pts), sgl.plan(16, pts, backend="tiled")
+    f8, f64 = sgl.forward(p8, c), sgl.forward(p64, c)
+    assert np.all(np.isfinite(f8))
+    assert rel(f8, f64) <= TOL_I8
+
+
+def test_zero_and_sparse_input(sgl):
+    rng = np.random.default_rng(10)
+    pts = sgl.gen_points_ball(1000, 3.0, rng)
+    p = sgl.plan(12, pts)
+    assert np.all(sgl.forward(p, np.zeros(p.count, complex)) == 0)
+    c = np.zeros(p.count, complex)
+    c[5] = 1.0
+    p64 = sgl.plan(12, pts, backend="tiled")
+    assert rel(sgl.forward(p, c), sgl.forward(p64, c)) <= TOL_I8
+
+
+@pytest.mark.parametrize("cfg,M", [(3, 200_000), (5, 100_000), (2, None)])
+def test_config_shapes_against_fp64(sgl, cfg, M):
+    from paper_1809_10786_b200 import workloads
+    w = workloads.config(cfg, M=M)
+    c = w.coeffs if w.coeffs.ndim == 1 else w.coeffs[0]
+    p8 = sgl.plan(w.B, w.points, rho=w.rho)
+    p64 = sgl.plan(w.B, w.points, rho=w.rho, backend="tiled")
+    assert p8.stats["i8_gather"]
+    assert rel(sgl.forward(p8, c), sgl.forward(p64, c)) <= TOL_I8
+
+
+def test_batched_and_repeated_calls(sgl):
+    rng = np.random.default_rng(11)
+    pts = sgl.gen_points_ball(5000, 3.0, rng)
+    p = sgl.plan(10, pts)
+    C = np.stack([sgl.gen_coeffs(10, rng) for _ in range(3)])
+    F = sgl.forward(p, C)
+    for k in range(3):
+        assert np.array_equal(F[k], sgl.forward(p, C[k]))   # deterministic: no atomics in the gather
