@@ -34,6 +34,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.1   # measured: DMMA m8n8k4 loop, profiles/fp64_peak_r01.txt (MEASURED_PEAKS.json has no FP64 entry)
+INT8_PEAK_TOPS = 4550.0   # measured: tcgen05.mma kind::i8 M=128 N=256 loop, profiles/i8_mma_rate_r01.txt
+# int8 gather: per K-step 21 digit pairs x (M = 128 nodes) x (N = 80 (b, re|im)) x (K = 32) MACs
+I8_OPS_PER_KSTEP = 2.0 * 21 * 128 * 80 * 32
 
 
 def parse():
@@ -350,32 +353,51 @@ def main():
                "h2d_bytes_per_step": int(c_h.nbytes * fw_io + v_h.nbytes * ad_io),
                "d2h_bytes_per_step": int(fo.nbytes * fw_io + ao.nbytes * ad_io), "ms_per_step": e_ms}
 
-    # roofline of the dominant kernel (FP64 tensor pipe; algorithmic FLOPs)
+    # roofline of the dominant kernel (algorithmic FP64 FLOPs at the FP64 peak).
+    # The forward window stage runs on the int8 tensor cores when the plan
+    # selected it: its algorithmic FP64-equivalent rate is reported beside the
+    # executed int8 rate against the measured int8 peak.
     q = 16
     flop_per_node = 4.0 * (2 * q) ** 3     # 2 real FMAs per nonzero tap, (2q)^3 taps
+    i8 = bool(stats.get("i8_gather"))
     kern = {}
     if direction in ("both", "fwd"):
-        kern["gather"] = {"ms": stages_fwd["window"] / K, "flop": w.M * flop_per_node}
+        kern["gather"] = {"ms": stages_fwd["window"] / K, "flop": w.M * flop_per_node,
+                          "engine": "int8 tensor cores (tcgen05.mma kind::i8, FP64 by 6x6 digit split)" if i8
+                          else "FP64 DMMA (mma.sync m8n8k4)"}
     if direction in ("both", "adj"):
-        kern["scatter"] = {"ms": stages_adj["window"], "flop": w.M * flop_per_node}
+        kern["scatter"] = {"ms": stages_adj["window"], "flop": w.M * flop_per_node, "engine": "FP64 DMMA (mma.sync m8n8k4)"}
     for k in kern.values():
         k["tflops"] = k["flop"] / (k["ms"] * 1e-3) / 1e12
         k["frac"] = k["tflops"] / FP64_PEAK_TFLOPS
+    if "gather" in kern and i8:
+        g = kern["gather"]
+        g["int8_tops"] = stats["i8_ksteps"] * I8_OPS_PER_KSTEP / (g["ms"] * 1e-3) / 1e12
+        g["int8_frac"] = g["int8_tops"] / INT8_PEAK_TOPS
+        g["int8_ops_per_launch"] = stats["i8_ksteps"] * I8_OPS_PER_KSTEP
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     try:
         if args.config == 3 and w.M == 10_000_000:   # the configuration the ncu capture was taken on
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(dom)
+                traffic = json.load(f).get(dom + ("_i8" if dom == "gather" and i8 else ""))
     except Exception:
         pass
-    roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": FP64_PEAK_TFLOPS,
-            "unit": "TFLOP/s", "frac": kern[dom]["frac"], "traffic": traffic,
-            "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
-            "algorithmic": f"{flop_per_node:.0f} FLOP/node x {w.M} nodes per launch"}
+    if dom == "gather" and i8:
+        roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["int8_tops"], "peak": INT8_PEAK_TOPS,
+                "unit": "TOP/s (int8)", "frac": kern[dom]["int8_frac"], "traffic": traffic,
+                "peak_source": "measured tcgen05 kind::i8 peak (profiles/i8_mma_rate_r01.txt)",
+                "algorithmic": f"{I8_OPS_PER_KSTEP:.0f} int8 ops per K-step x {stats['i8_ksteps']} K-steps per launch"}
+    else:
+        roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": kern[dom]["frac"], "traffic": traffic,
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 figure",
+                "algorithmic": f"{flop_per_node:.0f} FLOP/node x {w.M} nodes per launch"}
 
-    # whole-step roofline: window FLOPs at the FP64 peak + the
-    # FFTs at the HBM copy bandwidth (3 passes x read+write x 16 B per cell)
+    # whole-step roofline: each window stage at its engine's
+    # peak (FP64 FLOPs at the FP64 peak, or the int8 gather's executed ops at
+    # the int8 peak) + the FFTs at the HBM copy bandwidth (3 passes x
+    # read+write x 16 B per cell)
     hbm_gbs = 6534.1
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -384,10 +406,13 @@ def main():
         pass
     n_fwd, n_adj = (K if direction in ("both", "fwd") else 0), (1 if direction in ("both", "adj") else 0)
     cells = float(np.prod(p.nfft.grid_shape)) if p.nfft else 0.0
-    t_win = (n_fwd + n_adj) * w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    t_gat = (stats["i8_ksteps"] * I8_OPS_PER_KSTEP / (INT8_PEAK_TOPS * 1e12) if i8 else
+             w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
+    t_win = n_fwd * t_gat + n_adj * w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12) * 1e3
     t_fft = (n_fwd + n_adj) * 3 * 2 * 16.0 * cells / (hbm_gbs * 1e9) * 1e3
     step_roof = {"t_roof_ms": t_win + t_fft, "window_ms": t_win, "fft_ms": t_fft, "frac": (t_win + t_fft) / ms,
-                 "model": "window FLOPs / 37.1 TF/s (FP64 DMMA peak) + 3-pass FFT bytes / HBM copy GB/s "
+                 "model": ("gather: executed int8 ops / 4550 TOP/s (tcgen05 int8 peak); " if i8 else "") +
+                          "FP64 window FLOPs / 37.1 TF/s (FP64 DMMA peak) + 3-pass FFT bytes / HBM copy GB/s "
                           "(MEASURED_PEAKS.json); basal and halo work not counted"}
 
     cpu = None
@@ -415,10 +440,13 @@ def main():
                        "l2": l2_note,
                        "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": args.steps * (4 * K * (direction != "adj") + 4 * (direction != "fwd")),
-            "gpu_launches_note": "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled; per adjoint: "
-                                 "scatter_tiled, halo_fold, sph_adj, radial_adj (+ cuFFT and memsets, library calls)",
-            "kernels": {k: {"ms": v["ms"], "tflops": v["tflops"], "frac": v["frac"]} for k, v in kern.items()},
+            "gpu_launches": args.steps * ((8 if i8 else 4) * K * (direction != "adj") + 4 * (direction != "fwd")),
+            "gpu_launches_note": ("per forward vector: radial_fwd, sph_fwd, halo_fill, slab_absmax, slab_shift, "
+                                  "slice_grid, tile_shift, gather_i8" if i8 else
+                                  "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled") +
+                                 "; per adjoint: scatter_tiled, halo_fold, sph_adj, radial_adj (+ cuFFT and memsets, "
+                                 "library calls)",
+            "kernels": {k: {kk: vv for kk, vv in v.items() if kk != "flop"} for k, v in kern.items()},
             "stages_ms": {"forward": stages_fwd, "adjoint": stages_adj},
             "plan": {"seconds": plan_s, **stats},
         }

@@ -89,6 +89,8 @@ typedef struct {
     int32_t i8_gather;        /* 1 if the forward window stage runs on the int8
                                  tensor cores (tcgen05, FP64 by digit split)   */
     int64_t i8_tiles;         /* its 128-node tiles                            */
+    int64_t i8_ksteps;        /* K-steps of 32 per gather pass (9 MMAs each,
+                                 M = 128, N = 1680 digit columns in total)     */
 } sgl_plan_info;
 
 /* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */

@@ -50,6 +50,7 @@ class PlanInfo(ctypes.Structure):
         ("plan_ms", ctypes.c_double),
         ("i8_gather", ctypes.c_int32),
         ("i8_tiles", ctypes.c_int64),
+        ("i8_ksteps", ctypes.c_int64),
     ]
 
 

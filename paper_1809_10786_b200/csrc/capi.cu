@@ -613,6 +613,7 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->plan_ms = p.plan_ms;
     info->i8_gather = p.i8 ? 1 : 0;
     info->i8_tiles = p.n_itiles;
+    info->i8_ksteps = p.i8_ksteps;
     return SGL_OK;
 }
 

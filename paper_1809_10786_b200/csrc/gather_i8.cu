@@ -512,7 +512,9 @@ int setup_i8(Plan &p) {
     if (p.n_itiles > 0) {
         std::vector<Tile> ht(p.n_itiles);
         SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.itiles, sizeof(Tile) * p.n_itiles, cudaMemcpyDeviceToHost));
+        p.i8_ksteps = 0;
         for (const Tile &t : ht) {
+            p.i8_ksteps += (CHUNKS * t.e0 + 1) / 2;
             const int k0 = kstart2(t, w);
             if (t.o2 + w.pad < k0 || t.o2 + w.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 || t.e0 > kBox0Max ||
                 t.count > kI8Nodes) {

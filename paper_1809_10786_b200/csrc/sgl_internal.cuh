@@ -149,6 +149,7 @@ struct Plan {
     NodeSet inodes;
     Tile *itiles = nullptr;
     int64_t n_itiles = 0;
+    int64_t i8_ksteps = 0;         // K-steps of one gather pass (sum over tiles)
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
     int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
