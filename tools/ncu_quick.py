@@ -2,7 +2,8 @@
 import csv, subprocess, sys, io
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + kf, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, u, v = rows[0], rows[1], rows[-1]
 m = {k: (vv, uu) for k, uu, vv in zip(h, u, v)}
@@ -18,7 +19,8 @@ for k in h:
         try:
             if float(m[k][0]) > 0.1: print(f"  stall {k[34:-23]:30s} {m[k][0]}")
         except ValueError: pass
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kf, capture_output=True,
+                     text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hi = [i for i, r in enumerate(rows[:5]) if "Source" in r][0]
 hdr = rows[hi]; isrc = hdr.index("Source"); ia = hdr.index("Address"); ws = hdr.index("Warp Stall Sampling (All Samples)")
