@@ -80,6 +80,58 @@ __global__ void k_check(const int8_t *A, const int8_t *B, int32_t *D, int K, int
     if (warp == 0) umma::tmem_free(td, 256);
 }
 
+// MN-major (no swizzle) operands: element (mn, k) at (mn / 16) * SBO + (k / 8) * LBO + (k % 8) * 16 + mn % 16
+__global__ void k_check_mn(const int8_t *A, const int8_t *B, int32_t *D, int K, int N) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t *sA = sm;
+    uint8_t *sB = sm + 128 * K;
+    // A: SBO = 128 B (next 16 rows), LBO = 16 * 128 = 2048 B (next 8 K)
+    const uint32_t sboA = 128, lboA = 128 / 16 * 128, sboB = 128, lboB = N / 16 * 128;
+    for (int i = tid; i < 128 * K; i += blockDim.x) {
+        int r = i / K, k = i % K;
+        sA[(r / 16) * sboA + (k / 8) * lboA + (k % 8) * 16 + r % 16] = (uint8_t)A[i];
+    }
+    for (int i = tid; i < N * K; i += blockDim.x) {
+        int r = i / K, k = i % K;
+        sB[(r / 16) * sboB + (k / 8) * lboB + (k % 8) * 16 + r % 16] = (uint8_t)B[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) umma::tmem_alloc(&tbase, 256);
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t td = tbase;
+    if (tid == 0) {
+        const uint32_t id = umma::idesc_i8(128, N, true, true) | (1u << 15) | (1u << 16);   // A, B MN-major
+        for (int kb = 0; kb < K / 32; ++kb) {
+            uint64_t da = umma::desc_kmajor(umma::smem_addr(sA) + kb * 4 * lboA, lboA, sboA);
+            uint64_t db = umma::desc_kmajor(umma::smem_addr(sB) + kb * 4 * lboB, lboB, sboB);
+            umma::mma_i8(td, da, db, id, kb > 0);
+        }
+        umma::commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    umma::fence_after();
+    for (int c = 0; c < N; c += 16) {
+        int32_t v[16];
+        umma::tmem_ld16(td + ((uint32_t)(warp * 32) << 16) + c, v);
+        umma::tmem_ld_wait();
+        for (int j = 0; j < 16; ++j)
+            if (c + j < N) D[(warp * 32 + lane) * N + c + j] = v[j];
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(td, 256);
+}
+
 // throughput: each CTA issues iters x (K/32) MMAs on its resident operands
 __global__ void k_rate(int K, int N, int iters, int32_t *sink) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -220,6 +272,36 @@ int main() {
                 cudaFree(dB);
                 cudaFree(dD);
             }
+    }
+    for (int N : {80, 160, 240}) {
+        const int KK = 128;
+        std::vector<int8_t> A(128 * KK), B(N * KK);
+        std::vector<int32_t> D(128 * N), R(128 * N);
+        srand(7 + N);
+        for (auto &x : A) x = (int8_t)(rand() & 255);
+        for (auto &x : B) x = (int8_t)(rand() & 255);
+        for (int m = 0; m < 128; ++m)
+            for (int n = 0; n < N; ++n) {
+                long sacc = 0;
+                for (int k = 0; k < KK; ++k) sacc += (int)A[m * KK + k] * (int)B[n * KK + k];
+                R[m * N + n] = (int32_t)sacc;
+            }
+        int8_t *dA, *dB;
+        int32_t *dD;
+        cudaMalloc(&dA, A.size());
+        cudaMalloc(&dB, B.size());
+        cudaMalloc(&dD, D.size() * 4);
+        cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+        size_t smem = (128 + N) * KK;
+        cudaFuncSetAttribute(k_check_mn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_check_mn<<<1, 128, smem>>>(dA, dB, dD, KK, N);
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+        int nbad = 0;
+        for (int i = 0; i < 128 * N; ++i) nbad += D[i] != R[i];
+        printf("check MN-major N=%d: %s, %d mismatches (D[0]=%d ref %d)\n", N, cudaGetErrorString(e), nbad, D[0], R[0]);
+        bad += nbad != 0 || e != cudaSuccess;
     }
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
