@@ -50,7 +50,7 @@ void free_plan(Plan *p) {
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
-                    p->itiles, p->digits, p->gmax};
+                    p->itiles, p->digits, p->gmax, p->istiles, p->tsv};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
@@ -207,7 +207,7 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
         if (rc) return rc;
     } else {
         SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-        rc = launch_scatter(p, v, p.grid_buf, st);
+        rc = p.i8s ? launch_scatter_i8(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
         if (rc) return rc;
         mark(SGL_STAGE_FFT);
         rc = launch_halo_fold(p, p.grid_buf, st);
@@ -308,6 +308,8 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         // int8 tensor-core gather unless FP64 is asked for (flag, or SGL_GATHER=fp64 for experiments)
         const char *ge = getenv("SGL_GATHER");
         p->i8 = !p->generic && !(flags & SGL_FLAG_FP64_WINDOW) && !(ge && !strcmp(ge, "fp64"));
+        const char *se = getenv("SGL_SCATTER");   // "i8": int8 tensor-core scatter (experimental)
+        p->i8s = p->i8 && se && !strcmp(se, "i8");
     }
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
@@ -364,6 +366,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
     if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;   // (not reached: pad widens the plane)
     if (wp.N1p < kI8Box1 || pad != q) p->i8 = false;   // digit TMA box within the plane; aligned K ranges
+    if (!p->i8) p->i8s = false;
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         if (exact) {
@@ -471,6 +474,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     }
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && p->i8) rc = setup_i8(*p);
+    if (rc == SGL_OK && p->i8s) rc = setup_scatter_i8(*p);
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");
         rc = SGL_ECUDA;

@@ -43,16 +43,15 @@
 
 #include "sgl_internal.cuh"
 #include "umma.cuh"
+#include "i8_common.cuh"
 
 namespace sgl {
 namespace {
 
-constexpr int ND = 6;                     // byte digits per operand
-constexpr int DMIN = 5;                   // kept digit diagonals p + q = DMIN .. 2 ND - 2
-constexpr int NBLK = 2 * ND - 1 - DMIN;   // 6 TMEM accumulators
+using namespace i8;
+
 constexpr int IM = kI8Nodes;              // MMA M (nodes)
 constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
-constexpr int CHUNKS = kI8Box2 / 16;      // 16-cell K-chunks per slab
 constexpr int NSTG = 5;                   // weight-digit ring depth (K-steps of 32)
 constexpr int NSTGB = 7;                  // grid-digit (TMA) ring depth: hides the L2 latency
 constexpr int A_DIGIT = IM * 16;          // one K-chunk of one weight digit (2048 B)
@@ -64,12 +63,6 @@ constexpr int B_STAGE = 2 * B_CHUNK;
 constexpr int NGW = 12;                   // generator warps (3 chunk columns x 128 nodes)
 constexpr int NEW = 4;                    // epilogue warps
 constexpr int IT = (2 + NGW + NEW) * 32;
-constexpr uint32_t TCOLS = 512;
-constexpr double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, y, MAGIC) rounds x y to an integer
-// + 128 in each of the 6 digit bytes: the bytes of fma(x, y, MAGIC_BAL) are
-// the balanced digits of rint(x y) (< 2^46) offset by 128 (undone by ^ 0x80)
-constexpr double MAGIC_BAL = 6755399441055744.0 + 141289400074368.0;
-constexpr int NOSLAB = 4096;   // shift of an all-zero slab (never the tile minimum)
 static_assert(NBLK * ROWS <= (int)TCOLS, "diagonal accumulators must fit TMEM");
 static_assert(CHUNKS == 3, "K-chunk bookkeeping assumes 48-cell slabs");
 
@@ -85,78 +78,6 @@ struct I8Smem {
 // B digits q0 .. q0+nq-1 (stacked along N) into the diagonal accumulators
 // p+q0-DMIN .. ; 21 digit pairs with p + q >= DMIN in 9 MMAs.
 
-__device__ __forceinline__ int wrapi(int i, int n) {
-    i %= n;
-    return i < 0 ? i + n : i;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(umma::smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(umma::smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(umma::smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, int tag = 0) {
-    uint32_t ok = 0, spins = 0;
-    for (;;) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(umma::smem_addr(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (++spins == (1u << 26)) __trap();   // lost phase: trap instead of hanging the GPU
-    }
-}
-__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
-                                            uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-        "[%6];\n" ::"r"(umma::smem_addr(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(umma::smem_addr(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(s));
-    return r;
-}
-
-// digit shift of a slab from its max |G| (bits of a non-negative double):
-// |G| 2^sG < 2^46
-__device__ __forceinline__ int slab_shift(unsigned long long bits) {
-    const double m = __longlong_as_double((long long)bits);
-    if (!(m > 0.0) || !isfinite(m)) return NOSLAB;
-    int ex;
-    frexp(m, &ex);   // m < 2^ex
-    return 46 - ex;
-}
-
-// 2^e for e <= 0 (0 below 2^-1022)
-__device__ __forceinline__ double pow2n(int e) {
-    return e < -1022 ? 0.0 : __longlong_as_double((long long)(e + 1023) << 52);
-}
-
-// slab index modulo N0 for boxes that start at most one period out
-__device__ __forceinline__ int wrap1(int a, int n) {
-    a += a < 0 ? n : 0;
-    return a >= n ? a - n : a;
-}
-
-// First padded axis-2 cell of a slab's K range: the TMA box start of the
-// innermost dimension must be 16-byte aligned (measured: unaligned starts
-// fault with an illegal instruction), so the 48-cell K range starts at the
-// 16-aligned cell at or below the box origin; 16-aligned pencils with
-// pad == q <= 16 keep every window inside it (checked at plan time).
-__host__ __device__ __forceinline__ int kstart2(const Tile &t, const WindowParams &wp) {
-    return (t.o2 + wp.pad) & ~15;
-}
 
 __device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * t.e0 + 1) >> 1; }
 

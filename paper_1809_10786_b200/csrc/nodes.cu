@@ -386,6 +386,16 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         if (rc) return rc;
         rc = reorder_tiles(p.itiles, p.n_itiles, st);
         if (rc) return rc;
+        if (p.i8s) {
+            // int8 scatter: same order, 512-node tiles (fewer grid REDs per node)
+            TileGeom sg = ig;
+            sg.max_nodes = kI8SNodes;
+            rc = order_and_tile(p, a0.p, a1.p, a2.p, kI8Box1 - 32, kI8Box2 - 32, sg, p.inodes, &p.istiles,
+                                &p.n_istiles, true, st, true);
+            if (rc) return rc;
+            rc = reorder_tiles(p.istiles, p.n_istiles, st);
+            if (rc) return rc;
+        }
     }
     // Scatter order: with dense nodes, W x W2 pencils whose axis-2 box is a
     // multiple of 8 (exact 8-column DMMA tiles, ~17 % fewer DMMAs; warps own

@@ -1,0 +1,358 @@
+// Gaussian-window scatter (adjoint NFFT spreading, _gridding.py:77-95) on the
+// int8 tensor cores (tcgen05.mma kind::i8) with FP64 results by the same
+// exact byte-digit split as the gather (gather_i8.cu).  sm_100a.
+//
+// Per tile of <= 512 sorted nodes (one 8 x 16 pencil, consecutive in lo0) and
+// its box of e0 x 40 x 48 cells, the spreading sum
+//     G[a,b,c] += sum_n w0[n,a] w1[n,b] w2[n,c] v[n]
+// is a GEMM with K = nodes: per M-block of 128 box cells (a, c),
+//     D[(a,c), (b,re|im)] = sum_n W[(a,c), n] V[n, (b,re|im)],
+//     W = w0 (x) w2 (weights, fixed point at the plan scale sA),
+//     V = w1 v      (fixed point at a per-tile scale from the tile's max |v|),
+// both split into 6 balanced bytes; the 21 digit pairs with p + q >= 5 in 9
+// MMAs per K-step of 32 nodes (W digit p times V digits stacked along N),
+// int32 diagonal accumulators in TMEM (6 x 80 columns).  Operands are built
+// by generator warps straight into the MN-major UMMA layout (16 consecutive
+// cells / columns per 16-byte row, 8 nodes per core matrix).  The epilogue
+// converts an M-block to FP64 into a per-thread staging column, frees TMEM
+// for the next block's MMAs and only then reduces the block into the
+// halo-padded grid with RED.E.ADD.F64 (k_halo_fold folds the halo as for the
+// FP64 scatter).  512-node tiles keep the REDs at ~300 per node.
+//
+// CTA (one per SM, persistent): warp 0 MMA issuer, warps 1-8 weight-digit
+// generators (node x 16-cell group), warps 9-13 value-digit generators (node
+// x 16-column group), warps 14-17 epilogue (TMEM lane quarters = cells).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "i8_common.cuh"
+#include "sgl_internal.cuh"
+#include "umma.cuh"
+
+namespace sgl {
+namespace {
+
+using namespace i8;
+
+constexpr int SN = kI8SNodes;            // nodes per tile (K)
+constexpr int MR = 128;                  // box cells per M-block (MMA M)
+constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
+constexpr int NSTG = 3;                  // operand ring depth (K-steps of 32 nodes)
+constexpr int A_DIGIT = 4 * 8 * 128;     // 4 node blocks x 8 cell blocks x 128 B (MN-major)
+constexpr int A_STAGE = ND * A_DIGIT;
+constexpr int B_KBLK = ND * (ROWS / 16) * 128;   // one 8-node block of all 6 value digits
+constexpr int B_STAGE = 4 * B_KBLK;
+constexpr int NWG = 8, NVG = 5;          // weight / value generator warps
+constexpr int NGEN = NWG + NVG;
+constexpr int NEW = 4;
+constexpr int ST = (1 + NGEN + NEW) * 32;
+static_assert(ROWS % 16 == 0 && NVG * 32 == 32 * ROWS / 16, "value items: 32 nodes x 5 column groups");
+
+struct SSmem {
+    uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
+    uint8_t b[NSTG][B_STAGE];    // value digits  [node/8][digit][col/16][node%8][col%16]
+    double stage[ROWS][MR];      // epilogue: one M-block in FP64, [column][cell]
+    double u0[SN], u1[SN], u2[SN];
+    double2 v[SN];
+    uint64_t full[NSTG], empty[NSTG];
+    uint64_t tfull, tempty;
+    uint32_t tbase;
+};
+
+__device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NGEN * 32) : "memory"); }
+
+__device__ __forceinline__ void red_add(double *addr, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ int mblocks(const Tile &t) { return (t.e0 * CHUNKS * 16 + MR - 1) / MR; }
+__device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + 31) >> 5; }
+
+__global__ void __launch_bounds__(ST, 1)
+    k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
+                 double s2, int sA, const int *__restrict__ tsv, const double2 *__restrict__ values,
+                 double *__restrict__ grid) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    SSmem &S = *reinterpret_cast<SSmem *>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTG; ++s) {
+            mbar_init(&S.full[s], NGEN);
+            mbar_init(&S.empty[s], 1);
+        }
+        mbar_init(&S.tfull, 1);
+        mbar_init(&S.tempty, NEW);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) umma::tmem_alloc(&S.tbase, TCOLS);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tbase = S.tbase;
+
+    if (warp == 0) {
+        // ---- MMA issuer
+        const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), 1024, 128);       // MN-major: LBO = node
+        const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);     // block, SBO = 16 rows
+        constexpr uint32_t MN = (1u << 15) | (1u << 16);                                 // A, B MN-major
+        uint32_t g = 0, mc = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile t = tiles[ti];
+            const int nmb = mblocks(t), nks = ksteps(t);
+            for (int mb = 0; mb < nmb; ++mb, ++mc) {
+                if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
+                umma::fence_after();
+                for (int ks = 0; ks < nks; ++ks, ++g) {
+                    const int stg = (int)(g % NSTG);
+                    mbar_wait(&S.full[stg], (g / NSTG) & 1);
+                    umma::fence_after();
+                    if (umma::elect_one()) {
+                        const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
+                        const uint64_t bd = b0 + (uint64_t)(stg * (B_STAGE >> 4));
+                        const bool acc = ks > 0;
+#define SGL_I8S_OP(P, Q0, NQ, ACC)                                                                         \
+    umma::mma_i8(tbase + (uint32_t)(((P) + (Q0)-DMIN) * ROWS), ad + (uint64_t)((P)*A_DIGIT >> 4),         \
+                 bd + (uint64_t)((Q0) * (ROWS / 16) * 128 >> 4), umma::idesc_i8(MR, (NQ)*ROWS, true, true) | MN, \
+                 ACC)
+                        // the two p = 5 MMAs cover every accumulator and carry the per-block reset
+                        SGL_I8S_OP(5, 0, 3, acc);
+                        SGL_I8S_OP(5, 3, 3, acc);
+                        SGL_I8S_OP(4, 1, 3, true);
+                        SGL_I8S_OP(4, 4, 2, true);
+                        SGL_I8S_OP(3, 2, 3, true);
+                        SGL_I8S_OP(3, 5, 1, true);
+                        SGL_I8S_OP(2, 3, 3, true);
+                        SGL_I8S_OP(1, 4, 2, true);
+                        SGL_I8S_OP(0, 5, 1, true);
+#undef SGL_I8S_OP
+                        umma::commit(&S.empty[stg]);
+                    }
+                    __syncwarp();
+                }
+                if (umma::elect_one()) umma::commit(&S.tfull);
+                __syncwarp();
+            }
+        }
+    } else if (warp <= NGEN) {
+        // ---- operand generators: warps 1-8 weight digits (node, 16-cell group),
+        // warps 9-13 value digits (node, 16-column group = 8 axis-1 cells x re|im)
+        const int gt = tid - 32;
+        const bool wgen = gt < NWG * 32;
+        const int item = wgen ? gt : gt - NWG * 32;
+        const int kl = wgen ? item >> 3 : item / NVG;    // node within the K-step
+        const int grp = wgen ? item & 7 : item % NVG;    // cell group / column group
+        uint32_t g = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile t = tiles[ti];
+            gen_sync();   // the previous tile's readers of the node tables are done
+            for (int i = gt; i < t.count; i += NGEN * 32) {
+                const int64_t si = (int64_t)t.start + i;
+                S.u0[i] = nodes.u0[si];
+                S.u1[i] = nodes.u1[si];
+                S.u2[i] = nodes.u2[si];
+                S.v[i] = values[nodes.perm[si]];
+            }
+            gen_sync();
+            const int nmb = mblocks(t), nks = ksteps(t);
+            const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
+            const int svt = __ldg(tsv + ti);
+            const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);   // value fixed-point scale of the tile
+            for (int mb = 0; mb < nmb; ++mb) {
+                for (int ks = 0; ks < nks; ++ks, ++g) {
+                    const int stg = (int)(g % NSTG);
+                    const uint32_t use = g / NSTG;
+                    const int kn = ks * 32 + kl;
+                    const bool live = kn < t.count;
+                    uint32_t dw[ND][4];
+                    if (wgen) {
+                        const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
+                        double w0 = 0.0;
+                        double w2[16];
+                        const double u0 = live ? S.u0[kn] : -1e9, u2 = live ? S.u2[kn] : -1e9;
+                        int lo0, hi0, lo2, hi2;
+                        window_cells(u0, wp.q, lo0, hi0);
+                        window_cells(u2, wp.q, lo2, hi2);
+                        const int cell0 = t.o0 + al;
+                        if (live && al < t.e0 && cell0 >= lo0 && cell0 <= hi0) {
+                            const double d0 = u0 - (double)cell0;
+                            w0 = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                        }
+                        const int cb = kst + 16 * cc;
+                        const int ef = max(0, lo2 - cb);
+                        const double d = u2 - (double)(cb + ef);
+                        double w = s2 * (wp.c2 * exp(-d * d * wp.h2)), r = exp(wp.h2 * (2.0 * d - 1.0));
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            w2[e] = (e >= ef && cb + e <= hi2) ? w : 0.0;
+                            if (e >= ef) {
+                                w *= r;
+                                r *= wp.r2_1;
+                            }
+                        }
+                        digits16(w0, w2, dw);
+                    } else {
+                        double wv[16];
+                        const double u1 = live ? S.u1[kn] : -1e9;
+                        const double2 vv = live ? S.v[kn] : make_double2(0.0, 0.0);
+                        int lo1, hi1;
+                        window_cells(u1, wp.q, lo1, hi1);
+                        const int bb = t.o1 + grp * 8;
+                        const int bf = max(0, lo1 - bb);
+                        const double d = u1 - (double)(bb + bf);
+                        double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const double w1 = (live && j >= bf && bb + j <= hi1) ? w : 0.0;
+                            if (j >= bf) {
+                                w *= r;
+                                r *= wp.r1_1;
+                            }
+                            wv[2 * j] = w1 * vv.x;
+                            wv[2 * j + 1] = w1 * vv.y;
+                        }
+                        digits16(vsc, wv, dw);
+                    }
+                    if (use) mbar_wait(&S.empty[stg], (use - 1) & 1);
+                    if (wgen) {
+                        uint8_t *dst = S.a[stg] + (kl >> 3) * 1024 + grp * 128 + (kl & 7) * 16;
+#pragma unroll
+                        for (int p = 0; p < ND; ++p)
+                            *reinterpret_cast<uint4 *>(dst + p * A_DIGIT) =
+                                make_uint4(dw[p][0], dw[p][1], dw[p][2], dw[p][3]);
+                    } else {
+                        uint8_t *dst = S.b[stg] + (kl >> 3) * B_KBLK + grp * 128 + (kl & 7) * 16;
+#pragma unroll
+                        for (int q = 0; q < ND; ++q)
+                            *reinterpret_cast<uint4 *>(dst + q * (ROWS / 16) * 128) =
+                                make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
+                    }
+                    umma::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&S.full[stg]);
+                }
+            }
+        }
+    } else {
+        // ---- epilogue: thread = box cell of the M-block = TMEM lane
+        const int quarter = warp & 3, m = quarter * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
+        uint32_t mc = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            const Tile t = tiles[ti];
+            const int nmb = mblocks(t);
+            const int sv = __ldg(tsv + ti);
+            const double unit = sv == NOSLAB ? 0.0 : ldexp(1.0, 8 * DMIN - sA - sv);
+            const int kst = kstart2(t, wp);   // padded axis-2 cell of K column 0
+            const int c_in0 = t.o2 + wp.pad - kst, c_in1 = c_in0 + t.e2;
+            for (int mb = 0; mb < nmb; ++mb, ++mc) {
+                mbar_wait(&S.tfull, mc & 1);
+                umma::fence_after();
+#pragma unroll 1
+                for (int cb = 0; cb < ROWS / 8; ++cb) {
+                    int32_t D[NBLK][8];
+                    __syncwarp();   // tcgen05.ld is .sync.aligned
+#pragma unroll
+                    for (int k = 0; k < NBLK; ++k) umma::tmem_ld8(tl + (uint32_t)(k * ROWS + cb * 8), D[k]);
+                    umma::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        S.stage[cb * 8 + j][m] = combine6(D[0][j], D[1][j], D[2][j], D[3][j], D[4][j], D[5][j], unit);
+                }
+                umma::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
+                const int cell = mb * MR + m, al = cell / (CHUNKS * 16), cl = cell - al * CHUNKS * 16;
+                if (al < t.e0 && cl >= c_in0 && cl < c_in1) {
+                    double *gp = grid + 2 * (((size_t)wrap1(t.o0 + al, wp.N0) * wp.N1p + (t.o1 + wp.pad)) * wp.N2p +
+                                             (kst + cl));
+                    for (int b = 0; b < t.e1; ++b) {
+                        const double re = S.stage[2 * b][m], im = S.stage[2 * b + 1][m];
+                        if (re != 0.0) red_add(gp, re);
+                        if (im != 0.0) red_add(gp + 1, im);
+                        gp += 2 * (size_t)wp.N2p;
+                    }
+                }
+            }
+        }
+    }
+
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        umma::fence_after();
+        umma::tmem_free(tbase, TCOLS);
+    }
+}
+
+// per tile: value scale from the tile's max |Re v|, |Im v| (|w1 v| 2^sV < 2^46, w1 <= c1)
+__global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet nodes,
+                              const double2 *__restrict__ values, double c1, int *__restrict__ tsv) {
+    const int64_t ti = blockIdx.x;
+    if (ti >= n) return;
+    const Tile t = tiles[ti];
+    double m = 0.0;
+    for (int i = threadIdx.x; i < t.count; i += blockDim.x) {
+        const double2 v = values[nodes.perm[(int64_t)t.start + i]];
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ double wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+        m = fmax(m, wm[0]) * c1;
+        int ex;
+        frexp(m, &ex);
+        tsv[ti] = (m > 0.0 && isfinite(m)) ? 46 - ex : NOSLAB;
+    }
+}
+
+}  // namespace
+
+int setup_scatter_i8(Plan &p) {
+    const WindowParams &w = p.wp;
+    if (p.n_istiles > 0) {
+        std::vector<Tile> ht(p.n_istiles);
+        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
+        for (const Tile &t : ht) {
+            const int k0 = kstart2(t, w);
+            if (t.o2 + w.pad < k0 || t.o2 + w.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 || t.e0 > kBox0Max ||
+                t.count > kI8SNodes) {
+                set_error("internal: int8 scatter tile outside its K range");
+                return SGL_ECUDA;
+            }
+        }
+    }
+    if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("out of device memory for the int8 scatter scales");
+        return SGL_ENOMEM;
+    }
+    return SGL_OK;
+}
+
+int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st) {
+    if (p.M == 0 || p.n_istiles == 0) return SGL_OK;
+    k_tile_vscale<<<(unsigned)p.n_istiles, 256, 0, st>>>(p.istiles, p.n_istiles, p.inodes, values, p.wp.c1, p.tsv);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
+    const int sA = 46 - e, a0 = sA / 2;
+    const size_t sm = sizeof(SSmem);
+    SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, num_sms()));
+    k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
+                                                  std::ldexp(1.0, sA - a0), sA, p.tsv, values,
+                                                  reinterpret_cast<double *>(grid));
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+}  // namespace sgl

@@ -32,6 +32,7 @@ constexpr int kMaxQTiled = 16;   // tiled kernels need 2q + W - 1 <= kBoxMax
 constexpr int kI8Nodes = 128;    // tcgen05 M
 constexpr int kI8Box1 = 40;      // axis-1 box (80 re|im rows per digit = MMA N)
 constexpr int kI8Box2 = 48;      // axis-2 box (3 K-chunks of 16 cells per slab)
+constexpr int kI8SNodes = 512;   // int8 scatter tiles (MMA K: more nodes per RED)
 
 struct Tile {
     int32_t start;    // first sorted node
@@ -150,6 +151,10 @@ struct Plan {
     Tile *itiles = nullptr;
     int64_t n_itiles = 0;
     int64_t i8_ksteps = 0;         // K-steps of one gather pass (sum over tiles)
+    bool i8s = false;              // int8 tensor-core scatter (scatter_i8.cu), same node order
+    Tile *istiles = nullptr;       // its 512-node tiles
+    int64_t n_istiles = 0;
+    int *tsv = nullptr;            // per scatter tile: value fixed-point shift
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
     int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
@@ -204,6 +209,8 @@ int launch_direct_adjoint(int B, int64_t M, const double *pts, const double2 *v,
 int launch_halo_fill(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
+int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
+int setup_scatter_i8(Plan &p);
 int setup_i8(Plan &p);
 int num_sms();
 
