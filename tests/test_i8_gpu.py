@@ -88,3 +88,40 @@ def test_batched_and_repeated_calls(sgl):
     F = sgl.forward(p, C)
     for k in range(3):
         assert np.array_equal(F[k], sgl.forward(p, C[k]))   # deterministic: no atomics in the gather
+
+
+# ---- the opt-in int8 scatter (SGL_SCATTER=i8, csrc/scatter_i8.cu)
+def _plan_i8s(sgl, *a, **kw):
+    import os
+    os.environ["SGL_SCATTER"] = "i8"
+    try:
+        return sgl.plan(*a, **kw)
+    finally:
+        os.environ.pop("SGL_SCATTER", None)
+
+
+@pytest.mark.parametrize("name", ["b8_q16", "b12_q12", "cfg1", "cfg2_sub2000", "cfg3_sub600", "edges_b8_q16"])
+def test_int8_scatter_matches_fp64_and_reference(sgl, name):
+    g = load_golden(name)
+    kw = dict(q=int(g["q"]), rho=float(g["rho"]), compact_k1=bool(g["compact"]))
+    p8 = _plan_i8s(sgl, int(g["B"]), g["points"], **kw)
+    p64 = sgl.plan(int(g["B"]), g["points"], backend="tiled", **kw)
+    a8, a64 = sgl.adjoint(p8, g["values"]), sgl.adjoint(p64, g["values"])
+    assert rel(a8, a64) <= TOL_I8, rel(a8, a64)
+    assert rel(a8, g["adj"]) <= TOL_I8, rel(a8, g["adj"])
+
+
+@pytest.mark.parametrize("scale", [1e-200, 1.0, 1e200])
+def test_int8_scatter_dynamic_range_and_pairing(sgl, scale):
+    rng = np.random.default_rng(12)
+    pts = sgl.gen_points_ball(4000, 4.0, rng)
+    v = (rng.uniform(-1, 1, 4000) + 1j * rng.uniform(-1, 1, 4000)) * scale
+    v[::7] *= 1e-9   # per-tile value scale: small values next to large ones
+    p8 = _plan_i8s(sgl, 16, pts)
+    p64 = sgl.plan(16, pts, backend="tiled")
+    a8 = sgl.adjoint(p8, v)
+    assert np.all(np.isfinite(a8)) and rel(a8, sgl.adjoint(p64, v)) <= TOL_I8
+    x = sgl.gen_coeffs(16, rng)
+    fx = sgl.forward(p8, x)
+    nv = np.linalg.norm(v / scale) * scale   # (the plain norm underflows at 1e-200)
+    assert abs(np.vdot(v, fx) - np.vdot(a8, x)) <= 1e-11 * nv * (np.linalg.norm(x) + np.linalg.norm(fx))

@@ -205,16 +205,23 @@ __global__ void k_rate2(int N, int iters, int lay, int32_t *sink) {
             da = umma::desc_kmajor(sa, 16, 1024) | ((uint64_t)2 << 61);
             db = umma::desc_kmajor(sb, 16, 1024) | ((uint64_t)2 << 61);
             kadv_a = kadv_b = 32;
-        } else {
+        } else if (lay == 3) {
             da = umma::desc_kmajor(sa, 16, 256) | ((uint64_t)6 << 61);
             db = umma::desc_kmajor(sb, 16, 256) | ((uint64_t)6 << 61);
             kadv_a = 128 * 32;
             kadv_b = N * 32;
+        } else {
+            // MN-major interleave: SBO = 128 (next 16 MN), LBO = next 8 K
+            da = umma::desc_kmajor(sa, 1024, 128);
+            db = umma::desc_kmajor(sb, N / 16 * 128, 128);
+            kadv_a = 4 * 1024;
+            kadv_b = 4 * (N / 16 * 128);
         }
+        const uint32_t idm = lay == 4 ? (id | (1u << 15) | (1u << 16)) : id;
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb)
-                umma::mma_i8(td + (it & 1) * 256, da + ((kb * kadv_a) >> 4), db + ((kb * kadv_b) >> 4), id, true);
+                umma::mma_i8(td + (it & 1) * 256, da + ((kb * kadv_a) >> 4), db + ((kb * kadv_b) >> 4), idm, true);
         umma::commit(&bar);
     }
     __syncwarp();
@@ -326,7 +333,7 @@ int main() {
             printf("rate M=128 N=%d K/issue-block=%d: %.1f int8 TOPS (%.3f ms) %s\n", N, Kr, ops / ms / 1e9, ms,
                    cudaGetErrorString(cudaGetLastError()));
         }
-    for (int lay = 0; lay < 4; ++lay)
+    for (int lay = 0; lay < 5; lay += (lay == 0 ? 4 : 1))
         for (int N : {80, 160, 240, 256}) {
             cudaFuncSetAttribute(k_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             const int iters = 5000;
