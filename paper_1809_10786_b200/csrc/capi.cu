@@ -576,6 +576,16 @@ int sgl_nfft_plan_create(int32_t d, const int32_t *n_axis_d, int64_t M, const do
     p->profile = flags & SGL_FLAG_PROFILE;
     p->exact = exact;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled || d < 3;
+    {
+        // The int8 gather's digit-split error (~1e-15 of the local grid scale) is
+        // amplified by the deconvolution gain of the spectrum's edge (up to
+        // ~65 per axis at sigma = 2): harmless for SGL spectra (<= 2.5e-12 even
+        // for edge-concentrated coefficients, tools/i8_adversarial.py) but 1.8e-10
+        // for a white raw NFFT spectrum at q = 16.  Raw NFFT plans therefore keep
+        // the FP64 gather unless SGL_GATHER=i8 asks for it.
+        const char *ge = getenv("SGL_GATHER");
+        p->i8 = !p->generic && ge && !strcmp(ge, "i8");
+    }
     p->count = (int64_t)n_axis[0] * n_axis[1] * n_axis[2];
     for (int ax = 0; ax < 3; ++ax) {   // nfft.py:174, 181-182 (no sigma escalation in the NFFT layer)
         const bool dummy = ax < 3 - d;

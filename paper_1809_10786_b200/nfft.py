@@ -87,8 +87,10 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
 
     ``nodes`` (m, d), reduced into [0, 2 pi).  ``sigma``: integer >= 2, or
     one per axis.  ``backend``:
-    "auto" / "tiled" / "generic" (the reference names "numba" / "numpy" are
-    accepted as "auto").  ``precompute`` is accepted; windows are evaluated
+    "auto" / "tiled" (FP64 DMMA kernels for d = 3, q <= 16; the int8 gather
+    of SGL plans is not used here: a white NFFT spectrum amplifies its
+    digit-split error to ~1e-10), "generic" (per-node kernels); the reference
+    names "numba" / "numpy" are accepted as "auto".  ``precompute`` is accepted; windows are evaluated
     on the fly on the device.  ``exact=True`` plans the direct NDFT."""
     _check_d(d)
     n_axis = _as_axes(n_axis, d, "n_axis")
@@ -130,7 +132,8 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
     _native.check(_native.lib().sgl_plan_get_info(h, ctypes.byref(info)))
     return NfftPlan(d=d, n_axis=n_axis, sigma=sig, q=int(q), grid_shape=tuple(info.grid)[3 - d:],
                     sigma_eff=tuple(info.sigma_eff)[3 - d:], lam=tuple(info.lam)[3 - d:], nodes=pts,
-                    backend="generic" if info.generic else "tiled", exact=bool(exact), _handle=h.value)
+                    backend="generic" if info.generic else ("i8" if info.i8_gather else "tiled"), exact=bool(exact),
+                    _handle=h.value)
 
 
 def nfft_execute(plan: NfftPlan, coeffs):

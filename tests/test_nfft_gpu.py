@@ -19,7 +19,7 @@ def sgl():
     return s
 
 
-@pytest.mark.parametrize("backend", ["auto", "generic"])
+@pytest.mark.parametrize("backend", ["auto", "tiled", "generic"])
 @pytest.mark.parametrize("name", NFFT)
 def test_nfft_matches_reference(sgl, name, backend):
     g = load_golden(name)
