@@ -125,3 +125,17 @@ def test_int8_scatter_dynamic_range_and_pairing(sgl, scale):
     fx = sgl.forward(p8, x)
     nv = np.linalg.norm(v / scale) * scale   # (the plain norm underflows at 1e-200)
     assert abs(np.vdot(v, fx) - np.vdot(a8, x)) <= 1e-11 * nv * (np.linalg.norm(x) + np.linalg.norm(fx))
+
+
+@pytest.mark.parametrize("B", [8, 16, 32])
+def test_edge_concentrated_sgl_spectra(sgl, B):
+    # coefficients only at the highest |m| (trig volume at the spectral edge,
+    # where the deconvolution gain amplifies the digit-split error most)
+    from paper_1809_10786_b200 import indexing
+    rng = np.random.default_rng(40 + B)
+    pts = sgl.gen_points_ball(5000, 2.0 + B / 8, rng)
+    nlm = indexing.mu_to_nlm_array(B)
+    c = np.where(np.abs(nlm[:, 2]) == B - 1, sgl.gen_coeffs(B, rng), 0)
+    f8 = sgl.forward(sgl.plan(B, pts), c)
+    f64 = sgl.forward(sgl.plan(B, pts, backend="tiled"), c)
+    assert rel(f8, f64) <= TOL_I8   # measured <= 2.5e-12 (tools/i8_adversarial.py)

@@ -18,13 +18,8 @@ def rel(a, b):
 
 
 def mk(B, pts, rho, q=16, i8=False, sigma=2):
-    if i8:
-        os.environ["SGL_GATHER"] = "i8"
-    else:
-        os.environ.pop("SGL_GATHER", None)
-    p = sgl.plan(B, pts, rho=rho, q=q, sigma=sigma, profile=True)
-    os.environ.pop("SGL_GATHER", None)
-    return p
+    # default backend: int8 tensor-core gather; "tiled": the FP64 DMMA gather
+    return sgl.plan(B, pts, rho=rho, q=q, sigma=sigma, profile=True, backend="auto" if i8 else "tiled")
 
 
 ap = argparse.ArgumentParser()
