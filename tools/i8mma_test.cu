@@ -132,6 +132,72 @@ __global__ void k_check_mn(const int8_t *A, const int8_t *B, int32_t *D, int K, 
     if (warp == 0) umma::tmem_free(td, 256);
 }
 
+// A from TMEM: thread m writes its row (K bytes, 4 per 32-bit column) with
+// tcgen05.st.32x32b.x8 (32 bytes = one K-step per store) at columns [col_a + 8 kb ...)
+__global__ void k_check_ts(const int8_t *A, const int8_t *B, int32_t *D, int K, int N) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t *sB = sm;
+    const uint32_t lboB = N * 16;
+    for (int i = tid; i < N * K; i += blockDim.x) {
+        int r = i / K, k = i % K;
+        sB[(k / 16) * lboB + (r / 8) * 128 + (r % 8) * 16 + (k % 16)] = (uint8_t)B[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) umma::tmem_alloc(&tbase, 512);
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t td = tbase, ta = tbase + 256;
+    // row m = tid: K bytes -> K / 4 words
+    for (int kb = 0; kb < K / 32; ++kb) {
+        uint32_t w[8];
+        for (int j = 0; j < 8; ++j) {
+            uint32_t x = 0;
+            for (int b = 0; b < 4; ++b) x |= (uint32_t)(uint8_t)A[tid * K + kb * 32 + j * 4 + b] << (8 * b);
+            w[j] = x;
+        }
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(
+                         ta + ((uint32_t)(warp * 32) << 16) + kb * 8),
+                     "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    if (tid == 0) {
+        const uint32_t id = umma::idesc_i8(128, N, true, true);
+        for (int kb = 0; kb < K / 32; ++kb) {
+            uint64_t db = umma::desc_kmajor(umma::smem_addr(sB) + kb * 2 * lboB, lboB, 128);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(td),
+                "r"(ta + kb * 8), "l"(db), "r"(id), "r"((uint32_t)(kb > 0)));
+        }
+        umma::commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    umma::fence_after();
+    for (int c = 0; c < N; c += 16) {
+        int32_t v[16];
+        umma::tmem_ld16(td + ((uint32_t)(warp * 32) << 16) + c, v);
+        umma::tmem_ld_wait();
+        for (int j = 0; j < 16; ++j)
+            if (c + j < N) D[(warp * 32 + lane) * N + c + j] = v[j];
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(td, 512);
+}
+
 // throughput: each CTA issues iters x (K/32) MMAs on its resident operands
 __global__ void k_rate(int K, int N, int iters, int32_t *sink) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -309,6 +375,37 @@ int main() {
         for (int i = 0; i < 128 * N; ++i) nbad += D[i] != R[i];
         printf("check MN-major N=%d: %s, %d mismatches (D[0]=%d ref %d)\n", N, cudaGetErrorString(e), nbad, D[0], R[0]);
         bad += nbad != 0 || e != cudaSuccess;
+    }
+    for (int N : {64, 128, 256}) {
+        const int KK = 96;
+        std::vector<int8_t> A(128 * KK), B(N * KK);
+        std::vector<int32_t> D(128 * N), R(128 * N);
+        srand(17 + N);
+        for (auto &x : A) x = (int8_t)(rand() & 255);
+        for (auto &x : B) x = (int8_t)(rand() & 255);
+        for (int m = 0; m < 128; ++m)
+            for (int n = 0; n < N; ++n) {
+                long sacc = 0;
+                for (int k = 0; k < KK; ++k) sacc += (int)A[m * KK + k] * (int)B[n * KK + k];
+                R[m * N + n] = (int32_t)sacc;
+            }
+        int8_t *dA, *dB;
+        int32_t *dD;
+        cudaMalloc(&dA, A.size());
+        cudaMalloc(&dB, B.size());
+        cudaMalloc(&dD, D.size() * 4);
+        cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice);
+        size_t smem = N * KK;
+        cudaFuncSetAttribute(k_check_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_check_ts<<<1, 128, smem>>>(dA, dB, dD, KK, N);
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+        int nbad = 0;
+        for (int i = 0; i < 128 * N; ++i) nbad += D[i] != R[i];
+        printf("check A-in-TMEM N=%d: %s, %d mismatches (D[0]=%d ref %d)\n", N, cudaGetErrorString(e), nbad, D[0], R[0]);
+        bad += nbad != 0 || e != cudaSuccess;
+        if (e != cudaSuccess) return 1;
     }
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
