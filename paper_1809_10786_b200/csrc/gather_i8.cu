@@ -450,9 +450,16 @@ int setup_i8(Plan &p) {
     if (cudaMalloc(&p.digits, bytes) != cudaSuccess ||
         cudaMalloc(&p.gmax, (sizeof(unsigned long long) + sizeof(int)) * w.N0 + sizeof(int) * (p.n_itiles + 1)) !=
             cudaSuccess) {
+        // not enough memory for the grid digits (0.75x the grid): fall back to
+        // the FP64 DMMA gather, which needs none
         cudaGetLastError();
-        set_error("out of device memory for the int8 grid digits");
-        return SGL_ENOMEM;
+        if (p.digits) cudaFree(p.digits);
+        if (p.gmax) cudaFree(p.gmax);
+        p.digits = nullptr;
+        p.gmax = nullptr;
+        p.i8 = false;
+        p.i8s = false;
+        return SGL_OK;
     }
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult qr;
