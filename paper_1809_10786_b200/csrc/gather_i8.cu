@@ -79,9 +79,17 @@ struct I8Smem {
 // p+q0-DMIN .. ; 21 digit pairs with p + q >= DMIN in 9 MMAs.
 
 
+__device__ __forceinline__ void st_async_v4(void *dst, const uint32_t (&v)[4], uint64_t *bar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
+            umma::smem_addr(dst)),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(umma::smem_addr(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * t.e0 + 1) >> 1; }
 
-__global__ void __launch_bounds__(IT, 1)
+__global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
     k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
                 NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
                 const int *__restrict__ gsh, const int *__restrict__ tsh, double2 *__restrict__ out,
@@ -92,7 +100,7 @@ __global__ void __launch_bounds__(IT, 1)
 
     if (tid == 0) {
         for (int s = 0; s < NSTG; ++s) {
-            mbar_init(&S.fullA[s], 8);   // 2 chunks x 4 warps per K-step
+            mbar_init(&S.fullA[s], 1);   // one expect_tx arrive + the st.async bytes of a K-step
             mbar_init(&S.empty[s], 1);
         }
         for (int s = 0; s < NSTGB; ++s) {
@@ -262,13 +270,13 @@ __global__ void __launch_bounds__(IT, 1)
                     dw[5][q4] = prmt(h0, h1, 0x7632) ^ 0x80808080u;
                 }
                 if (use) mbar_wait(&S.empty[stg], (use - 1) & 1, 5);
+                // st.async: async-proxy stores that complete_tx on the stage's
+                // barrier (no proxy fence, no per-warp arrive); one thread per
+                // K-step registers the stage's byte count
+                if (h == 0 && n == 0) mbar_expect_tx(&S.fullA[stg], A_STAGE);
                 uint8_t *dst = S.a[stg] + h * A_CHUNK + n * 16;
 #pragma unroll
-                for (int p = 0; p < ND; ++p)
-                    *reinterpret_cast<uint4 *>(dst + p * A_DIGIT) = make_uint4(dw[p][0], dw[p][1], dw[p][2], dw[p][3]);
-                umma::fence_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.fullA[stg]);
+                for (int p = 0; p < ND; ++p) st_async_v4(dst + p * A_DIGIT, dw[p], &S.fullA[stg]);
             }
             g += (uint32_t)ns;
         }
