@@ -51,3 +51,20 @@ def test_plan_create_rejects_like_reference(B, M, sigma, q, flags, msg):
     assert not h.value
     with pytest.raises(ValueError):
         _native.check(rc)
+
+
+def test_plan_info_layout_matches_header(tmp_path):
+    # the ctypes mirror of sgl_plan_info must match the C struct field by field
+    # (size and offsets from the header, compiled with the host C compiler)
+    fields = [f[0] for f in _native.PlanInfo._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "sgl_b200.h"\nint main(void){\n'
+                   '  printf("%zu\\n", sizeof(sgl_plan_info));\n' +
+                   "".join(f'  printf("%zu\\n", offsetof(sgl_plan_info, {f}));\n' for f in fields) + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    rc = os.system(f"gcc -I{os.path.join(ROOT, 'include')} -o {exe} {src} 2>/dev/null")
+    if rc != 0:
+        pytest.skip("no host C compiler")
+    got = [int(x) for x in os.popen(str(exe)).read().split()]
+    assert got[0] == ctypes.sizeof(_native.PlanInfo)
+    assert got[1:] == [getattr(_native.PlanInfo, f).offset for f in fields]
