@@ -9,6 +9,9 @@ import numpy as np
 import paper_1809_10786_b200 as sgl
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+# second argument: the backend under test ("tiled": FP64 DMMA kernels; "auto":
+# the int8 tensor-core gather + FP64 scatter), always against the per-node kernels
+backend = sys.argv[2] if len(sys.argv) > 2 else "tiled"
 worst = 0.0
 t0 = time.time()
 for seed in range(n):
@@ -33,7 +36,7 @@ for seed in range(n):
     compact = bool(rng.random() < 0.2)
     c = sgl.gen_coeffs(B, rng)
     v = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
-    pa = sgl.plan(B, pts, sigma=sigma, q=q, compact_k1=compact, backend="tiled" if q <= 16 else "auto")
+    pa = sgl.plan(B, pts, sigma=sigma, q=q, compact_k1=compact, backend=backend if q <= 16 else "auto")
     pb = sgl.plan(B, pts, sigma=sigma, q=q, compact_k1=compact, backend="generic")
     for x, y in ((sgl.forward(pa, c), sgl.forward(pb, c)), (sgl.adjoint(pa, v), sgl.adjoint(pb, v))):
         den = np.max(np.abs(y))
@@ -43,4 +46,4 @@ for seed in range(n):
             print("MISMATCH", seed, B, sigma, q, M, kind, compact, r)
     pa.close()
     pb.close()
-print(f"{n} random plans, worst tiled-vs-generic rel-linf {worst:.2e}, {time.time() - t0:.0f} s")
+print(f"{n} random plans, worst {backend}-vs-generic rel-linf {worst:.2e}, {time.time() - t0:.0f} s")
