@@ -530,15 +530,18 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
         unsigned long long h[4 * 1024];
         cudaMemcpyAsync(h, prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        double tot = 0, a = 0, b = 0, e = 0;
+        double tot = 0, a = 0, b = 0, e = 0, mn = 1e300, mx = 0;
         for (int i = 0; i < blocks; ++i) {
+            mn = std::min(mn, (double)h[4 * i]);
+            mx = std::max(mx, (double)h[4 * i]);
             tot += h[4 * i];
             a += h[4 * i + 1];
             b += h[4 * i + 2];
             e += h[4 * i + 3];
         }
-        fprintf(stderr, "i8 MMA warp: total %.0f cycles/CTA, wait fullA %.1f%%, fullB %.1f%%, tempty %.1f%%\n",
-                tot / blocks, 100 * a / tot, 100 * b / tot, 100 * e / tot);
+        fprintf(stderr,
+                "i8 MMA warp: total %.0f cycles/CTA (min %.0f, max %.0f), wait fullA %.1f%%, fullB %.1f%%, tempty %.1f%%\n",
+                tot / blocks, mn, mx, 100 * a / tot, 100 * b / tot, 100 * e / tot);
     }
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
