@@ -11,26 +11,23 @@
 //     V = w1 v      (fixed point at a per-tile scale from the tile's max |v|),
 // both split into 6 balanced bytes; the 21 digit pairs with p + q >= 5 in 9
 // MMAs per K-step of 32 nodes (W digit p times V digits stacked along N),
-// int32 diagonal accumulators in TMEM (6 x 80 columns).  Operands are built
-// by generator warps straight into the MN-major UMMA layout (16 consecutive
-// cells / columns per 16-byte row, 8 nodes per core matrix).  The epilogue
-// converts an M-block to FP64 and reduces it into the halo-padded grid with
-// RED.E.ADD.F64 straight from the TMEM loads (k_halo_fold folds the halo as
-// for the FP64 scatter); meanwhile the generators fill the 5-deep ring for
-// the next block.  512-node tiles keep the REDs at ~300 per node.
+// int32 diagonal accumulators in TMEM (6 x 80 columns).
 //
-// CTA (one per SM, persistent): warp 0 MMA issuer, warps 1-8 weight-digit
-// generators (node x 16-cell group), warps 9-13 value-digit generators (node
-// x 16-column group), warps 14-17 epilogue (TMEM lane quarters = cells).
+// V does not depend on the M-block: its digits are built once per adjoint by
+// k_vdigits into global memory, already in the MN-major UMMA layout of a
+// K-step (15 KB per 32 nodes), and a producer warp streams them into shared
+// memory with 1-D bulk copies (cp.async.bulk, L2-resident across the tile's
+// M-blocks).  Only W is built on the fly, by 8 generator warps (node x
+// 16-cell group, weights from per-node factors in shared memory), stored with
+// st.async.  The epilogue converts an M-block to FP64 into a per-thread
+// staging column, frees TMEM for the next block's MMAs and only then reduces
+// the block into the halo-padded grid with RED.E.ADD.F64 (k_halo_fold folds
+// the halo as for the FP64 scatter).  512-node tiles keep the REDs at ~300
+// per node.
 //
-// Status (round 1): correct (1e-13 .. 2.5e-12 vs the FP64 scatter and the
-// reference goldens) but not faster than the FP64 DMMA scatter (config 3:
-// 54.7 vs 50.1 ms), so it is opt-in (SGL_SCATTER=i8).  The MMA warp waits
-// ~57 % on the operand generators (SGL_I8_PROF=1): unlike the gather, where a
-// generator thread owns one node for a whole tile (weights in registers), K
-// runs over the nodes here, so every K-step hands each thread a new node and
-// the weights are rebuilt from per-node factors in shared memory; with the
-// staging column the ring is only 2 stages deep.
+// CTA (one per SM, persistent, cluster of 1 for st.async): warp 0 MMA
+// issuer, warp 1 value-digit producer, warps 2-9 weight-digit generators,
+// warps 10-13 epilogue (TMEM lane quarters = cells).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,28 +48,26 @@ using namespace i8;
 constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
-constexpr int NSTG = 2;                  // operand ring depth (the staging column takes the rest)
-constexpr int KST = 32;                  // nodes per stage (one MMA K-step)
-constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 8 node blocks x 8 cell blocks x 128 B (MN-major)
+constexpr int NSTG = 2;                  // weight-digit ring (K-steps of 32 nodes)
+constexpr int NSTGB = 3;                 // value-digit ring
+constexpr int KST = 32;                  // nodes per K-step
+constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 4 node blocks x 8 cell blocks x 128 B (MN-major)
 constexpr int A_STAGE = ND * A_DIGIT;
 constexpr int B_KBLK = ND * (ROWS / 16) * 128;   // one 8-node block of all 6 value digits
-constexpr int B_STAGE = (KST / 8) * B_KBLK;
-constexpr int NWG = 8, NVG = 5;          // weight / value generator warps
-constexpr int NGEN = NWG + NVG;
+constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (global and smem layout)
+constexpr int NWG = 8;                   // weight generator warps (32 nodes x 8 cell groups)
 constexpr int NEW = 4;
-constexpr int ST = (1 + NGEN + NEW) * 32;
-static_assert(ROWS % 16 == 0 && NVG * 32 == 32 * ROWS / 16, "value items: 32 nodes x 5 column groups");
+constexpr int ST = (2 + NWG + NEW) * 32;
 
 struct SSmem {
     uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
-    uint8_t b[NSTG][B_STAGE];    // value digits  [node/8][digit][col/16][node%8][col%16]
-    double u0[SN], u1[SN];
-    double2 v[SN];
+    uint8_t b[NSTGB][B_STAGE];   // value digits  [node/8][digit][col/16][node%8][col%16]
+    double stage[ROWS][MR];      // epilogue: one M-block in FP64, [column][cell]
+    double u0[SN];
     double e2[CHUNKS][SN], f2[CHUNKS][SN];   // W2 of chunk cc: w(cb + j) = e2 f2^j exp(-h2 j^2)
-    int lo0[SN], hi0[SN], lo2[SN], hi2[SN];
-    double w0t[4][SN];                      // W0 of the current M-block's (<= 4) slabs
-    double stage[ROWS][MR];                 // epilogue: one M-block in FP64, [column][cell]
-    uint64_t full[NSTG], empty[NSTG];
+    int lo2[SN], hi2[SN];
+    double w0t[4][SN];           // W0 of the current M-block's (<= 4) slabs
+    uint64_t fullA[NSTG], emptyA[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
     uint32_t tbase;
 };
@@ -82,27 +77,89 @@ struct G16 {
     __device__ __forceinline__ double operator[](int j) const { return v[j]; }
 };
 
-__device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NGEN * 32) : "memory"); }
+__device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NWG * 32) : "memory"); }
 
 __device__ __forceinline__ void red_add(double *addr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_async_v4(void *dst, const uint32_t (&v)[4], uint64_t *bar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
+            umma::smem_addr(dst)),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(umma::smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     umma::smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(umma::smem_addr(bar))
+                 : "memory");
+}
+
 __device__ __forceinline__ int mblocks(const Tile &t) { return (t.e0 * CHUNKS * 16 + MR - 1) / MR; }
 __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1) / KST; }
 
-__global__ void __launch_bounds__(ST, 1)
+// value digits of every K-step of every tile (once per adjoint): thread =
+// (node of the K-step, 16-column group = 8 axis-1 cells x re|im)
+__global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
+                          const double2 *__restrict__ values, const int *__restrict__ tsv,
+                          const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig) {
+    const int kl = threadIdx.x & 31, vg = threadIdx.x >> 5;   // 5 warps = 5 column groups
+    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const Tile t = tiles[ti];
+        const int svt = tsv[ti];
+        const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);
+        const int bb = t.o1 + vg * 8;
+        for (int ks = 0; ks < ksteps(t); ++ks) {
+            const int kn = ks * KST + kl;
+            const bool live = kn < t.count;
+            const int64_t si = (int64_t)t.start + kn;
+            const double u1 = live ? nodes.u1[si] : -1e9;
+            const double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
+            int lo1, hi1;
+            window_cells(u1, wp.q, lo1, hi1);
+            const int bf = max(0, lo1 - bb);
+            const double d = u1 - (double)(bb + bf);
+            double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
+            double wv[16];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double w1 = (live && j >= bf && bb + j <= hi1) ? w : 0.0;
+                if (j >= bf) {
+                    w *= r;
+                    r *= wp.r1_1;
+                }
+                wv[2 * j] = w1 * vv.x;
+                wv[2 * j + 1] = w1 * vv.y;
+            }
+            uint32_t dw[ND][4];
+            digits16(vsc, wv, dw);
+            uint8_t *dst = vdig + (voff[ti] + ks) * (int64_t)B_STAGE + (kl >> 3) * B_KBLK + vg * 128 + (kl & 7) * 16;
+#pragma unroll
+            for (int q = 0; q < ND; ++q)
+                *reinterpret_cast<uint4 *>(dst + q * (ROWS / 16) * 128) = make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
+        }
+    }
+}
+
+__global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
-                 double s2, int sA, const int *__restrict__ tsv, const double2 *__restrict__ values,
-                 double *__restrict__ grid, unsigned long long *__restrict__ prof, const G16 g2) {
+                 double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
+                 const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SSmem &S = *reinterpret_cast<SSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
         for (int s = 0; s < NSTG; ++s) {
-            mbar_init(&S.full[s], NGEN);
-            mbar_init(&S.empty[s], 1);
+            mbar_init(&S.fullA[s], 1);   // one expect_tx arrive + the st.async bytes
+            mbar_init(&S.emptyA[s], 1);
+        }
+        for (int s = 0; s < NSTGB; ++s) {
+            mbar_init(&S.fullB[s], 1);
+            mbar_init(&S.emptyB[s], 1);
         }
         mbar_init(&S.tfull, 1);
         mbar_init(&S.tempty, NEW);
@@ -116,31 +173,25 @@ __global__ void __launch_bounds__(ST, 1)
 
     if (warp == 0) {
         // ---- MMA issuer
-        const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), 1024, 128);       // MN-major: LBO = node
-        const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);     // block, SBO = 16 rows
-        constexpr uint32_t MN = (1u << 15) | (1u << 16);                                 // A, B MN-major
+        const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), 1024, 128);      // MN-major: LBO = node
+        const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);    // block, SBO = 16 rows
+        constexpr uint32_t MN = (1u << 15) | (1u << 16);                                // A, B MN-major
         uint32_t g = 0, mc = 0;
-        long long q0 = clock64(), qf = 0, qe = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
-                long long x0 = clock64();
                 if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
-                qe += clock64() - x0;
                 umma::fence_after();
                 for (int ks = 0; ks < nks; ++ks, ++g) {
-                    const int stg = (int)(g % NSTG);
-                    long long x1 = clock64();
-                    mbar_wait(&S.full[stg], (g / NSTG) & 1);
-                    qf += clock64() - x1;
+                    const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
+                    mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1);
+                    mbar_wait(&S.fullA[stg], (g / NSTG) & 1);
                     umma::fence_after();
                     if (umma::elect_one()) {
-#pragma unroll
-                        for (int kh = 0; kh < KST / 32; ++kh) {   // MMA K-steps of 32 nodes in the stage
-                        const uint64_t ad = a0 + (uint64_t)((stg * A_STAGE + kh * 4 * 1024) >> 4);
-                        const uint64_t bd = b0 + (uint64_t)((stg * B_STAGE + kh * 4 * B_KBLK) >> 4);
-                        const bool acc = ks > 0 || kh > 0;
+                        const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
+                        const uint64_t bd = b0 + (uint64_t)(stgb * (B_STAGE >> 4));
+                        const bool acc = ks > 0;
 #define SGL_I8S_OP(P, Q0, NQ, ACC)                                                                         \
     umma::mma_i8(tbase + (uint32_t)(((P) + (Q0)-DMIN) * ROWS), ad + (uint64_t)((P)*A_DIGIT >> 4),         \
                  bd + (uint64_t)((Q0) * (ROWS / 16) * 128 >> 4), umma::idesc_i8(MR, (NQ)*ROWS, true, true) | MN, \
@@ -156,8 +207,8 @@ __global__ void __launch_bounds__(ST, 1)
                         SGL_I8S_OP(1, 4, 2, true);
                         SGL_I8S_OP(0, 5, 1, true);
 #undef SGL_I8S_OP
-                        }
-                        umma::commit(&S.empty[stg]);
+                        umma::commit(&S.emptyA[stg]);
+                        umma::commit(&S.emptyB[stgb]);
                     }
                     __syncwarp();
                 }
@@ -165,36 +216,41 @@ __global__ void __launch_bounds__(ST, 1)
                 __syncwarp();
             }
         }
-        if (prof && lane == 0) {
-            prof[blockIdx.x * 8 + 0] = clock64() - q0;
-            prof[blockIdx.x * 8 + 1] = qf;
-            prof[blockIdx.x * 8 + 2] = qe;
-            prof[blockIdx.x * 8 + 3] = mc;
+    } else if (warp == 1) {
+        // ---- value-digit producer: one bulk copy per K-step (re-read from L2 per M-block)
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+                const Tile t = tiles[ti];
+                const int nmb = mblocks(t), nks = ksteps(t);
+                const uint8_t *src = vdig + voff[ti] * (int64_t)B_STAGE;
+                for (int mb = 0; mb < nmb; ++mb)
+                    for (int ks = 0; ks < nks; ++ks, ++g) {
+                        const int stg = (int)(g % NSTGB);
+                        const uint32_t use = g / NSTGB;
+                        if (use) mbar_wait(&S.emptyB[stg], (use - 1) & 1);
+                        mbar_expect_tx(&S.fullB[stg], B_STAGE);
+                        bulk_load(S.b[stg], src + ks * (int64_t)B_STAGE, B_STAGE, &S.fullB[stg]);
+                    }
+            }
         }
-    } else if (warp <= NGEN) {
-        // ---- operand generators: warps 1-8 weight digits (node, 16-cell group),
-        // warps 9-13 value digits (node, 16-column group = 8 axis-1 cells x re|im)
-        // lanes 0-7 of a warp take 8 consecutive nodes, so each 16-byte store
-        // row of a warp covers all 32 banks (conflict-free STS.128)
-        const int gt = tid - 32;
-        const bool wgen = gt < NWG * 32;
-        const int wi = gt >> 5, vi = gt - NWG * 32, vc = vi >> 3;
-        const int kl = wgen ? (wi & 3) * 8 + (lane & 7) : (vc / NVG) * 8 + (vi & 7);   // node within the K-step
-        const int grp = wgen ? (wi >> 2) * 4 + (lane >> 3) : vc % NVG;                // cell / column group
+    } else if (warp < 2 + NWG) {
+        // ---- weight-digit generators: thread = (node of the K-step, 16-cell group);
+        // lanes 0-7 take 8 consecutive nodes (each 16-byte store row of a warp
+        // covers all 32 banks)
+        const int gt = tid - 64, wi = gt >> 5;
+        const int kl = (wi & 3) * 8 + (lane & 7), grp = (wi >> 2) * 4 + (lane >> 3);
         uint32_t g = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
             gen_sync();   // the previous tile's readers of the node tables are done
             const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
-            for (int i = gt; i < t.count; i += NGEN * 32) {
-                // per node: coordinates, value, window limits and the W2 factors of the
-                // three 16-cell chunks (2 exps per chunk here instead of per K-step)
+            for (int i = gt; i < t.count; i += NWG * 32) {
+                // per node: axis-0 coordinate, axis-2 window and the W2 factors of
+                // the three 16-cell chunks (2 exps per chunk here, none per K-step)
                 const int64_t si = (int64_t)t.start + i;
-                const double u0 = nodes.u0[si], u2 = nodes.u2[si];
-                S.u0[i] = u0;
-                S.u1[i] = nodes.u1[si];
-                S.v[i] = values[nodes.perm[si]];
-                window_cells(u0, wp.q, S.lo0[i], S.hi0[i]);
+                const double u2 = nodes.u2[si];
+                S.u0[i] = nodes.u0[si];
                 window_cells(u2, wp.q, S.lo2[i], S.hi2[i]);
 #pragma unroll
                 for (int cc = 0; cc < CHUNKS; ++cc) {
@@ -205,95 +261,57 @@ __global__ void __launch_bounds__(ST, 1)
             }
             gen_sync();
             const int nmb = mblocks(t), nks = ksteps(t);
-            const int svt = __ldg(tsv + ti);
-            const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);   // value fixed-point scale of the tile
             for (int mb = 0; mb < nmb; ++mb) {
                 // W0 of every node on the (<= 4) slabs of this M-block, once per block
                 const int a_mb = (mb * 8) / CHUNKS;
                 gen_sync();   // the previous block's readers of w0t are done
-                for (int i = gt; i < 4 * t.count; i += NGEN * 32) {
+                for (int i = gt; i < 4 * t.count; i += NWG * 32) {
                     const int j = i / t.count, n = i - j * t.count, al = a_mb + j, cell0 = t.o0 + al;
+                    const double u0 = S.u0[n];
+                    int lo0, hi0;
+                    window_cells(u0, wp.q, lo0, hi0);
                     double w0 = 0.0;
-                    if (al < t.e0 && cell0 >= S.lo0[n] && cell0 <= S.hi0[n]) {
-                        const double d0 = S.u0[n] - (double)cell0;
+                    if (al < t.e0 && cell0 >= lo0 && cell0 <= hi0) {
+                        const double d0 = u0 - (double)cell0;
                         w0 = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
                     }
                     S.w0t[j][n] = w0;
                 }
                 gen_sync();
+                const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
+                const int cb = kst + 16 * cc;
                 for (int ks = 0; ks < nks; ++ks, ++g) {
                     const int stg = (int)(g % NSTG);
                     const uint32_t use = g / NSTG;
-                  for (int h = 0; h < KST / 32; ++h) {   // two 32-node halves of the stage
-                    const int kn = ks * KST + 32 * h + kl;
+                    const int kn = ks * KST + kl;
                     const bool live = kn < t.count;
+                    const int kk = live ? kn : 0;
+                    // w2(cb + j) = e f^j g_j: powers of f by a depth-4 product tree
+                    const double w0 = live ? S.w0t[al - a_mb][kk] : 0.0;
+                    const int jlo = S.lo2[kk] - cb, jhi = S.hi2[kk] - cb;
+                    const double e = live ? (cc == 0 ? S.e2[0][kk] : (cc == 1 ? S.e2[1][kk] : S.e2[2][kk])) : 0.0;
+                    const double f = cc == 0 ? S.f2[0][kk] : (cc == 1 ? S.f2[1][kk] : S.f2[2][kk]);
+                    double pw[16], w2[16];
+                    pw[0] = e;
+                    pw[1] = e * f;
+                    const double f2 = f * f, f4 = f2 * f2, f8 = f4 * f4;
+                    pw[2] = e * f2;
+                    pw[3] = pw[1] * f2;
+                    pw[4] = e * f4;
+                    pw[5] = pw[1] * f4;
+                    pw[6] = pw[2] * f4;
+                    pw[7] = pw[3] * f4;
+#pragma unroll
+                    for (int j = 8; j < 16; ++j) pw[j] = pw[j - 8] * f8;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) w2[j] = (j >= jlo && j <= jhi) ? pw[j] * g2[j] : 0.0;
                     uint32_t dw[ND][4];
-                    if (wgen) {
-                        const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
-                        double w2[16];
-                        const int kk = live ? kn : 0;
-                        const double w0 = live ? S.w0t[al - a_mb][kk] : 0.0;
-                        // w2(cb + j) = e f^j g_j (g_j = exp(-h2 j^2), per plan): powers of f
-                        // by a depth-4 product tree instead of a 16-step recurrence
-                        const int cb = kst + 16 * cc;
-                        const int jlo = S.lo2[kk] - cb, jhi = S.hi2[kk] - cb;
-                        const double e = live ? (cc == 0 ? S.e2[0][kk] : (cc == 1 ? S.e2[1][kk] : S.e2[2][kk])) : 0.0;
-                        const double f = cc == 0 ? S.f2[0][kk] : (cc == 1 ? S.f2[1][kk] : S.f2[2][kk]);
-                        double pw[16];
-                        pw[0] = e;
-                        pw[1] = e * f;
-                        const double f2 = f * f, f4 = f2 * f2, f8 = f4 * f4;
-                        pw[2] = e * f2;
-                        pw[3] = pw[1] * f2;
-                        pw[4] = e * f4;
-                        pw[5] = pw[1] * f4;
-                        pw[6] = pw[2] * f4;
-                        pw[7] = pw[3] * f4;
+                    digits16(w0, w2, dw);
+                    if (use) mbar_wait(&S.emptyA[stg], (use - 1) & 1);
+                    if (gt == 0) mbar_expect_tx(&S.fullA[stg], A_STAGE);
+                    uint8_t *dst = S.a[stg] + (kl >> 3) * 1024 + grp * 128 + (kl & 7) * 16;
 #pragma unroll
-                        for (int j = 8; j < 16; ++j) pw[j] = pw[j - 8] * f8;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) w2[j] = (j >= jlo && j <= jhi) ? pw[j] * g2[j] : 0.0;
-                        digits16(w0, w2, dw);
-                    } else {
-                        double wv[16];
-                        const double u1 = live ? S.u1[kn] : -1e9;
-                        const double2 vv = live ? S.v[kn] : make_double2(0.0, 0.0);
-                        int lo1, hi1;
-                        window_cells(u1, wp.q, lo1, hi1);
-                        const int bb = t.o1 + grp * 8;
-                        const int bf = max(0, lo1 - bb);
-                        const double d = u1 - (double)(bb + bf);
-                        double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const double w1 = (live && j >= bf && bb + j <= hi1) ? w : 0.0;
-                            if (j >= bf) {
-                                w *= r;
-                                r *= wp.r1_1;
-                            }
-                            wv[2 * j] = w1 * vv.x;
-                            wv[2 * j + 1] = w1 * vv.y;
-                        }
-                        digits16(vsc, wv, dw);
-                    }
-                    if (use && h == 0) mbar_wait(&S.empty[stg], (use - 1) & 1);
-                    if (wgen) {
-                        uint8_t *dst = S.a[stg] + ((32 * h + kl) >> 3) * 1024 + grp * 128 + (kl & 7) * 16;
-#pragma unroll
-                        for (int p = 0; p < ND; ++p)
-                            *reinterpret_cast<uint4 *>(dst + p * A_DIGIT) =
-                                make_uint4(dw[p][0], dw[p][1], dw[p][2], dw[p][3]);
-                    } else {
-                        uint8_t *dst = S.b[stg] + ((32 * h + kl) >> 3) * B_KBLK + grp * 128 + (kl & 7) * 16;
-#pragma unroll
-                        for (int q = 0; q < ND; ++q)
-                            *reinterpret_cast<uint4 *>(dst + q * (ROWS / 16) * 128) =
-                                make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
-                    }
-                  }
-                    umma::fence_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&S.full[stg]);
+                    for (int p = 0; p < ND; ++p) st_async_v4(dst + p * A_DIGIT, dw[p], &S.fullA[stg]);
                 }
             }
         }
@@ -392,11 +410,21 @@ int setup_scatter_i8(Plan &p) {
             }
         }
     }
-    if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess) {
+    // value-digit buffer: one 15 KB block per K-step of every tile
+    std::vector<int64_t> off(p.n_istiles + 1, 0);
+    if (p.n_istiles > 0) {
+        std::vector<Tile> ht(p.n_istiles);
+        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < p.n_istiles; ++i) off[i + 1] = off[i] + (ht[i].count + KST - 1) / KST;
+    }
+    if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
+        cudaMalloc(&p.svoff, sizeof(int64_t) * (p.n_istiles + 1)) != cudaSuccess ||
+        cudaMalloc(&p.vdig, (size_t)std::max<int64_t>(1, off[p.n_istiles]) * B_STAGE) != cudaSuccess) {
         cudaGetLastError();
-        set_error("out of device memory for the int8 scatter scales");
+        set_error("out of device memory for the int8 scatter digits");
         return SGL_ENOMEM;
     }
+    SGL_CUDA_CHECK(cudaMemcpy(p.svoff, off.data(), sizeof(int64_t) * (p.n_istiles + 1), cudaMemcpyHostToDevice));
     return SGL_OK;
 }
 
@@ -404,34 +432,20 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     if (p.M == 0 || p.n_istiles == 0) return SGL_OK;
     k_tile_vscale<<<(unsigned)p.n_istiles, 256, 0, st>>>(p.istiles, p.n_istiles, p.inodes, values, p.wp.c1, p.tsv);
     SGL_CUDA_CHECK(cudaGetLastError());
+    const int sms = num_sms();
+    k_vdigits<<<(unsigned)std::min<int64_t>(p.n_istiles, (int64_t)sms * 12), (ROWS / 16) * 32, 0, st>>>(
+        p.istiles, p.n_istiles, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig);
+    SGL_CUDA_CHECK(cudaGetLastError());
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
     const int sA = 46 - e, a0 = sA / 2;
     const size_t sm = sizeof(SSmem);
     SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, num_sms()));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
-    static unsigned long long *prof = nullptr;
-    const bool want = getenv("SGL_I8_PROF") != nullptr;
-    if (want && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 8 * 1024);
-    if (!want) prof = nullptr;
     k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
-                                                  std::ldexp(1.0, sA - a0), sA, p.tsv, values,
-                                                  reinterpret_cast<double *>(grid), prof, g2);
-    if (want) {
-        std::vector<unsigned long long> h(8 * blocks);
-        cudaMemcpyAsync(h.data(), prof, sizeof(unsigned long long) * 8 * blocks, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        double tot = 0, f = 0, e = 0, nb = 0;
-        for (int i = 0; i < blocks; ++i) {
-            tot += h[8 * i];
-            f += h[8 * i + 1];
-            e += h[8 * i + 2];
-            nb += h[8 * i + 3];
-        }
-        fprintf(stderr, "i8 scatter MMA warp: %.0f cycles/CTA, wait operands %.1f%%, wait TMEM drain %.1f%% (%.0f cycles per M-block, %.0f M-blocks/CTA)\n",
-                tot / blocks, 100 * f / tot, 100 * e / tot, e / nb, nb / blocks);
-    }
+                                                  std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
+                                                  reinterpret_cast<double *>(grid), g2);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }

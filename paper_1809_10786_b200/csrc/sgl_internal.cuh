@@ -155,6 +155,8 @@ struct Plan {
     Tile *istiles = nullptr;       // its 512-node tiles
     int64_t n_istiles = 0;
     int *tsv = nullptr;            // per scatter tile: value fixed-point shift
+    int64_t *svoff = nullptr;      // per scatter tile: first value-digit block (K-step)
+    uint8_t *vdig = nullptr;       // value digits, 15 KB per K-step of every tile
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
     int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
