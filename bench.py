@@ -366,7 +366,10 @@ def main():
                           "engine": "int8 tensor cores (tcgen05.mma kind::i8, FP64 by 6x6 digit split)" if i8
                           else "FP64 DMMA (mma.sync m8n8k4)"}
     if direction in ("both", "adj"):
-        kern["scatter"] = {"ms": stages_adj["window"], "flop": w.M * flop_per_node, "engine": "FP64 DMMA (mma.sync m8n8k4)"}
+        i8s = bool(stats.get("i8_scatter"))
+        kern["scatter"] = {"ms": stages_adj["window"], "flop": w.M * flop_per_node,
+                           "engine": "int8 tensor cores (tcgen05.mma kind::i8, FP64 by 6x6 digit split)" if i8s
+                           else "FP64 DMMA (mma.sync m8n8k4)"}
     for k in kern.values():
         k["tflops"] = k["flop"] / (k["ms"] * 1e-3) / 1e12
         k["frac"] = k["tflops"] / FP64_PEAK_TFLOPS
@@ -375,19 +378,25 @@ def main():
         g["int8_tops"] = stats["i8_ksteps"] * I8_OPS_PER_KSTEP / (g["ms"] * 1e-3) / 1e12
         g["int8_frac"] = g["int8_tops"] / INT8_PEAK_TOPS
         g["int8_ops_per_launch"] = stats["i8_ksteps"] * I8_OPS_PER_KSTEP
+    if "scatter" in kern and stats.get("i8_scatter"):
+        g = kern["scatter"]   # same MMA shape per K-step: 21 pairs x M 128 cells x N 80 x K 32 nodes
+        g["int8_tops"] = stats["i8_sksteps"] * I8_OPS_PER_KSTEP / (g["ms"] * 1e-3) / 1e12
+        g["int8_frac"] = g["int8_tops"] / INT8_PEAK_TOPS
+        g["int8_ops_per_launch"] = stats["i8_sksteps"] * I8_OPS_PER_KSTEP
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic = None
     try:
         if args.config == 3 and w.M == 10_000_000:   # the configuration the ncu capture was taken on
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(dom + ("_i8" if dom == "gather" and i8 else ""))
+                traffic = json.load(f).get(dom + ("_i8" if "int8_tops" in kern[dom] else ""))
     except Exception:
         pass
-    if dom == "gather" and i8:
+    if "int8_tops" in kern[dom]:
+        ksteps = stats["i8_ksteps"] if dom == "gather" else stats["i8_sksteps"]
         roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["int8_tops"], "peak": INT8_PEAK_TOPS,
                 "unit": "TOP/s (int8)", "frac": kern[dom]["int8_frac"], "traffic": traffic,
                 "peak_source": "measured tcgen05 kind::i8 peak (profiles/i8_mma_rate_r01.txt)",
-                "algorithmic": f"{I8_OPS_PER_KSTEP:.0f} int8 ops per K-step x {stats['i8_ksteps']} K-steps per launch"}
+                "algorithmic": f"{I8_OPS_PER_KSTEP:.0f} int8 ops per K-step x {ksteps} K-steps per launch"}
     else:
         roof = {"bound": "tensor", "kernel": dom, "achieved": kern[dom]["tflops"], "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": kern[dom]["frac"], "traffic": traffic,
@@ -408,10 +417,12 @@ def main():
     cells = float(np.prod(p.nfft.grid_shape)) if p.nfft else 0.0
     t_gat = (stats["i8_ksteps"] * I8_OPS_PER_KSTEP / (INT8_PEAK_TOPS * 1e12) if i8 else
              w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
-    t_win = n_fwd * t_gat + n_adj * w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12) * 1e3
+    t_sca = (stats["i8_sksteps"] * I8_OPS_PER_KSTEP / (INT8_PEAK_TOPS * 1e12) if stats.get("i8_scatter") else
+             w.M * flop_per_node / (FP64_PEAK_TFLOPS * 1e12)) * 1e3
+    t_win = n_fwd * t_gat + n_adj * t_sca
     t_fft = (n_fwd + n_adj) * 3 * 2 * 16.0 * cells / (hbm_gbs * 1e9) * 1e3
     step_roof = {"t_roof_ms": t_win + t_fft, "window_ms": t_win, "fft_ms": t_fft, "frac": (t_win + t_fft) / ms,
-                 "model": ("gather: executed int8 ops / 4550 TOP/s (tcgen05 int8 peak); " if i8 else "") +
+                 "model": ("int8 window stages: executed int8 ops / 4550 TOP/s (tcgen05 int8 peak); " if i8 else "") +
                           "FP64 window FLOPs / 37.1 TF/s (FP64 DMMA peak) + 3-pass FFT bytes / HBM copy GB/s "
                           "(MEASURED_PEAKS.json); basal and halo work not counted"}
 
@@ -440,12 +451,15 @@ def main():
                        "l2": l2_note,
                        "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": args.steps * ((8 if i8 else 4) * K * (direction != "adj") + 4 * (direction != "fwd")),
+            "gpu_launches": args.steps * ((8 if i8 else 4) * K * (direction != "adj") +
+                                         (6 if stats.get("i8_scatter") else 4) * (direction != "fwd")),
             "gpu_launches_note": ("per forward vector: radial_fwd, sph_fwd, halo_fill, slab_absmax, slab_shift, "
                                   "slice_grid, tile_shift, gather_i8" if i8 else
                                   "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled") +
-                                 "; per adjoint: scatter_tiled, halo_fold, sph_adj, radial_adj (+ cuFFT and memsets, "
-                                 "library calls)",
+                                 ("; per adjoint: tile_vscale, vdigits, scatter_i8, halo_fold, sph_adj, radial_adj"
+                                    if stats.get("i8_scatter") else
+                                    "; per adjoint: scatter_tiled, halo_fold, sph_adj, radial_adj") +
+                                 " (+ cuFFT and memsets, library calls)",
             "kernels": {k: {kk: vv for kk, vv in v.items() if kk != "flop"} for k, v in kern.items()},
             "stages_ms": {"forward": stages_fwd, "adjoint": stages_adj},
             "plan": {"seconds": plan_s, **stats},

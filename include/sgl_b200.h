@@ -91,6 +91,9 @@ typedef struct {
     int64_t i8_tiles;         /* its 128-node tiles                            */
     int64_t i8_ksteps;        /* K-steps of 32 per gather pass (9 MMAs each,
                                  M = 128, N = 1680 digit columns in total)     */
+    int32_t i8_scatter;       /* 1 if the adjoint window stage runs on the int8
+                                 tensor cores (dense node sets, or forced)     */
+    int64_t i8_sksteps;       /* its K-steps (32 nodes x 128 cells) per pass   */
 } sgl_plan_info;
 
 /* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */

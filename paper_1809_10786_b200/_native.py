@@ -51,6 +51,8 @@ class PlanInfo(ctypes.Structure):
         ("i8_gather", ctypes.c_int32),
         ("i8_tiles", ctypes.c_int64),
         ("i8_ksteps", ctypes.c_int64),
+        ("i8_scatter", ctypes.c_int32),
+        ("i8_sksteps", ctypes.c_int64),
     ]
 
 

@@ -309,7 +309,10 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
         const char *ge = getenv("SGL_GATHER");
         p->i8 = !p->generic && !(flags & SGL_FLAG_FP64_WINDOW) && !(ge && !strcmp(ge, "fp64"));
         const char *se = getenv("SGL_SCATTER");   // "i8": int8 tensor-core scatter (experimental)
+        // int8 scatter: automatic for dense node sets (see build_nodes), forced by SGL_SCATTER=i8,
+        // off with SGL_SCATTER=fp64 or backend "tiled"
         p->i8s = p->i8 && se && !strcmp(se, "i8");
+        p->i8s_auto = p->i8 && !p->i8s && !(se && !strcmp(se, "fp64"));
     }
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
@@ -366,7 +369,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     p->grid_elems = (size_t)wp.N0 * wp.N1p * wp.N2p;
     if (wp.N1p < kBoxMax || wp.N2p < kBoxMax) p->generic = true;   // (not reached: pad widens the plane)
     if (wp.N1p < kI8Box1 || pad != q) p->i8 = false;   // digit TMA box within the plane; aligned K ranges
-    if (!p->i8) p->i8s = false;
+    if (!p->i8) p->i8s = p->i8s_auto = false;
     double *cs[3] = {&wp.c0, &wp.c1, &wp.c2}, *hs[3] = {&wp.h0, &wp.h1, &wp.h2};
     for (int ax = 0; ax < 3; ++ax) {
         if (exact) {
@@ -628,6 +631,8 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->i8_gather = p.i8 ? 1 : 0;
     info->i8_tiles = p.n_itiles;
     info->i8_ksteps = p.i8_ksteps;
+    info->i8_scatter = p.i8s ? 1 : 0;
+    info->i8_sksteps = p.i8_sksteps;
     return SGL_OK;
 }
 

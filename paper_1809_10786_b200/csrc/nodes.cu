@@ -386,7 +386,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         if (rc) return rc;
         rc = reorder_tiles(p.itiles, p.n_itiles, st);
         if (rc) return rc;
-        if (p.i8s) {
+        if (p.i8s || p.i8s_auto) {
             // int8 scatter: same order, 512-node tiles (fewer grid REDs per node)
             TileGeom sg = ig;
             sg.max_nodes = kI8SNodes;
@@ -395,6 +395,23 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
             if (rc) return rc;
             rc = reorder_tiles(p.istiles, p.n_istiles, st);
             if (rc) return rc;
+            if (!p.i8s) {
+                // automatic choice: the int8 scatter costs ~2700 SM-cycles per
+                // K-step (32 nodes x 128 cells), the FP64 DMMA scatter ~1400 per
+                // node (config 3, r01): take it for large dense node sets only (config 2,
+                // 1e6 lattice nodes: 6.9 vs 5.2 ms, its per-M-block drain dominates)
+                std::vector<Tile> h(p.n_istiles);
+                if (p.n_istiles)
+                    SGL_CUDA_CHECK(cudaMemcpy(h.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
+                double ks = 0;
+                for (const Tile &t : h) ks += (double)((t.e0 * kI8Box2 + 127) / 128) * ((t.count + 31) / 32);
+                p.i8s = p.M >= 5000000 && ks < 0.5 * (double)p.M;   // config 3 (1e7): 0.45, 46.8 vs 50.1 ms
+                if (!p.i8s) {
+                    cudaFree(p.istiles);
+                    p.istiles = nullptr;
+                    p.n_istiles = 0;
+                }
+            }
         }
     }
     // Scatter order: with dense nodes, W x W2 pencils whose axis-2 box is a

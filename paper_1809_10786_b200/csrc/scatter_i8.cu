@@ -415,7 +415,11 @@ int setup_scatter_i8(Plan &p) {
     if (p.n_istiles > 0) {
         std::vector<Tile> ht(p.n_istiles);
         SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < p.n_istiles; ++i) off[i + 1] = off[i] + (ht[i].count + KST - 1) / KST;
+        p.i8_sksteps = 0;
+        for (int64_t i = 0; i < p.n_istiles; ++i) {
+            off[i + 1] = off[i] + (ht[i].count + KST - 1) / KST;
+            p.i8_sksteps += (int64_t)((ht[i].e0 * kI8Box2 + MR - 1) / MR) * ((ht[i].count + KST - 1) / KST);
+        }
     }
     if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
         cudaMalloc(&p.svoff, sizeof(int64_t) * (p.n_istiles + 1)) != cudaSuccess ||

@@ -152,9 +152,11 @@ struct Plan {
     int64_t n_itiles = 0;
     int64_t i8_ksteps = 0;         // K-steps of one gather pass (sum over tiles)
     bool i8s = false;              // int8 tensor-core scatter (scatter_i8.cu), same node order
+    bool i8s_auto = false;         // decide i8s from the tiles' density at plan time
     Tile *istiles = nullptr;       // its 512-node tiles
     int64_t n_istiles = 0;
     int *tsv = nullptr;            // per scatter tile: value fixed-point shift
+    int64_t i8_sksteps = 0;        // int8 scatter K-steps per pass
     int64_t *svoff = nullptr;      // per scatter tile: first value-digit block (K-step)
     uint8_t *vdig = nullptr;       // value digits, 15 KB per K-step of every tile
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes

@@ -103,7 +103,8 @@ class SglPlan:
         i = self._info
         return {"n_tiles": int(i.n_tiles), "tile_nodes": int(i.tile_nodes), "tile_dmma": int(i.tile_dmma),
                 "generic": bool(i.generic), "plan_ms": float(i.plan_ms), "i8_gather": bool(i.i8_gather),
-                "i8_tiles": int(i.i8_tiles), "i8_ksteps": int(i.i8_ksteps)}
+                "i8_tiles": int(i.i8_tiles), "i8_ksteps": int(i.i8_ksteps), "i8_scatter": bool(i.i8_scatter),
+                "i8_sksteps": int(i.i8_sksteps)}
 
     def stage_ms(self, direction: str = "forward") -> dict:
         """Per-stage device ms of the last call (plan(..., profile=True))."""

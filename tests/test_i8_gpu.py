@@ -139,3 +139,18 @@ def test_edge_concentrated_sgl_spectra(sgl, B):
     f8 = sgl.forward(sgl.plan(B, pts), c)
     f64 = sgl.forward(sgl.plan(B, pts, backend="tiled"), c)
     assert rel(f8, f64) <= TOL_I8   # measured <= 2.5e-12 (tools/i8_adversarial.py)
+
+
+def test_scatter_engine_selection_and_full_size_parity(sgl):
+    # the int8 scatter is chosen automatically for large dense node sets (config 3
+    # at 1e7 nodes) and not for sparse ones; forced off by backend="tiled"
+    from paper_1809_10786_b200 import workloads
+    w = workloads.config(3, M=10_000_000)
+    p = sgl.plan(w.B, w.points, rho=w.rho)
+    assert p.stats["i8_scatter"] and p.stats["i8_sksteps"] < 0.5 * w.M
+    p64 = sgl.plan(w.B, w.points, rho=w.rho, backend="tiled")
+    assert not p64.stats["i8_scatter"]
+    a8, a64 = sgl.adjoint(p, w.values), sgl.adjoint(p64, w.values)
+    assert rel(a8, a64) <= TOL_I8, rel(a8, a64)
+    w2 = workloads.config(3, M=1_000_000)
+    assert not sgl.plan(w2.B, w2.points, rho=w2.rho).stats["i8_scatter"]
