@@ -147,7 +147,8 @@ __global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSe
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
                  double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
-                 const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2) {
+                 const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2,
+                 unsigned long long *__restrict__ prof) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SSmem &S = *reinterpret_cast<SSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -177,16 +178,23 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);    // block, SBO = 16 rows
         constexpr uint32_t MN = (1u << 15) | (1u << 16);                                // A, B MN-major
         uint32_t g = 0, mc = 0;
+        long long q0 = clock64(), qa = 0, qb = 0, qe = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
+                long long x0 = clock64();
                 if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
+                qe += clock64() - x0;
                 umma::fence_after();
                 for (int ks = 0; ks < nks; ++ks, ++g) {
                     const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
+                    long long x1 = clock64();
                     mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1);
+                    long long x2 = clock64();
                     mbar_wait(&S.fullA[stg], (g / NSTG) & 1);
+                    qa += clock64() - x2;
+                    qb += x2 - x1;
                     umma::fence_after();
                     if (umma::elect_one()) {
                         const uint64_t ad = a0 + (uint64_t)(stg * (A_STAGE >> 4));
@@ -215,6 +223,12 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 if (umma::elect_one()) umma::commit(&S.tfull);
                 __syncwarp();
             }
+        }
+        if (prof && lane == 0) {
+            prof[blockIdx.x * 4 + 0] = clock64() - q0;
+            prof[blockIdx.x * 4 + 1] = qa;
+            prof[blockIdx.x * 4 + 2] = qb;
+            prof[blockIdx.x * 4 + 3] = qe;
         }
     } else if (warp == 1) {
         // ---- value-digit producer: one bulk copy per K-step (re-read from L2 per M-block)
@@ -447,10 +461,27 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
+    static unsigned long long *prof = nullptr;
+    const bool want = getenv("SGL_I8_PROF") != nullptr;
+    if (want && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 4 * 1024);
     k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
-                                                  reinterpret_cast<double *>(grid), g2);
+                                                  reinterpret_cast<double *>(grid), g2, want ? prof : nullptr);
     SGL_CUDA_CHECK(cudaGetLastError());
+    if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)
+        std::vector<unsigned long long> h(4 * blocks);
+        cudaMemcpyAsync(h.data(), prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        double tot = 0, a = 0, b = 0, e = 0;
+        for (int64_t i = 0; i < blocks; ++i) {
+            tot += h[4 * i];
+            a += h[4 * i + 1];
+            b += h[4 * i + 2];
+            e += h[4 * i + 3];
+        }
+        fprintf(stderr, "i8 scatter MMA warp: %.0f cycles/CTA, wait weights %.1f%%, values %.1f%%, TMEM drain %.1f%%\n",
+                tot / blocks, 100 * a / tot, 100 * b / tot, 100 * e / tot);
+    }
     return SGL_OK;
 }
 
