@@ -259,17 +259,20 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             const Tile t = tiles[ti];
             gen_sync();   // the previous tile's readers of the node tables are done
             const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
-            for (int i = gt; i < t.count; i += NWG * 32) {
+            const int kcount = ksteps(t) * KST;
+            for (int i = gt; i < kcount; i += NWG * 32) {
                 // per node: axis-0 coordinate, axis-2 window and the W2 factors of
-                // the three 16-cell chunks (2 exps per chunk here, none per K-step)
-                const int64_t si = (int64_t)t.start + i;
+                // the three 16-cell chunks (2 exps per chunk here, none per K-step);
+                // the padding nodes of the last K-step get zero weights
+                const bool live = i < t.count;
+                const int64_t si = (int64_t)t.start + (live ? i : 0);
                 const double u2 = nodes.u2[si];
-                S.u0[i] = nodes.u0[si];
+                S.u0[i] = live ? nodes.u0[si] : -1e9;
                 window_cells(u2, wp.q, S.lo2[i], S.hi2[i]);
 #pragma unroll
                 for (int cc = 0; cc < CHUNKS; ++cc) {
                     const double d = u2 - (double)(kst + 16 * cc);
-                    S.e2[cc][i] = s2 * (wp.c2 * exp(-d * d * wp.h2));
+                    S.e2[cc][i] = live ? s2 * (wp.c2 * exp(-d * d * wp.h2)) : 0.0;
                     S.f2[cc][i] = exp(2.0 * wp.h2 * d);
                 }
             }
@@ -279,8 +282,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 // W0 of every node on the (<= 4) slabs of this M-block, once per block
                 const int a_mb = (mb * 8) / CHUNKS;
                 gen_sync();   // the previous block's readers of w0t are done
-                for (int i = gt; i < 4 * t.count; i += NWG * 32) {
-                    const int j = i / t.count, n = i - j * t.count, al = a_mb + j, cell0 = t.o0 + al;
+                for (int i = gt; i < 4 * kcount; i += NWG * 32) {
+                    const int j = i / kcount, n = i - j * kcount, al = a_mb + j, cell0 = t.o0 + al;
                     const double u0 = S.u0[n];
                     int lo0, hi0;
                     window_cells(u0, wp.q, lo0, hi0);
@@ -294,17 +297,16 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 gen_sync();
                 const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
                 const int cb = kst + 16 * cc;
+                // this thread's node tables for the M-block (padding nodes have e = 0)
+                const double *w0p = S.w0t[al - a_mb] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
+                const int *lo2p = S.lo2 + kl, *hi2p = S.hi2 + kl;
                 for (int ks = 0; ks < nks; ++ks, ++g) {
                     const int stg = (int)(g % NSTG);
                     const uint32_t use = g / NSTG;
-                    const int kn = ks * KST + kl;
-                    const bool live = kn < t.count;
-                    const int kk = live ? kn : 0;
+                    const int kn = ks * KST;
                     // w2(cb + j) = e f^j g_j: powers of f by a depth-4 product tree
-                    const double w0 = live ? S.w0t[al - a_mb][kk] : 0.0;
-                    const int jlo = S.lo2[kk] - cb, jhi = S.hi2[kk] - cb;
-                    const double e = live ? (cc == 0 ? S.e2[0][kk] : (cc == 1 ? S.e2[1][kk] : S.e2[2][kk])) : 0.0;
-                    const double f = cc == 0 ? S.f2[0][kk] : (cc == 1 ? S.f2[1][kk] : S.f2[2][kk]);
+                    const double w0 = w0p[kn], e = e2p[kn], f = f2p[kn];
+                    const int jlo = lo2p[kn] - cb, jhi = hi2p[kn] - cb;
                     double pw[16], w2[16];
                     pw[0] = e;
                     pw[1] = e * f;
