@@ -48,14 +48,15 @@ using namespace i8;
 constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
-constexpr int NSTG = 2;                  // weight-digit ring (K-steps of 32 nodes)
-constexpr int NSTGB = 3;                 // value-digit ring
+constexpr int NGRP = 2;                  // generator groups, alternating K-steps (group = ring stage)
+constexpr int NSTG = NGRP;               // weight-digit ring (one stage per generator group) (K-steps of 32 nodes)
+constexpr int NSTGB = 2;                 // value-digit ring
 constexpr int KST = 32;                  // nodes per K-step
 constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 4 node blocks x 8 cell blocks x 128 B (MN-major)
 constexpr int A_STAGE = ND * A_DIGIT;
 constexpr int B_KBLK = ND * (ROWS / 16) * 128;   // one 8-node block of all 6 value digits
 constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (global and smem layout)
-constexpr int NWG = 8;                   // weight generator warps (32 nodes x 8 cell groups)
+constexpr int NWG = 8 * NGRP;            // weight generator warps (per group: 32 nodes x 8 cell groups)
 constexpr int NEW = 4;
 constexpr int ST = (2 + NWG + NEW) * 32;
 
@@ -63,10 +64,11 @@ struct SSmem {
     uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
     uint8_t b[NSTGB][B_STAGE];   // value digits  [node/8][digit][col/16][node%8][col%16]
     double stage[ROWS][MR];      // epilogue: one M-block in FP64, [column][cell]
-    double u0[SN];
     double e2[CHUNKS][SN], f2[CHUNKS][SN];   // W2 of chunk cc: w(cb + j) = e2 f2^j exp(-h2 j^2)
-    int lo2[SN], hi2[SN];
-    double w0t[4][SN];           // W0 of the current M-block's (<= 4) slabs
+    int win2[SN];                // axis-2 window relative to K column 0: lo | hi << 16 (signed)
+    double w0t[4][SN];           // W0 of the current M-block's (<= 4) slabs, row = slab & 3
+    double w0s[SN], r0s[SN];     // axis-0 Gaussian walk per node: W0 of its next slab, ratio
+    int win0[SN];                // axis-0 window in tile slabs: lo | hi << 16 (signed)
     uint64_t fullA[NSTG], emptyA[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
     uint32_t tbase;
@@ -225,10 +227,10 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             }
         }
         if (prof && lane == 0) {
-            prof[blockIdx.x * 4 + 0] = clock64() - q0;
-            prof[blockIdx.x * 4 + 1] = qa;
-            prof[blockIdx.x * 4 + 2] = qb;
-            prof[blockIdx.x * 4 + 3] = qe;
+            prof[blockIdx.x * 8 + 0] = clock64() - q0;
+            prof[blockIdx.x * 8 + 1] = qa;
+            prof[blockIdx.x * 8 + 2] = qb;
+            prof[blockIdx.x * 8 + 3] = qe;
         }
     } else if (warp == 1) {
         // ---- value-digit producer: one bulk copy per K-step (re-read from L2 per M-block)
@@ -252,11 +254,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         // ---- weight-digit generators: thread = (node of the K-step, 16-cell group);
         // lanes 0-7 take 8 consecutive nodes (each 16-byte store row of a warp
         // covers all 32 banks)
-        const int gt = tid - 64, wi = gt >> 5;
+        const int gt = tid - 64, hg = gt >> 8, wi = (gt >> 5) & 7;
         const int kl = (wi & 3) * 8 + (lane & 7), grp = (wi >> 2) * 4 + (lane >> 3);
         uint32_t g = 0;
+        long long q0 = clock64(), qe = 0, qt = 0, qw = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
+            const long long x0 = clock64();
             gen_sync();   // the previous tile's readers of the node tables are done
             const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
             const int kcount = ksteps(t) * KST;
@@ -267,8 +271,18 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 const bool live = i < t.count;
                 const int64_t si = (int64_t)t.start + (live ? i : 0);
                 const double u2 = nodes.u2[si];
-                S.u0[i] = live ? nodes.u0[si] : -1e9;
-                window_cells(u2, wp.q, S.lo2[i], S.hi2[i]);
+                int lo2, hi2;
+                window_cells(u2, wp.q, lo2, hi2);
+                S.win2[i] = ((lo2 - kst) & 0xffff) | ((hi2 - kst) << 16);
+                // W0 walk from the node's first window cell: w(c + 1) = w(c) r, r <- r e^{-2 h0}
+                const double u0 = nodes.u0[si];
+                int lo0, hi0;
+                window_cells(u0, wp.q, lo0, hi0);
+                lo0 = max(lo0, t.o0);   // (the box covers the window; kept for safety)
+                const double d0 = u0 - (double)lo0;
+                S.w0s[i] = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                S.r0s[i] = exp(wp.h0 * (2.0 * d0 - 1.0));
+                S.win0[i] = live ? ((lo0 - t.o0) & 0xffff) | ((hi0 - t.o0) << 16) : (0x7fff | (-1 << 16));
 #pragma unroll
                 for (int cc = 0; cc < CHUNKS; ++cc) {
                     const double d = u2 - (double)(kst + 16 * cc);
@@ -277,36 +291,47 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 }
             }
             gen_sync();
+            qt += clock64() - x0;
             const int nmb = mblocks(t), nks = ksteps(t);
+            int nxt = 0;   // next slab of the W0 walk
             for (int mb = 0; mb < nmb; ++mb) {
-                // W0 of every node on the (<= 4) slabs of this M-block, once per block
+                const long long x1 = clock64();
+                // W0 of the slabs this M-block adds (slabs a_mb .. a_mb + 3, each
+                // computed once per tile, in order, by the walk; zero beyond e0)
                 const int a_mb = (mb * 8) / CHUNKS;
-                gen_sync();   // the previous block's readers of w0t are done
-                for (int i = gt; i < 4 * kcount; i += NWG * 32) {
-                    const int j = i / kcount, n = i - j * kcount, al = a_mb + j, cell0 = t.o0 + al;
-                    const double u0 = S.u0[n];
-                    int lo0, hi0;
-                    window_cells(u0, wp.q, lo0, hi0);
-                    double w0 = 0.0;
-                    if (al < t.e0 && cell0 >= lo0 && cell0 <= hi0) {
-                        const double d0 = u0 - (double)cell0;
-                        w0 = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                if (nxt <= a_mb + 3) {
+                    gen_sync();   // the readers of the rows being replaced are done
+                    for (int n = gt; n < kcount; n += NWG * 32) {
+                        const int wn = S.win0[n], lo = (int)(short)(wn & 0xffff), hi = wn >> 16;
+                        double w = S.w0s[n], r = S.r0s[n];
+                        for (int x = nxt; x <= a_mb + 3; ++x) {
+                            double v = 0.0;
+                            if (x >= lo && x <= hi && x < t.e0) {
+                                v = w;
+                                w *= r;
+                                r *= wp.r0_1;
+                            }
+                            S.w0t[x & 3][n] = v;
+                        }
+                        S.w0s[n] = w;
+                        S.r0s[n] = r;
                     }
-                    S.w0t[j][n] = w0;
+                    nxt = a_mb + 4;
+                    gen_sync();
                 }
-                gen_sync();
+                qw += clock64() - x1;
                 const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
-                const int cb = kst + 16 * cc;
                 // this thread's node tables for the M-block (padding nodes have e = 0)
-                const double *w0p = S.w0t[al - a_mb] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
-                const int *lo2p = S.lo2 + kl, *hi2p = S.hi2 + kl;
+                const double *w0p = S.w0t[al & 3] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
+                const int *win2p = S.win2 + kl;
                 for (int ks = 0; ks < nks; ++ks, ++g) {
+                    if ((int)(g % NGRP) != hg) continue;   // the other group's K-step
                     const int stg = (int)(g % NSTG);
                     const uint32_t use = g / NSTG;
                     const int kn = ks * KST;
                     // w2(cb + j) = e f^j g_j: powers of f by a depth-4 product tree
                     const double w0 = w0p[kn], e = e2p[kn], f = f2p[kn];
-                    const int jlo = lo2p[kn] - cb, jhi = hi2p[kn] - cb;
+                    const int wn = win2p[kn], jlo = (int)(short)(wn & 0xffff) - 16 * cc, jhi = (wn >> 16) - 16 * cc;
                     double pw[16], w2[16];
                     pw[0] = e;
                     pw[1] = e * f;
@@ -323,13 +348,21 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     for (int j = 0; j < 16; ++j) w2[j] = (j >= jlo && j <= jhi) ? pw[j] * g2[j] : 0.0;
                     uint32_t dw[ND][4];
                     digits16(w0, w2, dw);
+                    const long long x2 = clock64();
                     if (use) mbar_wait(&S.emptyA[stg], (use - 1) & 1);
-                    if (gt == 0) mbar_expect_tx(&S.fullA[stg], A_STAGE);
+                    qe += clock64() - x2;
+                    if ((gt & 255) == 0) mbar_expect_tx(&S.fullA[stg], A_STAGE);
                     uint8_t *dst = S.a[stg] + (kl >> 3) * 1024 + grp * 128 + (kl & 7) * 16;
 #pragma unroll
                     for (int p = 0; p < ND; ++p) st_async_v4(dst + p * A_DIGIT, dw[p], &S.fullA[stg]);
                 }
             }
+        }
+        if (prof && gt == 0) {
+            prof[blockIdx.x * 8 + 4] = clock64() - q0;
+            prof[blockIdx.x * 8 + 5] = qe;
+            prof[blockIdx.x * 8 + 6] = qt;
+            prof[blockIdx.x * 8 + 7] = qw;
         }
     } else {
         // ---- epilogue: thread = box cell of the M-block = TMEM lane
@@ -465,22 +498,28 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
     static unsigned long long *prof = nullptr;
     const bool want = getenv("SGL_I8_PROF") != nullptr;
-    if (want && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 4 * 1024);
+    if (want && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 8 * 1024);
     k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
                                                   reinterpret_cast<double *>(grid), g2, want ? prof : nullptr);
     SGL_CUDA_CHECK(cudaGetLastError());
     if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)
-        std::vector<unsigned long long> h(4 * blocks);
-        cudaMemcpyAsync(h.data(), prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
+        std::vector<unsigned long long> h(8 * blocks);
+        cudaMemcpyAsync(h.data(), prof, sizeof(unsigned long long) * 8 * blocks, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        double tot = 0, a = 0, b = 0, e = 0;
+        double tot = 0, a = 0, b = 0, e = 0, gt = 0, ge = 0, gtab = 0, gw0 = 0;
         for (int64_t i = 0; i < blocks; ++i) {
-            tot += h[4 * i];
-            a += h[4 * i + 1];
-            b += h[4 * i + 2];
-            e += h[4 * i + 3];
+            tot += h[8 * i];
+            a += h[8 * i + 1];
+            b += h[8 * i + 2];
+            e += h[8 * i + 3];
+            gt += h[8 * i + 4];
+            ge += h[8 * i + 5];
+            gtab += h[8 * i + 6];
+            gw0 += h[8 * i + 7];
         }
+        fprintf(stderr, "i8 scatter generator warp: %.0f cycles/CTA, wait emptyA %.1f%%, node tables %.1f%%, W0 %.1f%%\n",
+                gt / blocks, 100 * ge / gt, 100 * gtab / gt, 100 * gw0 / gt);
         fprintf(stderr, "i8 scatter MMA warp: %.0f cycles/CTA, wait weights %.1f%%, values %.1f%%, TMEM drain %.1f%%\n",
                 tot / blocks, 100 * a / tot, 100 * b / tot, 100 * e / tot);
     }
