@@ -49,7 +49,7 @@ constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
 constexpr int NGRP = 2;                  // generator groups, alternating K-steps (group = ring stage)
-constexpr int NSTG = NGRP;               // weight-digit ring (one stage per generator group) (K-steps of 32 nodes)
+constexpr int NSTG = NGRP < 2 ? 2 : NGRP;              // weight-digit ring (one stage per generator group) (K-steps of 32 nodes)
 constexpr int NSTGB = 2;                 // value-digit ring
 constexpr int KST = 32;                  // nodes per K-step
 constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 4 node blocks x 8 cell blocks x 128 B (MN-major)
@@ -57,7 +57,7 @@ constexpr int A_STAGE = ND * A_DIGIT;
 constexpr int B_KBLK = ND * (ROWS / 16) * 128;   // one 8-node block of all 6 value digits
 constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (global and smem layout)
 constexpr int NWG = 8 * NGRP;            // weight generator warps (per group: 32 nodes x 8 cell groups)
-constexpr int NEW = 4;
+constexpr int NEW = 8;                   // epilogue warps: 2 per TMEM lane quarter, half the columns each
 constexpr int ST = (2 + NWG + NEW) * 32;
 
 struct SSmem {
@@ -366,7 +366,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         }
     } else {
         // ---- epilogue: thread = box cell of the M-block = TMEM lane
-        const int quarter = warp & 3, m = quarter * 32 + lane;
+        const int quarter = warp & 3, m = quarter * 32 + lane, eh = (warp - 2 - NWG) >> 2;
         const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
         uint32_t mc = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
@@ -384,7 +384,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 mbar_wait(&S.tfull, mc & 1);
                 umma::fence_after();
 #pragma unroll 1
-                for (int cb = 0; cb < ROWS / 8; ++cb) {   // 8 columns = 4 axis-1 cells x (re, im)
+                for (int cb = eh * (ROWS / 16); cb < (eh + 1) * (ROWS / 16); ++cb) {   // 8 columns = 4 axis-1 cells x (re, im)
                     int32_t D[NBLK][8];
                     __syncwarp();   // tcgen05.ld is .sync.aligned
 #pragma unroll
@@ -398,7 +398,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
                 if (inbox) {
-                    for (int b = 0; b < t.e1; ++b) {
+                    for (int b = eh * (ROWS / 4); b < min(t.e1, (eh + 1) * (ROWS / 4)); ++b) {
                         const double re = S.stage[2 * b][m], im = S.stage[2 * b + 1][m];
                         double *q = gp + 2 * (size_t)b * wp.N2p;
                         if (re != 0.0) red_add(q, re);
