@@ -63,9 +63,25 @@ enum {
     SGL_FLAG_PROFILE = 1u << 3,           /* record per-stage CUDA-event timings    */
     SGL_FLAG_PRECISE = 1u << 4,           /* basal tables in 80-bit extended precision
                                              (precise=True, recurrences.py:13)      */
-    SGL_FLAG_FP64_WINDOW = 1u << 5        /* forward window stage on the FP64 DMMA
-                                             kernel instead of the int8 tensor-core
-                                             (digit-split) gather                   */
+    SGL_FLAG_FP64_WINDOW = 1u << 5,       /* both window stages on the FP64 DMMA
+                                             kernels instead of the int8 tensor-core
+                                             (digit-split) engines                  */
+    SGL_FLAG_I8_SCATTER = 1u << 6,        /* adjoint window stage on the int8 tensor
+                                             cores for any node set (default: only
+                                             large dense sets, chosen at plan time) */
+    SGL_FLAG_FP64_SCATTER = 1u << 7,      /* adjoint window stage on the FP64 DMMA
+                                             kernel (the int8 gather is kept)       */
+    SGL_FLAG_FULL_FFT = 1u << 8,          /* one 3-D cuFFT plan instead of the pruned
+                                             2-D + 1-D passes                      */
+    SGL_FLAG_I8_GATHER = 1u << 9,         /* sgl_nfft_plan_create only: int8 gather
+                                             (off by default on raw NFFT plans)     */
+    SGL_FLAG_SCATTER_WIDE = 1u << 10,     /* FP64 scatter tiles in the gather's W x W
+                                             pencils (default: by node density)     */
+    SGL_FLAG_SCATTER_NARROW = 1u << 11,   /* FP64 scatter tiles in W x W2 pencils   */
+    SGL_FLAG_I8_PROF = 1u << 12,          /* debug: clock64 wait counters of the int8
+                                             kernels, printed to stderr per call    */
+    SGL_FLAG_NO_GUARD = 1u << 13          /* disable the int8 accuracy guard (the
+                                             per-call switch to the FP64 kernels)   */
 };
 
 typedef struct {
@@ -94,6 +110,14 @@ typedef struct {
     int32_t i8_scatter;       /* 1 if the adjoint window stage runs on the int8
                                  tensor cores (dense node sets, or forced)     */
     int64_t i8_sksteps;       /* its K-steps (32 nodes x 128 cells) per pass   */
+    int32_t guard;            /* 1 if the int8 accuracy guard is on            */
+    double guard_ap;          /* adjoint guard: the tail's noise response (plan time) */
+    int64_t guard_fwd_fallbacks;  /* forward calls whose window stage ran on the
+                                     FP64 kernel (estimate above 1e-11, or a
+                                     non-finite grid)                          */
+    int64_t guard_adj_fallbacks;  /* adjoint calls likewise                     */
+    double guard_est_fwd;     /* last forward's digit-split error estimate     */
+    double guard_est_adj;     /* last adjoint's estimate                       */
 } sgl_plan_info;
 
 /* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */

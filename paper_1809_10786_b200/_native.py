@@ -19,6 +19,14 @@ FLAG_GENERIC_GRIDDING = 1 << 2
 FLAG_PROFILE = 1 << 3
 FLAG_PRECISE = 1 << 4
 FLAG_FP64_WINDOW = 1 << 5
+FLAG_I8_SCATTER = 1 << 6
+FLAG_FP64_SCATTER = 1 << 7
+FLAG_FULL_FFT = 1 << 8
+FLAG_I8_GATHER = 1 << 9
+FLAG_SCATTER_WIDE = 1 << 10
+FLAG_SCATTER_NARROW = 1 << 11
+FLAG_I8_PROF = 1 << 12
+FLAG_NO_GUARD = 1 << 13
 STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares
@@ -53,6 +61,12 @@ class PlanInfo(ctypes.Structure):
         ("i8_ksteps", ctypes.c_int64),
         ("i8_scatter", ctypes.c_int32),
         ("i8_sksteps", ctypes.c_int64),
+        ("guard", ctypes.c_int32),
+        ("guard_ap", ctypes.c_double),
+        ("guard_fwd_fallbacks", ctypes.c_int64),
+        ("guard_adj_fallbacks", ctypes.c_int64),
+        ("guard_est_fwd", ctypes.c_double),
+        ("guard_est_adj", ctypes.c_double),
     ]
 
 

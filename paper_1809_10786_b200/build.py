@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libsgl_b200.so")
-SOURCES = ["capi.cu", "nodes.cu", "basal.cu", "gridding.cu", "gather_i8.cu", "scatter_i8.cu", "exact.cu", "direct.cu"]
+SOURCES = ["capi.cu", "nodes.cu", "basal.cu", "gridding.cu", "gather_i8.cu", "scatter_i8.cu", "exact.cu", "direct.cu",
+           "guard.cu"]
 HEADERS = ["sgl_internal.cuh", "umma.cuh", "i8_common.cuh", os.path.join("..", "..", "include", "sgl_b200.h")]
 
 
@@ -39,26 +40,39 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [
-        nvcc(),
-        "-gencode", "arch=compute_100a,code=sm_100a",
-        "-O3", "-lineinfo", "-std=c++17",
-        "-Xcompiler", "-fPIC", "-shared",
-        "-Xptxas", "-v" if verbose else "-O3",
-        "-I", os.path.join(HERE, "..", "include"),
-        "-o", tmp,
-    ] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lcufft", "-lpthread"]
-    env = dict(os.environ)
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    base = [nvcc()]
     # /usr/bin/g++ is the host compiler with a complete toolchain in this image
     if os.path.exists("/usr/bin/g++"):
-        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    res = subprocess.run(cmd, capture_output=True, text=True, env=env)
+        base += ["-ccbin", "/usr/bin/g++"]
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+             "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+             "-I", os.path.join(HERE, "..", "include")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        res = subprocess.run(base + flags + ["-c", os.path.join(CSRC, src), "-o", obj],
+                             capture_output=True, text=True)
+        return src, obj, res
+
+    # one nvcc per translation unit, in parallel (the kernels are independent)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, obj, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed compiling {src}")
+        if verbose:
+            sys.stderr.write(res.stderr)
+    tmp = LIB + ".tmp"
+    res = subprocess.run(base + ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] +
+                         [obj for _, obj, _ in results] + ["-lcufft", "-lpthread"],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libsgl_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libsgl_b200.so")
     os.replace(tmp, LIB)
     return LIB
 

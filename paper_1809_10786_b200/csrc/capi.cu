@@ -50,7 +50,7 @@ void free_plan(Plan *p) {
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
-                    p->itiles, p->digits, p->gmax, p->istiles, p->tsv, p->svoff, p->vdig};
+                    p->itiles, p->digits, p->gmax, p->istiles, p->tsv, p->svoff, p->vdig, p->guard, p->prof};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
@@ -193,10 +193,25 @@ int forward_core(Plan &p, const double2 *c, double2 *v, cudaStream_t st, StageRe
     rc = launch_halo_fill(p, p.grid_buf, st);
     if (rc) return rc;
     mark(SGL_STAGE_WINDOW);
-    return p.i8 ? launch_gather_i8(p, p.grid_buf, v, st) : launch_gather(p, p.grid_buf, v, st);
+    // int8 gather with its accuracy guard (gated FP64 gather; guard.cu)
+    return p.i8 ? launch_gather_guarded(p, p.grid_buf, v, st) : launch_gather(p, p.grid_buf, v, st);
 }
 
-int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRec *rec) {
+// the adjoint's linear tail after the window stage: halo fold, FFT, crop +
+// deconvolution (+ basal adjoint)
+int adjoint_tail(Plan &p, double2 *c, cudaStream_t st, StageRec *rec) {
+    if (rec) rec->mark(SGL_STAGE_FFT);
+    int rc = launch_halo_fold(p, p.grid_buf, st);
+    if (rc) return rc;
+    rc = grid_fft(p, st, CUFFT_FORWARD);
+    if (rc) return rc;
+    if (rec) rec->mark(SGL_STAGE_BASAL);
+    return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
+}
+
+// may_sync: the int8 scatter's accuracy check reads its flag on the host
+// (not possible inside a CUDA-graph capture, where it is skipped)
+int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRec *rec, bool may_sync = true) {
     auto mark = [&](int s) {
         if (rec) rec->mark(s);
     };
@@ -205,18 +220,25 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
     if (p.exact) {   // direct adjoint NDFT (transform.py:404-405)
         rc = launch_exact_adjoint(p, v, p.grid_buf, st);
         if (rc) return rc;
-    } else {
-        SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-        rc = p.i8s ? launch_scatter_i8(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
-        if (rc) return rc;
-        mark(SGL_STAGE_FFT);
-        rc = launch_halo_fold(p, p.grid_buf, st);
-        if (rc) return rc;
-        rc = grid_fft(p, st, CUFFT_FORWARD);
-        if (rc) return rc;
+        mark(SGL_STAGE_BASAL);
+        return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
     }
-    mark(SGL_STAGE_BASAL);
-    return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
+    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+    rc = p.i8s ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
+    if (rc) return rc;
+    rc = adjoint_tail(p, c, st, rec);
+    if (rc || !(p.i8s && p.guard_on && may_sync && p.guard_ap > 0.0 && p.M > 0)) return rc;
+    // int8 scatter accuracy check (guard.cu): estimate from the result, rerun on FP64 above the bound
+    rc = guard_adjoint_estimate(p, v, c, st);
+    if (rc) return rc;
+    int redo = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&redo, &p.guard->adj_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (!redo) return SGL_OK;
+    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+    rc = launch_scatter(p, v, p.grid_buf, st);
+    if (rc) return rc;
+    return adjoint_tail(p, c, st, nullptr);
 }
 
 }  // namespace
@@ -303,16 +325,15 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->profile = flags & SGL_FLAG_PROFILE;
     p->precise = flags & SGL_FLAG_PRECISE;
     p->exact = exact;
+    p->flags = flags;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
     {
-        // int8 tensor-core gather unless FP64 is asked for (flag, or SGL_GATHER=fp64 for experiments)
-        const char *ge = getenv("SGL_GATHER");
-        p->i8 = !p->generic && !(flags & SGL_FLAG_FP64_WINDOW) && !(ge && !strcmp(ge, "fp64"));
-        const char *se = getenv("SGL_SCATTER");   // "i8": int8 tensor-core scatter (experimental)
-        // int8 scatter: automatic for dense node sets (see build_nodes), forced by SGL_SCATTER=i8,
-        // off with SGL_SCATTER=fp64 or backend "tiled"
-        p->i8s = p->i8 && se && !strcmp(se, "i8");
-        p->i8s_auto = p->i8 && !p->i8s && !(se && !strcmp(se, "fp64"));
+        // int8 tensor-core gather unless the FP64 kernels are asked for;
+        // int8 scatter automatic for dense node sets (see build_nodes), forced
+        // by SGL_FLAG_I8_SCATTER, off with SGL_FLAG_FP64_SCATTER / FP64_WINDOW
+        p->i8 = !p->generic && !(flags & SGL_FLAG_FP64_WINDOW);
+        p->i8s = p->i8 && (flags & SGL_FLAG_I8_SCATTER);
+        p->i8s_auto = p->i8 && !p->i8s && !(flags & SGL_FLAG_FP64_SCATTER);
     }
     p->n_axis[0] = 4 * B;
     p->n_axis[1] = p->compact ? 2 * B : 4 * B;
@@ -431,8 +452,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         // Pruned FFT when at most half the axis-0 planes carry the spectrum:
         // a batched 2-D plan and a 1-D plan sharing one work area; otherwise
         // (or if those plans fail) a single rank-d plan
-        const char *fe = getenv("SGL_FFT");
-        const bool want = rank == 3 && 2 * p->n_axis[0] <= p->grid[0] && !(fe && !strcmp(fe, "full"));
+        const bool want = rank == 3 && 2 * p->n_axis[0] <= p->grid[0] && !(p->flags & SGL_FLAG_FULL_FFT);
         if (want) {
             long long n2[2] = {p->grid[1], p->grid[2]}, e2[2] = {wp.N1p, wp.N2p};
             const long long pl = (long long)wp.N1p * wp.N2p;
@@ -478,6 +498,21 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && p->i8) rc = setup_i8(*p);
     if (rc == SGL_OK && p->i8s) rc = setup_scatter_i8(*p);
+    if (rc == SGL_OK) rc = setup_guard(*p);
+    if (rc == SGL_OK && (p->flags & SGL_FLAG_I8_PROF) && (p->i8 || p->i8s) &&
+        cudaMalloc(&p->prof, sizeof(unsigned long long) * 8 * num_sms()) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("out of device memory for the profile counters");
+        rc = SGL_ENOMEM;
+    }
+    if (rc == SGL_OK && p->i8s && p->guard_on && M > 0) {
+        // adjoint guard: response A_p of the tail to white grid noise of the
+        // spread's per-cell rms for unit-rms values (guard.cu)
+        const double cells = (double)p->grid[0] * p->grid[1] * p->grid[2];
+        rc = launch_noise_grid(*p, std::sqrt((double)M * p->guard_wmass2 / cells), st);
+        if (rc == SGL_OK) rc = adjoint_tail(*p, p->coef_buf, st, nullptr);
+        if (rc == SGL_OK) rc = read_absmax(*p, p->coef_buf, p->count, st, &p->guard_ap);
+    }
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");
         rc = SGL_ECUDA;
@@ -578,6 +613,7 @@ int sgl_nfft_plan_create(int32_t d, const int32_t *n_axis_d, int64_t M, const do
     p->q = q;
     p->profile = flags & SGL_FLAG_PROFILE;
     p->exact = exact;
+    p->flags = flags;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled || d < 3;
     {
         // The int8 gather's digit-split error (~1e-15 of the local grid scale) is
@@ -585,9 +621,9 @@ int sgl_nfft_plan_create(int32_t d, const int32_t *n_axis_d, int64_t M, const do
         // ~65 per axis at sigma = 2): harmless for SGL spectra (<= 2.5e-12 even
         // for edge-concentrated coefficients, tools/i8_adversarial.py) but 1.8e-10
         // for a white raw NFFT spectrum at q = 16.  Raw NFFT plans therefore keep
-        // the FP64 gather unless SGL_GATHER=i8 asks for it.
-        const char *ge = getenv("SGL_GATHER");
-        p->i8 = !p->generic && ge && !strcmp(ge, "i8");
+        // the FP64 gather unless SGL_FLAG_I8_GATHER asks for it (the accuracy
+        // guard then still switches a call to FP64 when its bound is exceeded).
+        p->i8 = !p->generic && (flags & SGL_FLAG_I8_GATHER);
     }
     p->count = (int64_t)n_axis[0] * n_axis[1] * n_axis[2];
     for (int ax = 0; ax < 3; ++ax) {   // nfft.py:174, 181-182 (no sigma escalation in the NFFT layer)
@@ -633,6 +669,25 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->i8_ksteps = p.i8_ksteps;
     info->i8_scatter = p.i8s ? 1 : 0;
     info->i8_sksteps = p.i8_sksteps;
+    info->guard = p.guard_on ? 1 : 0;
+    info->guard_ap = p.guard_ap;
+    info->guard_fwd_fallbacks = info->guard_adj_fallbacks = 0;
+    info->guard_est_fwd = info->guard_est_adj = 0.0;
+    if (p.guard) {   // diagnostics: a synchronous read of the device state
+        GuardState g;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(p.device);
+        if (cudaMemcpy(&g, p.guard, sizeof(g), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            info->guard_fwd_fallbacks = (int64_t)g.fwd_count;
+            info->guard_adj_fallbacks = (int64_t)g.adj_count;
+            info->guard_est_fwd = g.est_fwd;
+            info->guard_est_adj = g.est_adj;
+        } else {
+            cudaGetLastError();
+        }
+        cudaSetDevice(cur);
+    }
     return SGL_OK;
 }
 
@@ -727,7 +782,7 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
         v = p.val_buf;
     }
     double2 *c = cdev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;
-    const int rc = adjoint_core(p, v, c, st, &rec);
+    const int rc = adjoint_core(p, v, c, st, &rec, !guard.capturing);
     if (rc) return rc;
     rec.mark(SGL_STAGE_D2H);
     if (!cdev) {
@@ -786,7 +841,7 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
         SGL_CUDA_CHECK(cudaMemcpyAsync(values_out, p.val_buf, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, cs));
     if (!videv && p.M > 0) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_a, 0));
     double2 *cout = codev ? reinterpret_cast<double2 *>(coeffs_out) : p.coef_buf;
-    rc = adjoint_core(p, vin, cout, st, nullptr);
+    rc = adjoint_core(p, vin, cout, st, nullptr, !guard.capturing);
     if (rc) return rc;
     if (!codev)
         SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs_out, p.coef_buf, sizeof(double2) * p.count, cudaMemcpyDeviceToHost, st));

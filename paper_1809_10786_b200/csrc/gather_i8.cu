@@ -93,7 +93,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
     k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
                 NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
                 const int *__restrict__ gsh, const int *__restrict__ tsh, double2 *__restrict__ out,
-                unsigned long long *__restrict__ prof) {
+                unsigned long long *__restrict__ prof, const int *__restrict__ skip) {
+    if (*skip) return;   // non-finite grid: the gated FP64 gather runs instead (guard.cu)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     I8Smem &S = *reinterpret_cast<I8Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -350,13 +351,14 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
 }
 
 // per slab a: max(|Re G|, |Im G|) (bits of a non-negative double order like
-// the double); grid = (N0 slabs) x (blocks per slab)
+// the double; NaN counts as +Inf); grid = (N0 slabs) x (blocks per slab)
 __global__ void k_slab_absmax(const double2 *__restrict__ g, size_t per_slab, unsigned long long *out) {
     const double2 *s = g + (size_t)blockIdx.y * per_slab;
     double m = 0.0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slab; i += (size_t)gridDim.x * blockDim.x) {
         const double2 v = s[i];
-        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+        const double a = fmax(fabs(v.x), fabs(v.y));
+        m = (a != a) ? INFINITY : fmax(m, a);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -374,9 +376,13 @@ __global__ void k_tile_shift(const Tile *__restrict__ tiles, int64_t n, WindowPa
     tsh[i] = m;
 }
 
-__global__ void k_slab_shift(const unsigned long long *__restrict__ mx, int n, int *__restrict__ sh) {
+__global__ void k_slab_shift(const unsigned long long *__restrict__ mx, int n, int *__restrict__ sh,
+                             int *__restrict__ nonfinite) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) sh[i] = slab_shift(mx[i]);
+    if (i < n) {
+        sh[i] = slab_shift(mx[i]);
+        if (!isfinite(__longlong_as_double((long long)mx[i]))) *nonfinite = 1;   // FP64 gather propagates it
+    }
 }
 
 // Grid -> balanced byte digits: G 2^sG(a) = sum_j d_j 256^j, d_j in [-128, 127],
@@ -508,7 +514,7 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (per_slab + 8191) / 8192));
     k_slab_absmax<<<dim3(bx, p.wp.N0), 256, 0, st>>>(grid, per_slab, mx);
     SGL_CUDA_CHECK(cudaGetLastError());
-    k_slab_shift<<<(p.wp.N0 + 255) / 256, 256, 0, st>>>(mx, p.wp.N0, gsh);
+    k_slab_shift<<<(p.wp.N0 + 255) / 256, 256, 0, st>>>(mx, p.wp.N0, gsh, &p.guard->fwd);
     SGL_CUDA_CHECK(cudaGetLastError());
     k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.digits);   // P2 = column blocks
     SGL_CUDA_CHECK(cudaGetLastError());
@@ -521,14 +527,13 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     const size_t sm = sizeof(I8Smem);
     SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
-    static unsigned long long *prof = nullptr;
-    const bool want_prof = getenv("SGL_I8_PROF") != nullptr;
-    if (want_prof && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 4 * 1024);
+    unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
+    const bool want_prof = prof != nullptr;
     k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA, gsh,
-                                                  tsh, values, want_prof ? prof : nullptr);
+                                                  tsh, values, prof, &p.guard->fwd);
     if (want_prof) {
-        unsigned long long h[4 * 1024];
-        cudaMemcpyAsync(h, prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
+        std::vector<unsigned long long> h(4 * blocks);
+        cudaMemcpyAsync(h.data(), prof, sizeof(unsigned long long) * 4 * blocks, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         double tot = 0, a = 0, b = 0, e = 0, mn = 1e300, mx = 0;
         for (int i = 0; i < blocks; ++i) {

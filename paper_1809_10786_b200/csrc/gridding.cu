@@ -195,7 +195,9 @@ __device__ __forceinline__ void gather_slab(const double *sl, const double (&afr
 template <int NT>   // fragment tiles per slab axis: ceil(box / 4) of the plan's widest tile (9 at q = 16)
 __global__ void __launch_bounds__(GT, GCPS)
     k_gather_tiled(const __grid_constant__ CUtensorMap tmap, const Tile *__restrict__ tiles, int64_t ntiles,
-                   NodeSet nodes, WindowParams wp, double2 *__restrict__ out) {
+                   NodeSet nodes, WindowParams wp, double2 *__restrict__ out, const int *__restrict__ gate) {
+    // gated launch (accuracy guard of the int8 gather): nothing to do unless raised
+    if (gate && *gate == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     GatherSmem &S = *reinterpret_cast<GatherSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -432,7 +434,8 @@ __device__ __forceinline__ void scatter_group_any(int nct, int g, const ScatterS
 
 __global__ void __launch_bounds__(STH, 2)
     k_scatter_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
-                    const double2 *__restrict__ values, double *__restrict__ grid) {
+                    const double2 *__restrict__ values, double *__restrict__ grid, const int *__restrict__ gate) {
+    if (gate && *gate == 0) return;   // gated launch (fallback of the int8 scatter)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -705,29 +708,35 @@ namespace {
 
 namespace {
 template <int NT>
-cudaError_t launch_gather_nt(const Plan &p, double2 *values, unsigned blocks, cudaStream_t st) {
+cudaError_t launch_gather_nt(const Plan &p, double2 *values, unsigned blocks, const int *gate, cudaStream_t st) {
     const size_t sm = sizeof(GatherSmem);
     cudaError_t e = cudaFuncSetAttribute(k_gather_tiled<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_gather_tiled<NT><<<blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values);
+    k_gather_tiled<NT><<<blocks, GT, sm, st>>>(p.tmap, p.tiles, p.n_tiles, p.nodes, p.wp, values, gate);
     return cudaGetLastError();
 }
 }  // namespace
 
+int launch_gather_tiled_gated(const Plan &p, double2 *values, const int *gate, cudaStream_t st) {
+    if (p.M == 0 || p.generic) return SGL_OK;
+    int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * GCPS);
+    if (blocks < 1) blocks = 1;
+    switch (std::max(3, std::min(NTMAX, (p.tile_box + 3) / 4))) {
+    case 3: SGL_CUDA_CHECK(launch_gather_nt<3>(p, values, (unsigned)blocks, gate, st)); break;
+    case 4: SGL_CUDA_CHECK(launch_gather_nt<4>(p, values, (unsigned)blocks, gate, st)); break;
+    case 5: SGL_CUDA_CHECK(launch_gather_nt<5>(p, values, (unsigned)blocks, gate, st)); break;
+    case 6: SGL_CUDA_CHECK(launch_gather_nt<6>(p, values, (unsigned)blocks, gate, st)); break;
+    case 7: SGL_CUDA_CHECK(launch_gather_nt<7>(p, values, (unsigned)blocks, gate, st)); break;
+    case 8: SGL_CUDA_CHECK(launch_gather_nt<8>(p, values, (unsigned)blocks, gate, st)); break;
+    default: SGL_CUDA_CHECK(launch_gather_nt<NTMAX>(p, values, (unsigned)blocks, gate, st)); break;
+    }
+    return SGL_OK;
+}
+
 int launch_gather(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st) {
     if (p.M == 0) return SGL_OK;
     if (!p.generic) {
-        int64_t blocks = std::min<int64_t>(p.n_tiles, (int64_t)num_sms() * GCPS);
-        if (blocks < 1) blocks = 1;
-        switch (std::max(3, std::min(NTMAX, (p.tile_box + 3) / 4))) {
-        case 3: SGL_CUDA_CHECK(launch_gather_nt<3>(p, values, (unsigned)blocks, st)); break;
-        case 4: SGL_CUDA_CHECK(launch_gather_nt<4>(p, values, (unsigned)blocks, st)); break;
-        case 5: SGL_CUDA_CHECK(launch_gather_nt<5>(p, values, (unsigned)blocks, st)); break;
-        case 6: SGL_CUDA_CHECK(launch_gather_nt<6>(p, values, (unsigned)blocks, st)); break;
-        case 7: SGL_CUDA_CHECK(launch_gather_nt<7>(p, values, (unsigned)blocks, st)); break;
-        case 8: SGL_CUDA_CHECK(launch_gather_nt<8>(p, values, (unsigned)blocks, st)); break;
-        default: SGL_CUDA_CHECK(launch_gather_nt<NTMAX>(p, values, (unsigned)blocks, st)); break;
-        }
+        return launch_gather_tiled_gated(p, values, nullptr, st);
     } else {
         const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -788,15 +797,23 @@ int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st) {
     return SGL_OK;
 }
 
+int launch_scatter_tiled_gated(const Plan &p, const double2 *values, double2 *grid, const int *gate,
+                               cudaStream_t st) {
+    if (p.M == 0 || p.generic) return SGL_OK;
+    const size_t sm = sizeof(ScatterSmem);
+    SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int64_t blocks = std::min<int64_t>(p.n_stiles, (int64_t)num_sms() * 2 * 8);
+    if (blocks < 1) blocks = 1;
+    k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.snodes, p.wp, values,
+                                                      reinterpret_cast<double *>(grid), gate);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
 int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st) {
     if (p.M == 0) return SGL_OK;
     if (!p.generic) {
-        const size_t sm = sizeof(ScatterSmem);
-        SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        int64_t blocks = std::min<int64_t>(p.n_stiles, (int64_t)num_sms() * 2 * 8);
-        if (blocks < 1) blocks = 1;
-        k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.snodes, p.wp, values,
-                                                          reinterpret_cast<double *>(grid));
+        return launch_scatter_tiled_gated(p, values, grid, nullptr, st);
     } else {
         const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

@@ -423,10 +423,9 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     if (W2 < 1) W2 += 8;
     const double cells = (double)p.grid[0] * p.grid[1] * p.grid[2] / 4.0;   // nodes fill axes 0-1 up to pi
     const double per_row = (double)M / cells * W * W2;                        // nodes per lo0 row of a pencil
-    const char *force = getenv("SGL_SCATTER_PENCIL");                        // "wide" / "narrow": experiments
     bool narrow = W2 != W && per_row >= 1.5;   // crossover measured on the config-3 shape (r01)
-    if (force && !strcmp(force, "wide")) narrow = false;
-    if (force && !strcmp(force, "narrow")) narrow = W2 != W;
+    if (p.flags & SGL_FLAG_SCATTER_WIDE) narrow = false;   // experiments
+    if (p.flags & SGL_FLAG_SCATTER_NARROW) narrow = W2 != W;
     const TileGeom stg{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max};
     if (narrow) {
         rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W2, stg, p.snodes, &p.stiles, &p.n_stiles, true, st);

@@ -107,7 +107,8 @@ __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1
 // (node of the K-step, 16-column group = 8 axis-1 cells x re|im)
 __global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
                           const double2 *__restrict__ values, const int *__restrict__ tsv,
-                          const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig) {
+                          const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig, const int *__restrict__ skip) {
+    if (*skip) return;   // non-finite values: the gated FP64 scatter runs instead (guard.cu)
     const int kl = threadIdx.x & 31, vg = threadIdx.x >> 5;   // 5 warps = 5 column groups
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         const Tile t = tiles[ti];
@@ -150,7 +151,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
                  double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
                  const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2,
-                 unsigned long long *__restrict__ prof) {
+                 unsigned long long *__restrict__ prof, const int *__restrict__ skip) {
+    if (*skip) return;   // non-finite values (guard.cu)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SSmem &S = *reinterpret_cast<SSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -420,14 +422,16 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
 
 // per tile: value scale from the tile's max |Re v|, |Im v| (|w1 v| 2^sV < 2^46, w1 <= c1)
 __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet nodes,
-                              const double2 *__restrict__ values, double c1, int *__restrict__ tsv) {
+                              const double2 *__restrict__ values, double c1, int *__restrict__ tsv,
+                              int *__restrict__ nonfinite) {
     const int64_t ti = blockIdx.x;
     if (ti >= n) return;
     const Tile t = tiles[ti];
     double m = 0.0;
     for (int i = threadIdx.x; i < t.count; i += blockDim.x) {
         const double2 v = values[nodes.perm[(int64_t)t.start + i]];
-        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+        const double a = fmax(fabs(v.x), fabs(v.y));
+        m = (a != a) ? INFINITY : fmax(m, a);   // NaN counts as +Inf
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -440,6 +444,7 @@ __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet
         int ex;
         frexp(m, &ex);
         tsv[ti] = (m > 0.0 && isfinite(m)) ? 46 - ex : NOSLAB;
+        if (!isfinite(m)) *nonfinite = 1;   // the FP64 scatter propagates NaN / Inf (guard.cu)
     }
 }
 
@@ -470,12 +475,25 @@ int setup_scatter_i8(Plan &p) {
             p.i8_sksteps += (int64_t)((ht[i].e0 * kI8Box2 + MR - 1) / MR) * ((ht[i].count + KST - 1) / KST);
         }
     }
-    if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
+    // the digit buffer must leave room for the calls' own staging (val_buf2, cuFFT work):
+    // keep 2 GB free, else stay on the FP64 scatter (which needs none)
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (size_t)std::max<int64_t>(1, off[p.n_istiles]) * B_STAGE;
+    if (need + (size_t(2) << 30) > fr || cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
         cudaMalloc(&p.svoff, sizeof(int64_t) * (p.n_istiles + 1)) != cudaSuccess ||
-        cudaMalloc(&p.vdig, (size_t)std::max<int64_t>(1, off[p.n_istiles]) * B_STAGE) != cudaSuccess) {
+        cudaMalloc(&p.vdig, need) != cudaSuccess) {
         cudaGetLastError();
-        set_error("out of device memory for the int8 scatter digits");
-        return SGL_ENOMEM;
+        for (void *b : {(void *)p.tsv, (void *)p.svoff, (void *)p.vdig, (void *)p.istiles})
+            if (b) cudaFree(b);
+        p.tsv = nullptr;
+        p.svoff = nullptr;
+        p.vdig = nullptr;
+        p.istiles = nullptr;
+        p.n_istiles = 0;
+        p.i8_sksteps = 0;
+        p.i8s = false;   // FP64 scatter (as setup_i8 does for the gather)
+        return SGL_OK;
     }
     SGL_CUDA_CHECK(cudaMemcpy(p.svoff, off.data(), sizeof(int64_t) * (p.n_istiles + 1), cudaMemcpyHostToDevice));
     return SGL_OK;
@@ -483,11 +501,13 @@ int setup_scatter_i8(Plan &p) {
 
 int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st) {
     if (p.M == 0 || p.n_istiles == 0) return SGL_OK;
-    k_tile_vscale<<<(unsigned)p.n_istiles, 256, 0, st>>>(p.istiles, p.n_istiles, p.inodes, values, p.wp.c1, p.tsv);
+    int *skip = &p.guard->adj;
+    k_tile_vscale<<<(unsigned)p.n_istiles, 256, 0, st>>>(p.istiles, p.n_istiles, p.inodes, values, p.wp.c1, p.tsv,
+                                                         skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int sms = num_sms();
     k_vdigits<<<(unsigned)std::min<int64_t>(p.n_istiles, (int64_t)sms * 12), (ROWS / 16) * 32, 0, st>>>(
-        p.istiles, p.n_istiles, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig);
+        p.istiles, p.n_istiles, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig, skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
     const int sA = 46 - e, a0 = sA / 2;
@@ -496,12 +516,11 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
-    static unsigned long long *prof = nullptr;
-    const bool want = getenv("SGL_I8_PROF") != nullptr;
-    if (want && !prof) cudaMalloc(&prof, sizeof(unsigned long long) * 8 * 1024);
+    unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
+    const bool want = prof != nullptr;
     k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
-                                                  reinterpret_cast<double *>(grid), g2, want ? prof : nullptr);
+                                                  reinterpret_cast<double *>(grid), g2, prof, skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)
         std::vector<unsigned long long> h(8 * blocks);

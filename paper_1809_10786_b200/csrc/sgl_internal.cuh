@@ -84,7 +84,22 @@ struct StageTimer {
     bool ready = false;
 };
 
+// Per-plan device state of the int8 accuracy guard (guard.cu): per call, the
+// int8 window kernels raise `fwd` / `adj` when their input is non-finite or
+// the digit-split error estimate exceeds the bound; the gated FP64 kernel then
+// recomputes the stage (it returns at once when the flag is clear).
+struct GuardState {
+    int fwd, adj;                       // this call: 1 = the gated FP64 kernel recomputes the stage
+    int adj_redo, pad_;                 // adjoint estimate above the bound: rerun on the FP64 scatter
+    unsigned long long fwd_count, adj_count;   // calls that fell back (diagnostics)
+    unsigned long long outmax;          // bits of max |Re|, |Im| of the int8 gather output
+    double vsumsq;                      // sum |v|^2 of the adjoint input
+    unsigned long long amax;            // bits of max |Re|, |Im| of the adjoint output
+    double est_fwd, est_adj;            // last estimates (relative to the output's max)
+};
+
 struct Plan {
+    uint32_t flags = 0;
     int B = 0;
     int64_t M = 0;
     double rho = 0;
@@ -164,6 +179,14 @@ struct Plan {
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
     alignas(64) CUtensorMap dmap;  // TMA descriptor of the digit planes
 
+    // int8 accuracy guard and debug counters (guard.cu)
+    GuardState *guard = nullptr;   // device
+    bool guard_on = false;
+    double guard_wmass = 0.0;      // max window L1 mass sum |w0 w1 w2| over a node's taps
+    double guard_wmass2 = 0.0;     // max sum of squared tap weights of a node
+    double guard_ap = 0.0;         // adjoint tail's response to the spread noise model (plan time)
+    unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
+
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
 
@@ -215,6 +238,15 @@ int launch_halo_fold(const Plan &p, double2 *grid, cudaStream_t st);
 int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
 int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
 int setup_scatter_i8(Plan &p);
+int setup_guard(Plan &p);
+int launch_gather_guarded(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
+int launch_noise_grid(const Plan &p, double rms, cudaStream_t st);
+int read_absmax(const Plan &p, const double2 *v, int64_t n, cudaStream_t st, double *out);
+int guard_adjoint_estimate(const Plan &p, const double2 *values, const double2 *coeffs, cudaStream_t st);
+int launch_scatter_guarded(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
+int launch_gather_tiled_gated(const Plan &p, double2 *values, const int *gate, cudaStream_t st);
+int launch_scatter_tiled_gated(const Plan &p, const double2 *values, double2 *grid, const int *gate,
+                               cudaStream_t st);
 int setup_i8(Plan &p);
 int num_sms();
 

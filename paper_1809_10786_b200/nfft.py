@@ -27,7 +27,7 @@ import numpy as np
 from . import _native
 from .transform import _is_torch, _stream_ptr, _torch
 
-_BACKENDS = ("auto", "tiled", "generic", "numba", "numpy")
+_BACKENDS = ("auto", "tiled", "generic", "i8", "numba", "numpy")
 
 
 def _as_axes(value, d: int, name: str) -> tuple:
@@ -69,6 +69,15 @@ class NfftPlan:
         return [np.exp(2 * self.lam[j] * (np.pi * (np.arange(n) - n // 2) / self.grid_shape[j]) ** 2)
                 for j, n in enumerate(self.n_axis)]
 
+    @property
+    def guard(self) -> dict:
+        """Accuracy-guard diagnostics of the int8 gather (backend="i8")."""
+        i = _native.PlanInfo()
+        _native.check(_native.lib().sgl_plan_get_info(self._handle, ctypes.byref(i)))
+        return {"on": bool(i.guard), "fwd_fallbacks": int(i.guard_fwd_fallbacks),
+                "adj_fallbacks": int(i.guard_adj_fallbacks), "est_fwd": float(i.guard_est_fwd),
+                "est_adj": float(i.guard_est_adj)}
+
     def close(self) -> None:
         if self._handle:
             _native.lib().sgl_plan_destroy(self._handle)
@@ -89,7 +98,9 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
     one per axis.  ``backend``:
     "auto" / "tiled" (FP64 DMMA kernels for d = 3, q <= 16; the int8 gather
     of SGL plans is not used here: a white NFFT spectrum amplifies its
-    digit-split error to ~1e-10), "generic" (per-node kernels); the reference
+    digit-split error to ~1e-10), "generic" (per-node kernels), "i8" (the int8
+    gather, kept correct by the accuracy guard: a call whose error estimate
+    exceeds 1e-11 is recomputed on the FP64 gather); the reference
     names "numba" / "numpy" are accepted as "auto".  ``precompute`` is accepted; windows are evaluated
     on the fly on the device.  ``exact=True`` plans the direct NDFT."""
     _check_d(d)
@@ -123,6 +134,8 @@ def nfft_plan(d: int, n_axis, sigma, q: int, nodes, precompute: bool = True, bac
         flags |= _native.FLAG_EXACT_LAST_STAGE
     if backend == "generic":
         flags |= _native.FLAG_GENERIC_GRIDDING
+    if backend == "i8":
+        flags |= _native.FLAG_I8_GATHER
     n_arr = (ctypes.c_int32 * d)(*n_axis)
     s_arr = (ctypes.c_int32 * d)(*sig)
     h = ctypes.c_void_p(0)

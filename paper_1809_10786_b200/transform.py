@@ -17,7 +17,7 @@ import numpy as np
 from . import _native
 from .generate import coeff_count
 
-_BACKENDS = ("auto", "tiled", "generic", "numba", "numpy")
+_BACKENDS = ("auto", "tiled", "generic", "i8", "numba", "numpy")
 
 
 def _is_torch(x) -> bool:
@@ -69,6 +69,7 @@ class SglPlan:
     _info: _native.PlanInfo = field(repr=False)
     backend: str = "auto"
     precise_tables: bool = False
+    flags: int = 0
     _twin: object = field(default=None, repr=False)   # extended-precision twin for precise=True calls
 
     @property
@@ -104,7 +105,16 @@ class SglPlan:
         return {"n_tiles": int(i.n_tiles), "tile_nodes": int(i.tile_nodes), "tile_dmma": int(i.tile_dmma),
                 "generic": bool(i.generic), "plan_ms": float(i.plan_ms), "i8_gather": bool(i.i8_gather),
                 "i8_tiles": int(i.i8_tiles), "i8_ksteps": int(i.i8_ksteps), "i8_scatter": bool(i.i8_scatter),
-                "i8_sksteps": int(i.i8_sksteps)}
+                "i8_sksteps": int(i.i8_sksteps), "guard": bool(i.guard), "guard_ap": float(i.guard_ap)}
+
+    @property
+    def guard(self) -> dict:
+        """Accuracy-guard diagnostics of the int8 engines (reads device state)."""
+        i = _native.PlanInfo()
+        _native.check(_native.lib().sgl_plan_get_info(self._handle, ctypes.byref(i)))
+        return {"on": bool(i.guard), "fwd_fallbacks": int(i.guard_fwd_fallbacks),
+                "adj_fallbacks": int(i.guard_adj_fallbacks), "est_fwd": float(i.guard_est_fwd),
+                "est_adj": float(i.guard_est_adj), "adj_response": float(i.guard_ap)}
 
     def stage_ms(self, direction: str = "forward") -> dict:
         """Per-stage device ms of the last call (plan(..., profile=True))."""
@@ -136,13 +146,18 @@ def _stream_ptr(x) -> int | None:
 def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
          exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
          precompute: bool = True, device: int | None = None, profile: bool = False,
-         precise_tables: bool = False) -> SglPlan:
+         precise_tables: bool = False, flags: int = 0) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
     ``backend``: "auto" (q <= 16: the int8 tensor-core gather for the
     forward window stage (FP64 results by digit split) and the tiled FP64 DMMA
     scatter; per-node kernels otherwise), "tiled" (FP64 DMMA kernels in both
-    directions), "generic" (per-node kernels).  The reference names
+    directions), "generic" (per-node kernels), "i8" (int8 tensor-core engines
+    in both directions for any node set; "auto" takes the int8 scatter only for
+    large dense node sets).  Every int8 call is covered by the accuracy guard
+    (csrc/guard.cu): a call whose digit-split error estimate exceeds 1e-11, or
+    whose input is not finite, is recomputed on the FP64 kernels.  ``flags``
+    adds raw `SGL_FLAG_*` bits of the C ABI (experiments).  The reference names
     "numba" / "numpy" are accepted as aliases of "auto".  ``precompute`` is
     accepted for compatibility: window weights are always evaluated on the
     fly on the device.  ``exact_last_stage=True`` replaces the window
@@ -150,7 +165,7 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     if B < 1:
         raise ValueError("bandwidth must be >= 1")
     if backend not in _BACKENDS:
-        raise ValueError("backend must be 'auto', 'tiled', 'generic', 'numba' or 'numpy'")
+        raise ValueError("backend must be 'auto', 'tiled', 'generic', 'i8', 'numba' or 'numpy'")
     torch_in = _is_torch(points)
     if torch_in:
         torch = _torch()
@@ -180,7 +195,9 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     L = _native.lib()
     if dev is not None:
         _native.check(L.sgl_set_device(int(dev)))
-    flags = 0
+    flags = int(flags)
+    if backend == "i8":
+        flags |= _native.FLAG_I8_SCATTER
     if exact_last_stage:
         flags |= _native.FLAG_EXACT_LAST_STAGE
     if compact_k1:
@@ -206,7 +223,7 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
                    exact=bool(exact_last_stage),
                    compact_k1=bool(compact_k1), points=points, n_axis=tuple(info.n_axis), nfft=nf,
                    device=int(dev) if dev is not None else 0, _handle=h.value, _info=info, backend=backend,
-                   precise_tables=bool(precise_tables))
+                   precise_tables=bool(precise_tables), flags=int(flags))
 
 
 def _for_call(p: SglPlan, precise: bool) -> SglPlan:
@@ -218,7 +235,7 @@ def _for_call(p: SglPlan, precise: bool) -> SglPlan:
     if p._twin is None:
         p._twin = plan(p.B, p.points, sigma=p.sigma, q=p.q if not p.exact else 16, rho=p.rho,
                        exact_last_stage=p.exact, compact_k1=p.compact_k1, backend=p.backend, device=p.device,
-                       precise_tables=True)
+                       precise_tables=True, flags=p.flags)
     return p._twin
 
 

@@ -167,6 +167,74 @@ def cfg_cases(ref, skip_big):
     return out
 
 
+def scale_cases(ref):
+    """Round-2 parity subsets at the sizes SURVEY 8(d) asks for: config 3 on a
+    20k-node subset (forward + adjoint), config 2 on a 20k-node subset, and
+    config 5 with ALL 64 vectors on a 2k-node subset plus 4 vectors on a
+    20k-node subset.  rho is pinned to the full node set's.  Coefficients of
+    configs 3 and 5 are not stored (39 MB for config 5): the tests regenerate
+    them with the package's restated generators and check them against the
+    stored fingerprints (`c_head`, `c_sum`) first."""
+    from sglnufft.generate import cartesian_to_spherical
+    out = {}
+    # config 3: B=64, c / n, ball radius 16, M = 1e7 -> 20k-node subset
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 64
+    c = ref.gen_coeffs(B, rng) / ref.indexing.mu_to_nlm_array(B)[:, 0]
+    Mf = 10_000_000
+    full = ref.gen_points_ball(Mf, 16.0, rng)
+    vfull = _vals(rng, Mf)
+    rho = float(np.max(full[:, 0]))
+    sel = np.sort(np.random.Generator(np.random.PCG64(2)).choice(Mf, 20_000, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    out["cfg3_sub20k"] = dict(B=B, q=16, compact=False, points=full[sel], values=vfull[sel], rho=rho, sel=sel,
+                              c_head=c[:64], c_sum=np.array([c.sum(), np.abs(c).sum()]),
+                              fwd=ref.forward(p, c), adj=ref.adjoint(p, vfull[sel]))
+    print(f"cfg3_sub20k {time.time() - t:.1f}s", flush=True)
+    del full, vfull
+
+    # config 2: B=32, gen_grid(100, 4.0) -> 20k-node subset
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 32
+    c = ref.gen_coeffs(B, rng)
+    full = ref.gen_grid(100, 4.0)
+    vfull = _vals(rng, full.shape[0])
+    rho = float(np.max(full[:, 0]))
+    sel = np.sort(np.random.Generator(np.random.PCG64(2)).choice(full.shape[0], 20_000, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    out["cfg2_sub20k"] = dict(B=B, q=16, compact=False, points=full[sel], coeffs=c, values=vfull[sel], rho=rho,
+                              sel=sel, fwd=ref.forward(p, c), adj=ref.adjoint(p, vfull[sel]))
+    print(f"cfg2_sub20k {time.time() - t:.1f}s", flush=True)
+
+    # config 5: B=48, 64 vectors, 2e6 N(0, I/2) nodes: all 64 vectors on 2k
+    # nodes, vectors 0, 21, 42, 63 on 20k nodes
+    rng = np.random.Generator(np.random.PCG64(0))
+    B = 48
+    cs = np.stack([ref.gen_coeffs(B, rng) for _ in range(64)])
+    Mf = 2_000_000
+    full = cartesian_to_spherical(rng.normal(0.0, np.sqrt(0.5), (Mf, 3)))
+    rho = float(np.max(full[:, 0]))
+    fp = dict(c_head=cs[:, :16], c_sum=np.stack([cs.sum(axis=1), np.abs(cs).sum(axis=1)], axis=1))
+    sel = np.sort(np.random.Generator(np.random.PCG64(2)).choice(Mf, 2_000, replace=False))
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    fw = np.stack([ref.forward(p, cs[k]) for k in range(64)])
+    out["cfg5_sub2k_all64"] = dict(B=B, q=16, compact=False, points=full[sel], rho=rho, sel=sel, fwd=fw,
+                                   vectors=np.arange(64), **fp)
+    print(f"cfg5_sub2k_all64 {time.time() - t:.1f}s", flush=True)
+    sel = np.sort(np.random.Generator(np.random.PCG64(3)).choice(Mf, 20_000, replace=False))
+    vec = np.array([0, 21, 42, 63])
+    t = time.time()
+    p = ref.plan(B, full[sel], rho=rho)
+    fw = np.stack([ref.forward(p, cs[k]) for k in vec])
+    out["cfg5_sub20k_4v"] = dict(B=B, q=16, compact=False, points=full[sel], rho=rho, sel=sel, fwd=fw,
+                                 vectors=vec, **fp)
+    print(f"cfg5_sub20k_4v {time.time() - t:.1f}s", flush=True)
+    return out
+
+
 def invert_cases(ref):
     """The CG inverse (solvers.py:204-277) on small systems: CGNR and CGNE."""
     out = {}
@@ -326,6 +394,8 @@ def main():
         cases.update(small_cases(ref))
     if args.only in ("", "cfg"):
         cases.update(cfg_cases(ref, args.skip_big))
+    if args.only in ("", "scale"):
+        cases.update(scale_cases(ref))
     if args.only in ("", "invert"):
         cases.update(invert_cases(ref))
     if args.only in ("", "direct"):

@@ -1,0 +1,153 @@
+"""The accuracy guard of the int8 window engines (csrc/guard.cu) and their
+handling of non-finite input.
+
+Per call the guard estimates the digit-split error relative to the output's
+maximum and recomputes the window stage on the FP64 DMMA kernels when the
+estimate exceeds 1e-11, or when the input is not finite (the int8 split
+would map NaN / Inf to zero weights; the reference's FP64 loops,
+_gridding.py:53-95, propagate them).  Adversarial families: white raw-NFFT
+spectra, spectra pre-multiplied by the inverse deconvolution (energy at the
+spectral edge, nfft.py:183-186), single SGL coefficients at the (n, l, m)
+corners.  Whatever the family, the default path stays within the 1e-10 bar
+of the FP64 kernels, and a call that stayed on int8 is within its estimate.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x), np.asarray(ref)
+    return float(np.max(np.abs(x - ref)) / np.max(np.abs(ref)))
+
+
+@pytest.fixture(scope="module")
+def sgl():
+    import paper_1809_10786_b200 as m
+    return m
+
+
+def _same_nonfinite(a, b):
+    return np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(np.isinf(a), np.isinf(b))
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_nonfinite_coefficients_propagate(sgl, bad):
+    rng = np.random.default_rng(1)
+    pts = sgl.gen_points_ball(3000, 3.0, rng)
+    c = sgl.gen_coeffs(12, rng)
+    c[7] = bad
+    p8, p64 = sgl.plan(12, pts), sgl.plan(12, pts, backend="tiled")
+    assert p8.stats["i8_gather"]
+    f8, f64 = sgl.forward(p8, c), sgl.forward(p64, c)
+    assert not np.all(np.isfinite(f64))
+    assert _same_nonfinite(f8, f64)
+    assert p8.guard["fwd_fallbacks"] == 1
+    # a finite call afterwards is back on the int8 engine
+    c[7] = 0.5
+    sgl.forward(p8, c)
+    assert p8.guard["fwd_fallbacks"] == 1
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_nonfinite_values_propagate(sgl, bad):
+    rng = np.random.default_rng(2)
+    pts = sgl.gen_points_ball(4000, 4.0, rng)
+    v = rng.uniform(-1, 1, 4000) + 1j * rng.uniform(-1, 1, 4000)
+    v[123] = bad
+    p8, p64 = sgl.plan(16, pts, backend="i8"), sgl.plan(16, pts, backend="tiled")
+    a8, a64 = sgl.adjoint(p8, v), sgl.adjoint(p64, v)
+    assert not np.all(np.isfinite(a64))
+    assert _same_nonfinite(a8, a64)
+    assert p8.guard["adj_fallbacks"] >= 1
+
+
+def test_white_nfft_spectrum_is_guarded(sgl):
+    """A white raw-NFFT spectrum at q = 16 amplifies the digit-split error to
+    ~1e-10 through the deconvolution gain (DESIGN 5a): the guard must see it
+    and recompute on FP64."""
+    rng = np.random.default_rng(3)
+    n = (32, 32, 32)
+    nodes = rng.uniform(0, 2 * np.pi, (20000, 3))
+    f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    p8 = sgl.nfft_plan(3, n, 2, 16, nodes, backend="i8")
+    p64 = sgl.nfft_plan(3, n, 2, 16, nodes)
+    assert p8.backend == "i8"
+    out8, out64 = sgl.nfft_execute(p8, f), sgl.nfft_execute(p64, f)
+    assert rel(out8, out64) <= TOL
+    g = p8.guard
+    assert g["est_fwd"] > 1e-11 and g["fwd_fallbacks"] == 1, g
+
+
+@pytest.mark.parametrize("shape", ["deconv_edge", "corner"])
+def test_edge_spectra_within_bar(sgl, shape):
+    rng = np.random.default_rng(4)
+    n = (32, 32, 16)
+    nodes = rng.uniform(0, 2 * np.pi, (20000, 3))
+    p8 = sgl.nfft_plan(3, n, 2, 16, nodes, backend="i8")
+    p64 = sgl.nfft_plan(3, n, 2, 16, nodes)
+    f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    if shape == "deconv_edge":
+        for ax, d in enumerate(p64.deconv):   # pre-multiplied by the inverse deconvolution
+            f = f * np.expand_dims(d, tuple(a for a in range(3) if a != ax))
+    else:
+        f = np.zeros(n, complex)
+        f[0, 0, 0] = 1.0   # the corner frequency (-n/2, -n/2, -n/2)
+    out8, out64 = sgl.nfft_execute(p8, f), sgl.nfft_execute(p64, f)
+    e = rel(out8, out64)
+    g = p8.guard
+    assert e <= TOL, (e, g)
+    if g["fwd_fallbacks"] == 0:
+        assert e <= g["est_fwd"], (e, g)
+
+
+@pytest.mark.parametrize("B", [8, 16, 24])
+def test_single_sgl_coefficients_at_the_corners(sgl, B):
+    from paper_1809_10786_b200 import indexing
+    rng = np.random.default_rng(40 + B)
+    pts = sgl.gen_points_ball(5000, 2.0 + B / 8, rng)
+    p8, p64 = sgl.plan(B, pts), sgl.plan(B, pts, backend="tiled")
+    for n, l, m in [(B, B - 1, B - 1), (B, B - 1, -(B - 1)), (B, 0, 0), (1, 0, 0), (B, B - 1, 0)]:
+        c = np.zeros(p8.count, complex)
+        c[indexing.nlm_to_mu(n, l, m)] = 1.0
+        f8, f64 = sgl.forward(p8, c), sgl.forward(p64, c)
+        e = rel(f8, f64)
+        g = p8.guard
+        assert e <= TOL, ((n, l, m), e, g)
+        if e > 0 and g["est_fwd"] <= 1e-11:
+            assert e <= g["est_fwd"], ((n, l, m), e, g)
+
+
+def test_adjoint_estimate_bounds_the_int8_scatter(sgl):
+    rng = np.random.default_rng(5)
+    pts = sgl.gen_points_ball(20000, 4.0, rng)
+    p8, p64 = sgl.plan(16, pts, backend="i8"), sgl.plan(16, pts, backend="tiled")
+    assert p8.stats["guard_ap"] > 0
+    for kind in ("uniform", "sparse", "smooth"):
+        if kind == "uniform":
+            v = rng.uniform(-1, 1, 20000) + 1j * rng.uniform(-1, 1, 20000)
+        elif kind == "sparse":
+            v = np.zeros(20000, complex)
+            v[rng.choice(20000, 5)] = 1.0
+        else:
+            v = np.exp(-pts[:, 0] ** 2).astype(complex)
+        a8, a64 = sgl.adjoint(p8, v), sgl.adjoint(p64, v)
+        e = rel(a8, a64)
+        g = p8.guard
+        assert e <= TOL, (kind, e, g)
+        if g["est_adj"] <= 1e-11:
+            assert e <= g["est_adj"], (kind, e, g)
+
+
+def test_guard_off_flag(sgl):
+    from paper_1809_10786_b200 import _native
+    rng = np.random.default_rng(6)
+    pts = sgl.gen_points_ball(2000, 3.0, rng)
+    p = sgl.plan(8, pts, flags=_native.FLAG_NO_GUARD)
+    assert not p.stats["guard"]
+    c = sgl.gen_coeffs(8, rng)
+    f = sgl.forward(p, c)
+    assert rel(f, sgl.forward(sgl.plan(8, pts, backend="tiled"), c)) <= 1e-11
+    assert p.guard["est_fwd"] == 0.0

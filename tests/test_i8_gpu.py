@@ -90,14 +90,11 @@ def test_batched_and_repeated_calls(sgl):
         assert np.array_equal(F[k], sgl.forward(p, C[k]))   # deterministic: no atomics in the gather
 
 
-# ---- the opt-in int8 scatter (SGL_SCATTER=i8, csrc/scatter_i8.cu)
+# ---- the int8 scatter forced on any node set (backend="i8", csrc/scatter_i8.cu)
 def _plan_i8s(sgl, *a, **kw):
-    import os
-    os.environ["SGL_SCATTER"] = "i8"
-    try:
-        return sgl.plan(*a, **kw)
-    finally:
-        os.environ.pop("SGL_SCATTER", None)
+    p = sgl.plan(*a, backend="i8", **kw)
+    assert p.stats["i8_scatter"]
+    return p
 
 
 @pytest.mark.parametrize("name", ["b8_q16", "b12_q12", "cfg1", "cfg2_sub2000", "cfg3_sub600", "edges_b8_q16"])

@@ -89,3 +89,23 @@ def test_oracle_exact_stages_match_direct_sums():
     exact = np.einsum("abc,ma,mb,mc->m", eta, E[0], E[1], E[2])
     ref = o.evaluate_direct(c, B, pts)
     assert o.rel_linf(exact, ref) <= 1e-10
+
+
+def test_extended_precision_truth_pinned():
+    """oracle/extended.py (longdouble restatement of evaluate_direct_adjoint,
+    transform.py:120-139) reproduces the reference's own direct sums, and the
+    committed config-4 truth (tests/golden/make_truth.py) is consistent with
+    the reference outputs it was measured against."""
+    from oracle import extended as X
+    for name in ("direct_b7", "direct_b16"):
+        g = load_golden(name)
+        t = X.direct_adjoint_ld(g["values"], int(g["B"]), g["points"], cos_fp64=True).astype(complex)
+        assert o.rel_linf(t, g["adj"]) <= 1e-13
+    t = load_golden("cfg4_truth")
+    g = load_golden("cfg4_sub120")
+    # the mpmath (60 digits) spot check of the longdouble truth
+    assert float(np.max(t["mp_err"])) <= 1e-15
+    # the reference fast adjoint's own error against the truth (2.56e-9: the
+    # FP64 ill-conditioning of config 4, not a window error)
+    assert o.rel_linf(g["adj"], t["truth"]) == pytest.approx(float(t["ref_fast_err"]), rel=1e-6)
+    assert float(t["ref_direct_err"]) <= 1e-12

@@ -1,4 +1,4 @@
-"""int8 tensor-core gather (SGL_GATHER=i8) vs the FP64 DMMA gather and the
+"""int8 tensor-core gather (the default engine) vs the FP64 DMMA gather and the
 reference goldens: accuracy (rel-linf) and forward window-stage time."""
 import argparse
 import os

@@ -1,4 +1,4 @@
-"""int8 tensor-core scatter (SGL_SCATTER=i8) vs the FP64 scatter and the
+"""int8 tensor-core scatter (backend="i8") vs the FP64 scatter (backend="tiled") and the
 reference goldens: accuracy (rel-linf) and adjoint window-stage time."""
 import os
 import sys
@@ -16,11 +16,9 @@ def rel(a, b):
 
 
 def mk(B, pts, rho, q=16, i8s=False):
-    if i8s:
-        os.environ["SGL_SCATTER"] = "i8"
-    p = sgl.plan(B, pts, rho=rho, q=q, profile=True)
-    os.environ.pop("SGL_SCATTER", None)
-    return p
+    # the FP64 arm must be the FP64 kernel itself, not "auto" (which picks the
+    # int8 scatter for large dense node sets)
+    return sgl.plan(B, pts, rho=rho, q=q, profile=True, backend="i8" if i8s else "tiled")
 
 
 gd = os.path.join(ROOT, "tests", "golden")
