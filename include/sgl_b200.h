@@ -62,7 +62,9 @@ enum {
     SGL_FLAG_GENERIC_GRIDDING = 1u << 2,  /* force the per-node window kernels      */
     SGL_FLAG_PROFILE = 1u << 3,           /* record per-stage CUDA-event timings    */
     SGL_FLAG_PRECISE = 1u << 4,           /* basal tables in 80-bit extended precision
-                                             (precise=True, recurrences.py:13)      */
+                                             (precise=True, recurrences.py:13); the
+                                             default since round 2 unless
+                                             SGL_FLAG_FP64_TABLES                   */
     SGL_FLAG_FP64_WINDOW = 1u << 5,       /* both window stages on the FP64 DMMA
                                              kernels instead of the int8 tensor-core
                                              (digit-split) engines                  */
@@ -80,8 +82,14 @@ enum {
     SGL_FLAG_SCATTER_NARROW = 1u << 11,   /* FP64 scatter tiles in W x W2 pencils   */
     SGL_FLAG_I8_PROF = 1u << 12,          /* debug: clock64 wait counters of the int8
                                              kernels, printed to stderr per call    */
-    SGL_FLAG_NO_GUARD = 1u << 13          /* disable the int8 accuracy guard (the
-                                             per-call switch to the FP64 kernels)   */
+    SGL_FLAG_NO_GUARD = 1u << 13,         /* disable the int8 accuracy guard (the
+                                             per-call switch to the FP64 kernels;
+                                             estimates are still recorded)          */
+    SGL_FLAG_FP64_TABLES = 1u << 14       /* build the basal matrices in FP64 (the
+                                             reference's default arithmetic) instead
+                                             of x87 extended precision: config 4 is
+                                             4.7e-9 from the truth this way, 1.2e-9
+                                             with extended tables (reference: 2.6e-9) */
 };
 
 typedef struct {

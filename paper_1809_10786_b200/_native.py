@@ -27,6 +27,7 @@ FLAG_SCATTER_WIDE = 1 << 10
 FLAG_SCATTER_NARROW = 1 << 11
 FLAG_I8_PROF = 1 << 12
 FLAG_NO_GUARD = 1 << 13
+FLAG_FP64_TABLES = 1 << 14
 STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares

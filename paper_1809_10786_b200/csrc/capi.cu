@@ -227,10 +227,10 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
     rc = p.i8s ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
     if (rc) return rc;
     rc = adjoint_tail(p, c, st, rec);
-    if (rc || !(p.i8s && p.guard_on && may_sync && p.guard_ap > 0.0 && p.M > 0)) return rc;
+    if (rc || !(p.i8s && p.guard_ap > 0.0 && p.M > 0)) return rc;
     // int8 scatter accuracy check (guard.cu): estimate from the result, rerun on FP64 above the bound
     rc = guard_adjoint_estimate(p, v, c, st);
-    if (rc) return rc;
+    if (rc || !(p.guard_on && may_sync)) return rc;
     int redo = 0;
     SGL_CUDA_CHECK(cudaMemcpyAsync(&redo, &p.guard->adj_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
     SGL_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -323,7 +323,11 @@ int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, i
     p->q = q;
     p->compact = flags & SGL_FLAG_COMPACT_K1;
     p->profile = flags & SGL_FLAG_PROFILE;
-    p->precise = flags & SGL_FLAG_PRECISE;
+    // basal matrices in x87 extended precision unless FP64 tables are asked
+    // for (FP64 construction error dominates the ill-conditioned large-rho
+    // configurations: config 4 is 4.7e-9 from the extended-precision truth
+    // with FP64 tables, 1.2e-9 with extended ones; the reference: 2.6e-9)
+    p->precise = (flags & SGL_FLAG_PRECISE) || !(flags & SGL_FLAG_FP64_TABLES);
     p->exact = exact;
     p->flags = flags;
     p->generic = exact || (flags & SGL_FLAG_GENERIC_GRIDDING) || q > kMaxQTiled;
@@ -505,11 +509,11 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         set_error("out of device memory for the profile counters");
         rc = SGL_ENOMEM;
     }
-    if (rc == SGL_OK && p->i8s && p->guard_on && M > 0) {
+    if (rc == SGL_OK && p->i8s && M > 0) {
         // adjoint guard: response A_p of the tail to white grid noise of the
         // spread's per-cell rms for unit-rms values (guard.cu)
         const double cells = (double)p->grid[0] * p->grid[1] * p->grid[2];
-        rc = launch_noise_grid(*p, std::sqrt((double)M * p->guard_wmass2 / cells), st);
+        rc = launch_noise_grid(*p, std::sqrt((double)M * p->guard_tap2 / cells), st);
         if (rc == SGL_OK) rc = adjoint_tail(*p, p->coef_buf, st, nullptr);
         if (rc == SGL_OK) rc = read_absmax(*p, p->coef_buf, p->count, st, &p->guard_ap);
     }

@@ -183,7 +183,8 @@ struct Plan {
     GuardState *guard = nullptr;   // device
     bool guard_on = false;
     double guard_wmass = 0.0;      // max window L1 mass sum |w0 w1 w2| over a node's taps
-    double guard_wmass2 = 0.0;     // max sum of squared tap weights of a node
+    double guard_tap2 = 0.0;       // per-node error variance of the int8 spread in units of
+                                   // (2^-46 |v|)^2: (c0 c1 c2)^2 (2q+1)^3 (uniform per-tap error)
     double guard_ap = 0.0;         // adjoint tail's response to the spread noise model (plan time)
     unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
 

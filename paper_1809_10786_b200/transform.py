@@ -146,7 +146,7 @@ def _stream_ptr(x) -> int | None:
 def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
          exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
          precompute: bool = True, device: int | None = None, profile: bool = False,
-         precise_tables: bool = False, flags: int = 0) -> SglPlan:
+         precise_tables: bool | None = None, flags: int = 0) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
     ``backend``: "auto" (q <= 16: the int8 tensor-core gather for the
@@ -208,8 +208,14 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_FP64_WINDOW
     if profile:
         flags |= _native.FLAG_PROFILE
+    # basal matrices in x87 extended precision by default (closer to the
+    # truth on ill-conditioned configurations; SGL_FLAG_FP64_TABLES opts out)
+    if precise_tables is None:
+        precise_tables = not (flags & _native.FLAG_FP64_TABLES)
     if precise_tables:
         flags |= _native.FLAG_PRECISE
+    else:
+        flags |= _native.FLAG_FP64_TABLES
     h = ctypes.c_void_p(0)
     stream = _stream_ptr(pts)
     _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q or 0),

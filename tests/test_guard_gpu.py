@@ -150,4 +150,4 @@ def test_guard_off_flag(sgl):
     c = sgl.gen_coeffs(8, rng)
     f = sgl.forward(p, c)
     assert rel(f, sgl.forward(sgl.plan(8, pts, backend="tiled"), c)) <= 1e-11
-    assert p.guard["est_fwd"] == 0.0
+    assert p.guard["fwd_fallbacks"] == 0 and p.guard["est_fwd"] > 0.0   # estimated, never acted on

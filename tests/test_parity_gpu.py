@@ -139,16 +139,24 @@ def test_linearity_zero_and_errors(sgl):
 def test_precise_matches_reference_precise(sgl, name):
     # precise=True: basal tables in x87 extended precision on a cached twin
     # plan; against the reference's own precise=True outputs
+    # (default plans build their tables in extended precision: precise calls
+    # run on the plan itself; FP64-table plans get a cached twin)
     g = load_golden(name)
     p = _plan(sgl, g)
+    assert p.precise_tables
     f = sgl.forward(p, g["coeffs"], precise=True)
     a = sgl.adjoint(p, g["values"], precise=True)
     assert rel(f, g["fwd"]) <= TOL and rel(a, g["adj"]) <= TOL
-    assert p._twin is not None and p._twin.precise_tables
-    assert sgl.forward(p, g["coeffs"], precise=True).shape == f.shape   # the twin is reused
-    assert rel(sgl.forward(p, g["coeffs"]), g["fwd_double"]) <= TOL
-    p.close()
     assert p._twin is None
+    assert rel(sgl.forward(p, g["coeffs"]), g["fwd_double"]) <= TOL
+    p64 = _plan(sgl, g, precise_tables=False)
+    assert rel(sgl.forward(p64, g["coeffs"]), g["fwd_double"]) <= TOL
+    f = sgl.forward(p64, g["coeffs"], precise=True)
+    assert rel(f, g["fwd"]) <= TOL
+    assert p64._twin is not None and p64._twin.precise_tables
+    assert sgl.forward(p64, g["coeffs"], precise=True).shape == f.shape   # the twin is reused
+    p64.close()
+    assert p64._twin is None
 
 
 def test_compact_grid_agrees(sgl):
