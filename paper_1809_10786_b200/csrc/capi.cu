@@ -8,9 +8,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "sgl_internal.cuh"
 
@@ -19,6 +21,15 @@ namespace sgl {
 static thread_local std::string g_err;
 
 void set_error(const std::string &msg) { g_err = msg; }
+
+void plan_lap(Plan &p, cudaStream_t st, const char *what) {
+    if (!(p.flags & SGL_FLAG_I8_PROF)) return;
+    cudaStreamSynchronize(st);
+    const double now =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (p.lap_ms >= 0) fprintf(stderr, "plan %-28s %9.2f ms\n", what, now - p.lap_ms);
+    p.lap_ms = now;
+}
 
 namespace {
 
@@ -432,12 +443,23 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         }
         dpts = owned;
     }
+    plan_lap(*p, st, "start");
+    if (rc == SGL_OK) rc = resolve_rho(*p, dpts, st);
+    // the basal matrices depend on (B, rho) only: built on a host thread while
+    // the device sorts and tiles the nodes
+    std::vector<double> Kl, Km;
+    std::thread tables;
+    if (rc == SGL_OK && !p->raw) tables = std::thread([&]() { basal_tables_host(*p, Kl, Km); });
     if (rc == SGL_OK) rc = build_nodes(*p, dpts, st);
+    plan_lap(*p, st, "nodes (total)");
+    if (tables.joinable()) tables.join();
+    plan_lap(*p, st, "basal tables (host, join)");
     if (owned) {
         cudaStreamSynchronize(st);
         cudaFree(owned);
     }
-    if (rc == SGL_OK) rc = p->raw ? build_deconv_tables(*p) : build_basal_tables(*p);
+    if (rc == SGL_OK) rc = p->raw ? build_deconv_tables(*p) : upload_basal_tables(*p, Kl, Km);
+    plan_lap(*p, st, "basal tables upload");
     if (rc == SGL_OK) {
         if (cudaMalloc(&p->grid_buf, sizeof(double2) * p->grid_elems) != cudaSuccess ||
             cudaMalloc(&p->beta, sizeof(double2) * (size_t)std::max(1, p->B * p->B * 4 * p->B)) != cudaSuccess ||
@@ -499,9 +521,12 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
             }
         }
     }
+    plan_lap(*p, st, "buffers + cuFFT plans");
     if (rc == SGL_OK && !p->generic && !exact) rc = make_grid_tmap(*p);
     if (rc == SGL_OK && p->i8) rc = setup_i8(*p);
+    plan_lap(*p, st, "setup int8 gather");
     if (rc == SGL_OK && p->i8s) rc = setup_scatter_i8(*p);
+    plan_lap(*p, st, "setup int8 scatter");
     if (rc == SGL_OK) rc = setup_guard(*p);
     if (rc == SGL_OK && (p->flags & SGL_FLAG_I8_PROF) && (p->i8 || p->i8s) &&
         cudaMalloc(&p->prof, sizeof(unsigned long long) * 8 * num_sms()) != cudaSuccess) {
@@ -516,6 +541,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         rc = launch_noise_grid(*p, std::sqrt((double)M * p->guard_tap2 / cells), st);
         if (rc == SGL_OK) rc = adjoint_tail(*p, p->coef_buf, st, nullptr);
         if (rc == SGL_OK) rc = read_absmax(*p, p->coef_buf, p->count, st, &p->guard_ap);
+        plan_lap(*p, st, "guard calibration");
     }
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");

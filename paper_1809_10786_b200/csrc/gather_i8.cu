@@ -445,18 +445,14 @@ void i8_scales(const Plan &p, double &s0, double &s2, int &sA) {
 int setup_i8(Plan &p) {
     const WindowParams &w = p.wp;
     if (p.n_itiles > 0) {
-        std::vector<Tile> ht(p.n_itiles);
-        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.itiles, sizeof(Tile) * p.n_itiles, cudaMemcpyDeviceToHost));
-        p.i8_ksteps = 0;
-        for (const Tile &t : ht) {
-            p.i8_ksteps += (CHUNKS * t.e0 + 1) / 2;
-            const int k0 = kstart2(t, w);
-            if (t.o2 + w.pad < k0 || t.o2 + w.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 || t.e0 > kBox0Max ||
-                t.count > kI8Nodes) {
-                set_error("internal: int8 gather tile outside its K range");
-                return SGL_ECUDA;
-            }
+        TileStats ts;
+        const int rc = tile_stats(p.itiles, p.n_itiles, 1, w, nullptr, &ts);
+        if (rc) return rc;
+        if (ts.bad) {
+            set_error("internal: int8 gather tile outside its K range");
+            return SGL_ECUDA;
         }
+        p.i8_ksteps = ts.work;
     }
     p.P2 = (w.N2p + 15) / 16;   // 16-cell column blocks per row
     const size_t bytes = (size_t)w.N0 * p.P2 * ND * w.N1p * 32;

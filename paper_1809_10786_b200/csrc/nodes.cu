@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "i8_common.cuh"
 #include "sgl_internal.cuh"
 
 namespace sgl {
@@ -203,13 +204,100 @@ __global__ void k_tiles(const int32_t *starts, int64_t nruns, int64_t M, const d
     if (!out) counts[r] = nt;
 }
 
+// plan-time scratch from the stream-ordered pool (cudaMallocAsync): frees do
+// not synchronise the device
+thread_local cudaStream_t t_plan_stream = nullptr;
+
+// One warp per pencil run: the same greedy cut as k_tiles (tiles of <=
+// max_nodes nodes, lo0 span <= span0, box within the slab limits), 32 nodes
+// per step: per-lane window cells, warp prefix min / max of the box, and the
+// first lane that fails ends the tile.  write == nullptr: count only.
+__global__ void k_tiles_warp(const int32_t *starts, int64_t nruns, int64_t M, const double *u0, const double *u1,
+                             const double *u2, TileGeom g, int32_t *counts, const int32_t *offsets, Tile *out) {
+    const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= nruns) return;
+    const int64_t s = starts[r];
+    const int64_t e = (r + 1 < nruns) ? starts[r + 1] : M;
+    int32_t nt = 0;
+    int64_t pos = out ? offsets[r] : 0;
+    int64_t i = s;
+    const int BIG = 1 << 30;
+    while (i < e) {
+        const int first0 = lo_of(u0[i]);
+        int mn[3] = {BIG, BIG, BIG}, mx[3] = {-BIG, -BIG, -BIG};
+        int64_t j = i;
+        for (;;) {
+            const int64_t k = j + lane;
+            const bool valid = k < e && k - i < g.max_nodes;
+            int cl[3] = {BIG, BIG, BIG}, ch[3] = {-BIG, -BIG, -BIG};
+            bool fail = !valid;
+            if (valid) {
+                const double uu[3] = {u0[k], u1[k], u2[k]};
+                if (lo_of(uu[0]) - first0 > g.span0) fail = true;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) window_cells(uu[d], g.q, cl[d], ch[d]);
+            }
+            // inclusive prefix min / max over the lanes, merged with the tile so far
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int a = __shfl_up_sync(0xffffffffu, cl[d], o), b = __shfl_up_sync(0xffffffffu, ch[d], o);
+                    if (lane >= o) {
+                        cl[d] = min(cl[d], a);
+                        ch[d] = max(ch[d], b);
+                    }
+                }
+            }
+            int tmn[3], tmx[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                tmn[d] = min(mn[d], cl[d]);
+                tmx[d] = max(mx[d], ch[d]);
+            }
+            if (valid && k > i &&
+                (tmx[1] - tmn[1] + 1 > g.box1 || tmx[2] - tmn[2] + 1 > g.box2 || tmx[0] - tmn[0] + 1 > g.box0))
+                fail = true;
+            const unsigned bad = __ballot_sync(0xffffffffu, fail);
+            const int take = bad ? __ffs(bad) - 1 : 32;   // accepted lanes of this step
+            if (take > 0) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    mn[d] = __shfl_sync(0xffffffffu, tmn[d], take - 1);
+                    mx[d] = __shfl_sync(0xffffffffu, tmx[d], take - 1);
+                }
+            }
+            j += take;
+            if (take < 32) break;
+        }
+        if (out && lane == 0) {
+            Tile t;
+            t.start = (int32_t)i;
+            t.count = (int32_t)(j - i);
+            t.o0 = mn[0];
+            t.o1 = mn[1];
+            t.o2 = mn[2];
+            t.e0 = mx[0] - mn[0] + 1;
+            t.e1 = mx[1] - mn[1] + 1;
+            t.e2 = mx[2] - mn[2] + 1;
+            out[pos] = t;
+        }
+        ++pos;
+        ++nt;
+        i = j;
+    }
+    if (!out && lane == 0) counts[r] = nt;
+}
+
 template <typename T>
 struct DevBuf {
     T *p = nullptr;
+    cudaStream_t st = t_plan_stream;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
     }
-    cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * (n ? n : 1)); }
+    cudaError_t alloc(size_t n) { return cudaMallocAsync(&p, sizeof(T) * (n ? n : 1), st); }
 };
 
 inline unsigned grid_for(int64_t n, int threads) {
@@ -283,8 +371,8 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
     SGL_CUDA_CHECK(counts.alloc(nruns));
     SGL_CUDA_CHECK(offs.alloc(nruns));
     k_run_starts<<<grid_for(M, T), T, 0, st>>>(head.p, rank.p, M, starts.p);
-    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p, nullptr,
-                                                 nullptr);
+    k_tiles_warp<<<grid_for(nruns * 32, 256), 256, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p,
+                                                           nullptr, nullptr);
     {
         DevBuf<unsigned char> tmp;
         size_t tb = 0;
@@ -298,31 +386,119 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
     SGL_CUDA_CHECK(cudaStreamSynchronize(st));
     *ntiles = (int64_t)lc + lo;
     SGL_CUDA_CHECK(cudaMalloc(tiles, sizeof(Tile) * (*ntiles)));
-    k_tiles<<<grid_for(nruns, 128), 128, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p, offs.p,
-                                                 *tiles);
+    k_tiles_warp<<<grid_for(nruns * 32, 256), 256, 0, st>>>(starts.p, nruns, M, ns.u0, ns.u1, ns.u2, tg, counts.p,
+                                                           offs.p, *tiles);
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
 
+__global__ void k_tile_band_key(const Tile *__restrict__ t, int64_t n, uint64_t *key, int32_t *idx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // box origins are >= -(pad + 8): bias them non-negative; 21 bits per field
+    const uint64_t b0 = (uint64_t)((t[i].o0 >> 3) + 4096), b1 = (uint64_t)(t[i].o1 + 4096),
+                   b2 = (uint64_t)(t[i].o2 + 4096);
+    key[i] = (b0 << 42) | (b1 << 21) | b2;
+    idx[i] = (int32_t)i;
+}
+
+__global__ void k_tile_gather(const Tile *__restrict__ src, const int32_t *__restrict__ idx, int64_t n,
+                              Tile *__restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+// L2 order of a tile list (see build_nodes): a stable device radix sort by
+// (axis-0 band of 8 slabs, o1, o2)
 int reorder_tiles(Tile *tiles, int64_t n, cudaStream_t st) {
     if (n <= 1) return SGL_OK;
-    std::vector<Tile> h(n);
-    SGL_CUDA_CHECK(cudaMemcpyAsync(h.data(), tiles, sizeof(Tile) * n, cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-    std::stable_sort(h.begin(), h.end(), [](const Tile &a, const Tile &b) {
-        const int ba = a.o0 >> 3, bb = b.o0 >> 3;
-        if (ba != bb) return ba < bb;
-        if (a.o1 != b.o1) return a.o1 < b.o1;
-        return a.o2 < b.o2;
-    });
-    SGL_CUDA_CHECK(cudaMemcpyAsync(tiles, h.data(), sizeof(Tile) * n, cudaMemcpyHostToDevice, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    DevBuf<uint64_t> key, key_s;
+    DevBuf<int32_t> idx, idx_s;
+    DevBuf<Tile> copy;
+    SGL_CUDA_CHECK(key.alloc(n));
+    SGL_CUDA_CHECK(key_s.alloc(n));
+    SGL_CUDA_CHECK(idx.alloc(n));
+    SGL_CUDA_CHECK(idx_s.alloc(n));
+    SGL_CUDA_CHECK(copy.alloc(n));
+    k_tile_band_key<<<grid_for(n, 256), 256, 0, st>>>(tiles, n, key.p, idx.p);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    {
+        DevBuf<unsigned char> tmp;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_s.p, idx.p, idx_s.p, (int)n, 0, 63, st);
+        SGL_CUDA_CHECK(tmp.alloc(tb));
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_s.p, idx.p, idx_s.p, (int)n, 0, 63, st);
+        SGL_CUDA_CHECK(cudaGetLastError());
+    }
+    SGL_CUDA_CHECK(cudaMemcpyAsync(copy.p, tiles, sizeof(Tile) * n, cudaMemcpyDeviceToDevice, st));
+    k_tile_gather<<<grid_for(n, 256), 256, 0, st>>>(copy.p, idx_s.p, n, tiles);
+    SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
+}
+
+// per-list tile statistics on the device (one pass, 64-bit atomics)
+struct TileStatsDev {
+    unsigned long long nodes, work, bad;
+    int box;
+};
+
+__global__ void k_tile_stats(const Tile *__restrict__ tiles, int64_t n, int mode, WindowParams wp,
+                             TileStatsDev *out) {
+    unsigned long long nodes = 0, work = 0, bad = 0;
+    int box = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const Tile t = tiles[i];
+        nodes += (unsigned long long)t.count;
+        if (mode == 0) {   // FP64 gather tiles: DMMA m8n8k4 of one pass, box limits
+            const int64_t mt = (t.e1 + 3) / 4, ks = (t.e2 + 3) / 4, nt = (t.count + 7) / 8;
+            work += (unsigned long long)(t.e0 * mt * ks * nt);
+            box = max(box, max(t.e1, t.e2));
+            bad |= (t.e1 > kBoxMax || t.e2 > kBoxMax || t.e0 > kBox0Max);
+        } else {           // int8 tiles: K range of the digit boxes
+            const int k0 = i8::kstart2(t, wp);
+            bad |= (t.o2 + wp.pad < k0 || t.o2 + wp.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 ||
+                    t.e0 > kBox0Max || t.count > (mode == 1 ? kI8Nodes : kI8SNodes));
+            if (mode == 1) work += (unsigned long long)((i8::CHUNKS * t.e0 + 1) / 2);   // gather K-steps
+            else work += (unsigned long long)(((t.e0 * kI8Box2 + 127) / 128) * ((t.count + 31) / 32));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        nodes += __shfl_xor_sync(0xffffffffu, nodes, o);
+        work += __shfl_xor_sync(0xffffffffu, work, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        box = max(box, __shfl_xor_sync(0xffffffffu, box, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out->nodes, nodes);
+        atomicAdd(&out->work, work);
+        atomicOr(&out->bad, bad);
+        atomicMax(&out->box, box);
+    }
 }
 
 }  // namespace
 
-int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
+int tile_stats(const Tile *tiles, int64_t n, int mode, const WindowParams &wp, cudaStream_t st, TileStats *out) {
+    *out = TileStats();
+    if (n <= 0) return SGL_OK;
+    TileStatsDev *d = nullptr;
+    SGL_CUDA_CHECK(cudaMallocAsync(&d, sizeof(TileStatsDev), st));
+    SGL_CUDA_CHECK(cudaMemsetAsync(d, 0, sizeof(TileStatsDev), st));
+    k_tile_stats<<<(unsigned)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, st>>>(tiles, n, mode, wp, d);
+    TileStatsDev h;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaFreeAsync(d, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    out->nodes = (int64_t)h.nodes;
+    out->work = (int64_t)h.work;
+    out->bad = h.bad != 0;
+    out->box = h.box;
+    return SGL_OK;
+}
+
+int resolve_rho(Plan &p, const double *pts, cudaStream_t st) {
+    t_plan_stream = st;
     const int64_t M = p.M;
     const int T = 256;
     // rho: explicit, or the largest radius (choose_rho, transform.py:39-43)
@@ -356,6 +532,13 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
             return SGL_EINVAL;
         }
     }
+    return SGL_OK;
+}
+
+int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
+    t_plan_stream = st;
+    const int64_t M = p.M;
+    const int T = 256;
     DevBuf<double> a0, a1, a2;
     SGL_CUDA_CHECK(a0.alloc(M));
     SGL_CUDA_CHECK(a1.alloc(M));
@@ -373,8 +556,10 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     // the 8 consumer warps stay close together in the slab ring.
     int W = (4 - (2 * p.q - 1) % 4) % 4;
     if (W < 2) W += 4;
+    plan_lap(p, st, "rho + warp");
     int rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W, TileGeom{p.q, kBox0Max - 2 * p.q - 1, kTileNodes, kBox0Max},
                             p.nodes, &p.tiles, &p.n_tiles, !p.generic, st);
+    plan_lap(p, st, "gather order + tiles");
     if (rc || p.generic) return rc;
     if (p.i8) {
         // int8 tensor-core gather: 8 x 16 pencils (box 40 x 48 = MMA N x 3 K-chunks per slab), 128-node tiles
@@ -384,8 +569,10 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
         rc = order_and_tile(p, a0.p, a1.p, a2.p, kI8Box1 - 32, kI8Box2 - 32, ig, p.inodes, &p.itiles, &p.n_itiles,
                             true, st);
         if (rc) return rc;
+        plan_lap(p, st, "int8 order + tiles");
         rc = reorder_tiles(p.itiles, p.n_itiles, st);
         if (rc) return rc;
+        plan_lap(p, st, "int8 tile reorder");
         if (p.i8s || p.i8s_auto) {
             // int8 scatter: same order, 512-node tiles (fewer grid REDs per node)
             TileGeom sg = ig;
@@ -400,11 +587,10 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
                 // K-step (32 nodes x 128 cells), the FP64 DMMA scatter ~1400 per
                 // node (config 3, r01): take it for large dense node sets only (config 2,
                 // 1e6 lattice nodes: 6.9 vs 5.2 ms, its per-M-block drain dominates)
-                std::vector<Tile> h(p.n_istiles);
-                if (p.n_istiles)
-                    SGL_CUDA_CHECK(cudaMemcpy(h.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
-                double ks = 0;
-                for (const Tile &t : h) ks += (double)((t.e0 * kI8Box2 + 127) / 128) * ((t.count + 31) / 32);
+                TileStats ts;
+                rc = tile_stats(p.istiles, p.n_istiles, 2, p.wp, st, &ts);
+                if (rc) return rc;
+                const double ks = (double)ts.work;
                 p.i8s = p.M >= 5000000 && ks < 0.5 * (double)p.M;   // config 3 (1e7): 0.45, 46.8 vs 50.1 ms
                 if (!p.i8s) {
                     cudaFree(p.istiles);
@@ -426,6 +612,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     bool narrow = W2 != W && per_row >= 1.5;   // crossover measured on the config-3 shape (r01)
     if (p.flags & SGL_FLAG_SCATTER_WIDE) narrow = false;   // experiments
     if (p.flags & SGL_FLAG_SCATTER_NARROW) narrow = W2 != W;
+    plan_lap(p, st, "int8 scatter tiles");
     const TileGeom stg{p.q, kSBox0Max - 2 * p.q - 1, kSTileNodes, kSBox0Max};
     if (narrow) {
         rc = order_and_tile(p, a0.p, a1.p, a2.p, W, W2, stg, p.snodes, &p.stiles, &p.n_stiles, true, st);
@@ -439,30 +626,24 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
     // flight at any moment are a contiguous stretch of the list.  Ordering the
     // list by axis-0 band first (then axis 1, axis 2) keeps that stretch inside
     // a narrow slab band of the grid instead of a few full-length pencils.
+    plan_lap(p, st, "scatter order + tiles");
     rc = reorder_tiles(p.tiles, p.n_tiles, st);
     if (rc) return rc;
     rc = reorder_tiles(p.stiles, p.n_stiles, st);
     if (rc) return rc;
+    plan_lap(p, st, "tile reorder");
 
-    // tile statistics (host): nodes covered and DMMA count of one gather pass
-    std::vector<Tile> ht(p.n_tiles);
-    SGL_CUDA_CHECK(cudaMemcpyAsync(ht.data(), p.tiles, sizeof(Tile) * p.n_tiles, cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-    int64_t nodes = 0, dmma = 0;
-    int box = 1;
-    for (const Tile &t : ht) {
-        nodes += t.count;
-        box = std::max(box, std::max(t.e1, t.e2));
-        int64_t mt = (t.e1 + 3) / 4, ks = (t.e2 + 3) / 4, nt = (t.count + 7) / 8;
-        dmma += (int64_t)t.e0 * mt * ks * nt;
-        if (t.e1 > kBoxMax || t.e2 > kBoxMax || t.e0 > kBox0Max) {
-            set_error("internal: window tile exceeds the box limits");
-            return SGL_ECUDA;
-        }
+    // tile statistics (device): nodes covered and DMMA count of one gather pass
+    TileStats ts;
+    rc = tile_stats(p.tiles, p.n_tiles, 0, p.wp, st, &ts);
+    if (rc) return rc;
+    if (ts.bad) {
+        set_error("internal: window tile exceeds the box limits");
+        return SGL_ECUDA;
     }
-    p.tile_nodes = nodes;
-    p.tile_dmma = dmma;
-    p.tile_box = box;
+    p.tile_nodes = ts.nodes;
+    p.tile_dmma = ts.work;
+    p.tile_box = std::max(1, ts.box);
     return SGL_OK;
 }
 

@@ -30,6 +30,8 @@
 // warps 10-13 epilogue (TMEM lane quarters = cells).
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -420,6 +422,12 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     }
 }
 
+// K-steps of 32 nodes per tile (0 past the end: the scan's last entry is the total)
+__global__ void k_tile_ksteps(const Tile *__restrict__ tiles, int64_t n, int64_t *ks) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i <= n) ks[i] = i < n ? (tiles[i].count + KST - 1) / KST : 0;
+}
+
 // per tile: value scale from the tile's max |Re v|, |Im v| (|w1 v| 2^sV < 2^46, w1 <= c1)
 __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet nodes,
                               const double2 *__restrict__ values, double c1, int *__restrict__ tsv,
@@ -452,34 +460,23 @@ __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet
 
 int setup_scatter_i8(Plan &p) {
     const WindowParams &w = p.wp;
+    int64_t total_ks = 0;   // K-steps of all tiles (one 15 KB value-digit block each)
     if (p.n_istiles > 0) {
-        std::vector<Tile> ht(p.n_istiles);
-        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
-        for (const Tile &t : ht) {
-            const int k0 = kstart2(t, w);
-            if (t.o2 + w.pad < k0 || t.o2 + w.pad + t.e2 > k0 + kI8Box2 || t.e1 > kI8Box1 || t.e0 > kBox0Max ||
-                t.count > kI8SNodes) {
-                set_error("internal: int8 scatter tile outside its K range");
-                return SGL_ECUDA;
-            }
+        TileStats ts;
+        const int rc = tile_stats(p.istiles, p.n_istiles, 2, w, nullptr, &ts);
+        if (rc) return rc;
+        if (ts.bad) {
+            set_error("internal: int8 scatter tile outside its K range");
+            return SGL_ECUDA;
         }
-    }
-    // value-digit buffer: one 15 KB block per K-step of every tile
-    std::vector<int64_t> off(p.n_istiles + 1, 0);
-    if (p.n_istiles > 0) {
-        std::vector<Tile> ht(p.n_istiles);
-        SGL_CUDA_CHECK(cudaMemcpy(ht.data(), p.istiles, sizeof(Tile) * p.n_istiles, cudaMemcpyDeviceToHost));
-        p.i8_sksteps = 0;
-        for (int64_t i = 0; i < p.n_istiles; ++i) {
-            off[i + 1] = off[i] + (ht[i].count + KST - 1) / KST;
-            p.i8_sksteps += (int64_t)((ht[i].e0 * kI8Box2 + MR - 1) / MR) * ((ht[i].count + KST - 1) / KST);
-        }
+        p.i8_sksteps = ts.work;
+        total_ks = (ts.nodes + KST - 1) / KST + p.n_istiles;   // upper bound of sum ceil(count / 32)
     }
     // the digit buffer must leave room for the calls' own staging (val_buf2, cuFFT work):
     // keep 2 GB free, else stay on the FP64 scatter (which needs none)
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    const size_t need = (size_t)std::max<int64_t>(1, off[p.n_istiles]) * B_STAGE;
+    const size_t need = (size_t)std::max<int64_t>(1, total_ks) * B_STAGE;
     if (need + (size_t(2) << 30) > fr || cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
         cudaMalloc(&p.svoff, sizeof(int64_t) * (p.n_istiles + 1)) != cudaSuccess ||
         cudaMalloc(&p.vdig, need) != cudaSuccess) {
@@ -495,7 +492,21 @@ int setup_scatter_i8(Plan &p) {
         p.i8s = false;   // FP64 scatter (as setup_i8 does for the gather)
         return SGL_OK;
     }
-    SGL_CUDA_CHECK(cudaMemcpy(p.svoff, off.data(), sizeof(int64_t) * (p.n_istiles + 1), cudaMemcpyHostToDevice));
+    // first value-digit block of every tile: exclusive scan of ceil(count / 32)
+    if (p.n_istiles > 0) {
+        int64_t *ks = nullptr;
+        void *tmp = nullptr;
+        size_t tb = 0;
+        SGL_CUDA_CHECK(cudaMalloc(&ks, sizeof(int64_t) * (p.n_istiles + 1)));
+        k_tile_ksteps<<<(unsigned)((p.n_istiles + 256) / 256), 256>>>(p.istiles, p.n_istiles, ks);
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, ks, p.svoff, (int)(p.n_istiles + 1));
+        SGL_CUDA_CHECK(cudaMalloc(&tmp, tb));
+        cub::DeviceScan::ExclusiveSum(tmp, tb, ks, p.svoff, (int)(p.n_istiles + 1));
+        SGL_CUDA_CHECK(cudaGetLastError());
+        SGL_CUDA_CHECK(cudaDeviceSynchronize());
+        cudaFree(tmp);
+        cudaFree(ks);
+    }
     return SGL_OK;
 }
 

@@ -187,6 +187,7 @@ struct Plan {
                                    // (2^-46 |v|)^2: (c0 c1 c2)^2 (2q+1)^3 (uniform per-tap error)
     double guard_ap = 0.0;         // adjoint tail's response to the spread noise model (plan time)
     unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
+    double lap_ms = -1.0;          // SGL_FLAG_I8_PROF: plan-construction stage clock (plan_lap)
 
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
@@ -219,7 +220,23 @@ void set_error(const std::string &msg);
 
 // kernels / launchers (defined in the .cu files)
 int build_nodes(Plan &p, const double *points_dev, cudaStream_t st);
+// device statistics of a tile list: mode 0 = FP64 gather tiles (work = DMMA
+// count, box = widest axis-1/2 extent), 1 = int8 gather tiles (work = K-steps),
+// 2 = int8 scatter tiles (work = K-steps x M-blocks); bad = a tile outside its
+// kernel's limits
+struct TileStats {
+    int64_t nodes = 0, work = 0;
+    bool bad = false;
+    int box = 0;
+};
+int tile_stats(const Tile *tiles, int64_t n, int mode, const WindowParams &wp, cudaStream_t st, TileStats *out);
 int build_basal_tables(Plan &p);
+// the host half (no CUDA calls; uses B, rho, precise) and the upload half,
+// so plan creation can overlap the host tables with the device node work
+void basal_tables_host(Plan &p, std::vector<double> &Kl, std::vector<double> &Km);
+int upload_basal_tables(Plan &p, const std::vector<double> &Kl, const std::vector<double> &Km);
+// rho (choose_rho, transform.py:39-43) and the radius check (transform.py:50-51)
+int resolve_rho(Plan &p, const double *points_dev, cudaStream_t st);
 int build_deconv_tables(Plan &p);
 int launch_place_raw(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st);
 int launch_crop_raw(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
@@ -240,6 +257,9 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
 int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
 int setup_scatter_i8(Plan &p);
 int setup_guard(Plan &p);
+// SGL_FLAG_I8_PROF: synchronise and print the host time since the previous lap
+// of this plan's construction to stderr (diagnostics of plan time)
+void plan_lap(Plan &p, cudaStream_t st, const char *what);
 int launch_gather_guarded(const Plan &p, const double2 *grid, double2 *values, cudaStream_t st);
 int launch_noise_grid(const Plan &p, double rms, cudaStream_t st);
 int read_absmax(const Plan &p, const double2 *v, int64_t n, cudaStream_t st, double *out);
