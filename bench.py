@@ -1,7 +1,8 @@
 """NFSGLFT benchmark: nodes/sec of forward + adjoint at BASELINE config 3.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 3] [--m M]
+                    [--config 3] [--points M] [--scaling strong|weak]
+                    [--partition auto|coeffs|grid]
 
 A step is one forward (coefficients -> values at all M nodes) plus one adjoint
 (values -> coefficients) on a fixed plan: BASELINE.json's headline metric
@@ -9,13 +10,21 @@ A step is one forward (coefficients -> values at all M nodes) plus one adjoint
 the radius-16 ball, complex128).  Inputs are the seeded synthetic inputs of
 SURVEY 8(d) (no public dataset exists for this path).
 
-N > 1 (torchrun, one rank per GPU): weak scaling, each rank owns its own
-M-node shard drawn from the same distribution; rho is the all-reduce max; the
-adjoint's exchange step is an NCCL all-reduce of the coefficient vector.
+N > 1 (torchrun, one rank per GPU), default --scaling strong: every rank
+builds the SAME config (seed 0, same coefficients), takes its contiguous
+node shard (distributed.shard_bounds), rho is the all-reduce max over the
+shards (= the full set's); value = M_total / the slowest rank's step time.
+The adjoint's exchange is the partition `distributed.partition_model` picks
+(--partition overrides): the coefficient all-reduce or the north star's grid
+reduce-scatter + slab FFT.  --scaling weak: each rank its own M-node set.
 
---impl reference times the CPU reference path (the oracle port of the
-reference algorithm, oracle/; the reference is pure Python and cannot travel)
-on the host cores, extrapolated from bounded node samples.
+--impl reference times the reference itself: the unmodified `sglnufft`
+package (numba, as shipped: serial window loops, single-threaded pocketfft)
+installed in baseline/_ref, JIT warm-up excluded as the reference's own
+runners do (experiments.py:240-243); per step two rho-pinned node samples
+give T_fixed + M t_node, extrapolated to M and flagged as such.
+The 16-thread oracle port (oracle/) is reported beside it (`cpu_port`), and
+replaces it when the reference cannot be imported.
 """
 from __future__ import annotations
 
@@ -52,6 +61,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=4000)
     ap.add_argument("--direction", default=None, choices=["both", "fwd", "adj"],
                     help="default: the config's own (3: both, 4: adj, 5: batched fwd)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--partition", default="auto", choices=["auto", "coeffs", "grid"])
+    ap.add_argument("--no-stock", action="store_true", help="skip timing the stock reference package")
     return ap.parse_args()
 
 
@@ -176,6 +188,58 @@ def cpu_reference(work, rho, sample, direction="both", K=1, rank_threads=0):
             "t_fixed_s": nvec * t_ff + t_fa, "t_node_us": (nvec * t_g + t_s) * 1e6}
 
 
+STOCK = os.path.join(ROOT, "baseline", "_ref")
+
+
+def stock_reference(work, rho, direction="both", K=1, s1=1000, s2=21000):
+    """The unmodified reference package (baseline/_ref: numba backend, serial
+    loops, pocketfft) on rho-pinned samples of s1 and s2 nodes:
+    T(M) = T_fixed + M t_node per direction, plans excluded,
+    JIT warm-up excluded (experiments.py:240-243).  Raises ImportError when
+    the package is not installed."""
+    if STOCK not in sys.path:
+        sys.path.insert(0, STOCK)
+    import sglnufft as ref
+    c = work.coeffs if work.coeffs.ndim == 1 else work.coeffs[0]
+    idx = np.linspace(0, work.M - 1, min(s2, work.M)).astype(np.int64)
+    s1 = min(s1, len(idx) // 2) if len(idx) > 1 else len(idx)
+    vals = work.values if work.values is not None else np.zeros(work.M, complex)
+    fw, ad = direction in ("both", "fwd"), direction in ("both", "adj")
+    w0 = ref.plan(work.B, work.points[idx[:16]], rho=rho)   # JIT warm-up
+    if fw:
+        ref.forward(w0, c)
+    if ad:
+        ref.adjoint(w0, vals[idx[:16]])
+    t_start = time.perf_counter()
+    res = {}
+    for S in (s1, len(idx)):
+        sel = idx[:S] if S == s1 else idx
+        p = ref.plan(work.B, work.points[sel], rho=rho)
+        t0 = time.perf_counter()
+        if fw:
+            ref.forward(p, c)
+        t1 = time.perf_counter()
+        if ad:
+            ref.adjoint(p, vals[sel])
+        t2 = time.perf_counter()
+        res[S] = (t1 - t0, t2 - t1)
+    S1, S2 = s1, len(idx)
+    tn = [(res[S2][d] - res[S1][d]) / max(1, S2 - S1) for d in (0, 1)]
+    tf = [max(0.0, res[S1][d] - S1 * tn[d]) for d in (0, 1)]
+    nvec = K if direction == "fwd" else 1
+    T = nvec * (tf[0] + work.M * tn[0]) * fw + (tf[1] + work.M * tn[1]) * ad
+    units = work.M * nvec
+    return {"value": units / T, "unit": "nodes/s", "cores": 1, "kind": "reference",
+            "extrapolated": True, "sample_seconds": time.perf_counter() - t_start,
+            "sample": (f"unmodified sglnufft {getattr(ref, '__version__', '')} (baseline/_ref; numba backend, serial "
+                       f"loops, single-threaded pocketfft: the reference path uses one core), {direction}"
+                       + (f" x {nvec} vectors" if nvec > 1 else "") +
+                       f": T_fixed fwd {tf[0]:.2f} s / adj {tf[1]:.2f} s, t_node fwd {tn[0] * 1e6:.1f} us / adj "
+                       f"{tn[1] * 1e6:.1f} us from rho-pinned samples of {S1} and {S2} nodes, extrapolated to "
+                       f"M={work.M}; plans and JIT warm-up excluded (experiments.py:240-243)"),
+            "t_fixed_s": nvec * tf[0] * fw + tf[1] * ad, "t_node_us": (nvec * tn[0] * fw + tn[1] * ad) * 1e6}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -184,27 +248,46 @@ def run_reference(args, rank, world):
     direction = args.direction or {"fwd": "fwd", "adj": "adj"}.get(w.directions, "both")
     K = 1 if w.coeffs.ndim == 1 else w.coeffs.shape[0]
     steps = max(1, min(args.steps, 3))
-    vals = []
-    base = None
-    for i in range(steps + min(args.warmup, 1)):
-        r = cpu_reference(w, w.rho, args.cpu_sample, direction, K)
-        if i >= min(args.warmup, 1):
+    port = cpu_reference(w, w.rho, args.cpu_sample, direction, K)
+    port_line = {k: port[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    vals, base, stock_err = [], None, None
+    t_sample = 0.0
+    try:
+        if args.no_stock:
+            raise ImportError("--no-stock")
+        for _ in range(steps):
+            r = stock_reference(w, w.rho, direction, K)
             vals.append(r["value"])
+            t_sample += r["sample_seconds"]
             base = r
+    except Exception as e:  # reference not importable: the oracle port stands in
+        stock_err = f"{type(e).__name__}: {e}"
+        vals = [port["value"]]
+        base = port
     v = statistics.median(vals)
+    cpu = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    cpu["value"] = v
     line = {"metric": metric_name(args.config, direction, w.B, K), "impl": "reference", "value": v,
             "unit": "nodes/s",
-            "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
+            "n_gpus": world, "steps": len(vals), "warmup": 1,
             "ms_per_step": 1e3 * w.M * (K if direction == "fwd" else 1) / v, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "c128", "data": "synthetic (seeded PCG64, SURVEY 8(d))",
-            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": 16, "sigma": 2,
-                       "direction": direction, "vectors": K},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": bench_config(w, direction, K),
+            "extrapolated": True,
+            "sample_seconds": t_sample if stock_err is None else None,
+            "cpu_baseline": cpu, "cpu_port": port_line,
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": ("the reference is a pure-Python package; this arm times the oracle port of its algorithm "
-                     "(oracle/, C gridding with OpenMP + numpy/scipy) on the host, capped at 3 timed steps")}
+            "note": (("value: the unmodified reference package, timed on rho-pinned node samples and extrapolated "
+                      "to M (ms_per_step is the extrapolated step, not wall time); cpu_port: the 16-thread oracle "
+                      "port of the same algorithm") if stock_err is None else
+                     f"reference package not importable here ({stock_err}): the oracle port stands in")}
     print(json.dumps(line), flush=True)
+
+
+def bench_config(w, direction, K) -> dict:
+    """The workload identity: identical in both arms (extras go to config_extra)."""
+    return {"workload": w.name, "B": w.B, "M": w.M, "q": 16, "sigma": 2, "direction": direction, "vectors": K}
 
 
 def main():
@@ -221,7 +304,7 @@ def main():
 
     import paper_1809_10786_b200 as sgl
     from paper_1809_10786_b200 import _native, workloads
-    from paper_1809_10786_b200.distributed import ShardedPlan
+    from paper_1809_10786_b200.distributed import ShardedPlan, shard_bounds
 
     # test hooks: SGL_BENCH_DEVICE pins every rank to one GPU and
     # SGL_BENCH_BACKEND=gloo replaces NCCL, so the multi-rank logic can be
@@ -236,18 +319,25 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    w = workloads.config(args.config, M=args.points, seed=rank)
+    strong = args.scaling == "strong" or world == 1
+    # strong: the same transform on every rank (seed 0), sharded by nodes;
+    # weak: every rank its own M-node set of the config's distribution
+    w = workloads.config(args.config, M=args.points, seed=0 if strong else rank)
+    M_total = w.M * (1 if strong else world)
     direction = args.direction or {"fwd": "fwd", "adj": "adj"}.get(w.directions, "both")
     coeffs_h = w.coeffs                       # (count,) or (K, count) for the batched config 5
     K = 1 if coeffs_h.ndim == 1 else coeffs_h.shape[0]
     if w.values is None:
         w.values = np.zeros(w.M, dtype=complex)
+    if strong and world > 1:
+        s0, s1 = shard_bounds(w.M, rank, world)
+        w.points, w.values = w.points[s0:s1], w.values[s0:s1]
     pts_d = torch.as_tensor(w.points, device=dev)
     c_d = torch.as_tensor(coeffs_h, device=dev)
     v_d = torch.as_tensor(w.values, device=dev)
     t0 = time.perf_counter()
     # rho is global (all-reduce max over the ranks' shards) -- distributed.ShardedPlan
-    sp = ShardedPlan(w.B, pts_d, device=local) if world > 1 else None
+    sp = ShardedPlan(w.B, pts_d, device=local, partition=args.partition) if world > 1 else None
     p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local)
     rho = sp.rho if sp is not None else p.rho
     torch.cuda.synchronize()
@@ -260,9 +350,10 @@ def main():
         if direction in ("both", "fwd"):
             f = sgl.forward(pl, c_d)
         if direction in ("both", "adj"):
-            a = sgl.adjoint(pl, v_d)
-            if world > 1:   # the adjoint's exchange step (ShardedPlan.adjoint)
-                dist.all_reduce(torch.view_as_real(a))
+            if world > 1 and pl is p:   # the adjoint with its exchange step (ShardedPlan.adjoint)
+                a = sp.adjoint(v_d)
+            else:
+                a = sgl.adjoint(pl, v_d)
         return f, a
 
     # per-kernel timings (CUDA events inside the library, on the launching stream)
@@ -302,8 +393,8 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    units = w.M * (K if direction == "fwd" else 1)   # node evaluations per rank per step
-    value = world * units / (ms / 1e3)
+    units = M_total * (K if direction == "fwd" else 1)   # node evaluations of the whole job per step
+    value = units / (ms / 1e3)
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -317,22 +408,20 @@ def main():
         L = _native.lib()
 
         def e2e_step():
+            if world > 1:   # through the ShardedPlan API with host (pinned) arrays
+                if direction in ("both", "fwd"):
+                    _native.check(L.sgl_forward(p._handle, c_h.ctypes.data, K, fo.ctypes.data, None))
+                if direction in ("both", "adj"):
+                    ao[:] = sp.adjoint(v_h)
+                return
             if direction == "both" and K == 1:   # one call; copies overlap the compute
                 _native.check(L.sgl_forward_adjoint(p._handle, c_h.ctypes.data, fo.ctypes.data, v_h.ctypes.data,
                                                     ao.ctypes.data, None))
-                if world > 1:
-                    t = torch.from_numpy(ao).to(dev)
-                    dist.all_reduce(torch.view_as_real(t))
-                    ao[:] = t.cpu().numpy()
                 return
             if direction in ("both", "fwd"):
                 _native.check(L.sgl_forward(p._handle, c_h.ctypes.data, K, fo.ctypes.data, None))
             if direction in ("both", "adj"):
                 _native.check(L.sgl_adjoint(p._handle, v_h.ctypes.data, ao.ctypes.data, None))
-                if world > 1:
-                    t = torch.from_numpy(ao).to(dev)
-                    dist.all_reduce(torch.view_as_real(t))
-                    ao[:] = t.cpu().numpy()
 
         for _ in range(2):
             e2e_step()
@@ -349,7 +438,7 @@ def main():
             dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
         e_ms = float(e_t.item())
         fw_io, ad_io = direction in ("both", "fwd"), direction in ("both", "adj")
-        e2e = {"value": world * units / (e_ms / 1e3), "unit": "nodes/s",
+        e2e = {"value": units / (e_ms / 1e3), "unit": "nodes/s",
                "h2d_bytes_per_step": int(c_h.nbytes * fw_io + v_h.nbytes * ad_io),
                "d2h_bytes_per_step": int(fo.nbytes * fw_io + ao.nbytes * ad_io), "ms_per_step": e_ms}
 
@@ -426,13 +515,21 @@ def main():
                           "FP64 window FLOPs / 37.1 TF/s (FP64 DMMA peak) + 3-pass FFT bytes / HBM copy GB/s "
                           "(MEASURED_PEAKS.json); basal and halo work not counted"}
 
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             r = cpu_reference(w, rho, args.cpu_sample, direction, K)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu_port = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "nodes/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+            cpu_port = {"value": None, "unit": "nodes/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+        cpu = cpu_port
+        if not args.no_stock:
+            try:   # the reference itself (baseline/_ref), when it is installed
+                r = stock_reference(w, rho, direction, K)
+                cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "extrapolated",
+                                         "sample_seconds")}
+            except Exception as e:  # pragma: no cover
+                cpu_port = dict(cpu_port or {}, stock_unavailable=f"{type(e).__name__}: {e}")
 
     grid_gb = 16.0 * float(np.prod(p.nfft.grid_shape)) / 1e9 if p.nfft else 0.0
     node_gb = w.M * (3 * 8 * 2 + 4 * 2 + 16) / 1e9   # sorted u0..u2 + perm (gather and scatter orders) + values
@@ -443,20 +540,25 @@ def main():
             "metric": metric_name(args.config, direction, w.B, K),
             "value": value, "unit": "nodes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded PCG64 inputs of SURVEY 8(d); no public dataset)",
-            "config": {"workload": w.name, "B": w.B, "M_per_rank": w.M, "q": q, "sigma": 2, "direction": direction,
-                       "vectors": K,
-                       "grid": list(p.nfft.grid_shape), "rho": rho,
-                       "l2": l2_note,
-                       "parallelism": f"dp{world} (node shards; adjoint all-reduce of coefficients)"},
-            "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clk,
-            "gpu_launches": args.steps * ((8 if i8 else 4) * K * (direction != "adj") +
-                                         (6 if stats.get("i8_scatter") else 4) * (direction != "fwd")),
+            "config": bench_config(w, direction, K) | {"M": M_total},
+            "config_extra": {"grid": list(p.nfft.grid_shape), "rho": rho, "l2": l2_note, "M_per_rank": w.M,
+                             "parallelism": (f"{world} GPU(s), node shards; adjoint exchange: "
+                                             f"{sp.partition if sp is not None else 'none'}"
+                                             + (" (coefficient all-reduce)" if sp is not None and
+                                                sp.partition == "coeffs" else
+                                                " (grid reduce-scatter + slab FFT)" if sp is not None else ""))},
+            "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "cpu_port": cpu_port,
+            "clocks": clk,
+            "gpu_launches": args.steps * ((11 if i8 else 4) * K * (direction != "adj") +
+                                         (10 if stats.get("i8_scatter") else 4) * (direction != "fwd")),
             "gpu_launches_note": ("per forward vector: radial_fwd, sph_fwd, halo_fill, slab_absmax, slab_shift, "
-                                  "slice_grid, tile_shift, gather_i8" if i8 else
+                                  "slice_grid, tile_shift, gather_i8, absmax_c, guard_fwd, gather_tiled (gated: "
+                                  "returns at once unless the guard raised its flag)" if i8 else
                                   "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled") +
-                                 ("; per adjoint: tile_vscale, vdigits, scatter_i8, halo_fold, sph_adj, radial_adj"
+                                 ("; per adjoint: tile_vscale, vdigits, scatter_i8, scatter_tiled (gated), "
+                                  "halo_fold, sph_adj, radial_adj, sumsq_c, absmax_c, guard_adj"
                                     if stats.get("i8_scatter") else
                                     "; per adjoint: scatter_tiled, halo_fold, sph_adj, radial_adj") +
                                  " (+ cuFFT and memsets, library calls)",

@@ -185,6 +185,34 @@ int sgl_direct_adjoint(int32_t B, int64_t M, const double *points, const sgl_cdo
 
 int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info);
 
+/* ---- grid-partitioned multi-GPU adjoint (one process per GPU) ----------
+ * Stage entry points of the north star's adjoint partition: each rank
+ * spreads its node shard into its plan's own oversampled grid; the caller
+ * reduce-scatters axis-0 plane blocks of that grid (NCCL over NVLink); each
+ * rank FFTs its planes over axes 1-2 and packs the spectral box the basal
+ * stage reads; the caller gathers the packed planes to one rank, which
+ * finishes (1-D FFT along axis 0, crop, deconvolution, basal adjoint) and
+ * broadcasts the coefficients.  Replaces nfft_adjoint_execute +
+ * transform.adjoint (nfft.py:254-273, transform.py:398-429) split across
+ * ranks; see paper_1809_10786_b200/distributed.py.  All pointers device
+ * memory except `values` / `coeffs`, which may be host. */
+typedef struct {
+    void *data;               /* the plan's grid: N0 x N1p x N2p complex128 */
+    int32_t N0, N1, N2;       /* oversampled grid                           */
+    int32_t N1p, N2p, pad;    /* halo-padded pitches; interior at +pad      */
+    int64_t plane_elems;      /* N1p * N2p complex per axis-0 plane         */
+    int32_t crop1, crop2;     /* packed spectrum per plane: crop1 x crop2   */
+} sgl_grid_info;
+
+int sgl_plan_grid(const sgl_plan *plan, sgl_grid_info *info);
+/* zero the grid, spread `values` (M, this plan's nodes), fold the halo */
+int sgl_adjoint_spread(sgl_plan *plan, const sgl_cdouble *values, void *stream);
+/* 2-D forward FFT of planes [a0, a1) (in place), then pack their spectral box
+ * into `packed` ((a1 - a0) x crop1 x crop2, device) */
+int sgl_adjoint_slab_fft(sgl_plan *plan, int32_t a0, int32_t a1, sgl_cdouble *packed, void *stream);
+/* `packed`: all N0 planes (N0 x crop1 x crop2, device) -> coeff_count(B) */
+int sgl_adjoint_from_packed(sgl_plan *plan, const sgl_cdouble *packed, sgl_cdouble *coeffs, void *stream);
+
 /* per-stage device milliseconds of the last forward / adjoint call
  * (dir 0 = forward, 1 = adjoint); needs SGL_FLAG_PROFILE */
 int sgl_plan_stage_ms(const sgl_plan *plan, int32_t dir, float *ms, int32_t n);

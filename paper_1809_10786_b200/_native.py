@@ -35,7 +35,18 @@ EXPORTS = (
     "sgl_plan_create", "sgl_nfft_plan_create", "sgl_forward", "sgl_adjoint", "sgl_forward_adjoint", "sgl_direct_forward",
     "sgl_direct_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
+    "sgl_plan_grid", "sgl_adjoint_spread", "sgl_adjoint_slab_fft", "sgl_adjoint_from_packed",
 )
+
+
+class GridInfo(ctypes.Structure):
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("N0", ctypes.c_int32), ("N1", ctypes.c_int32), ("N2", ctypes.c_int32),
+        ("N1p", ctypes.c_int32), ("N2p", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("plane_elems", ctypes.c_int64),
+        ("crop1", ctypes.c_int32), ("crop2", ctypes.c_int32),
+    ]
 
 
 class PlanInfo(ctypes.Structure):
@@ -115,6 +126,14 @@ def lib() -> ctypes.CDLL:
     L.sgl_set_device.restype = ctypes.c_int
     L.sgl_device_count.argtypes = [ctypes.POINTER(i32)]
     L.sgl_device_count.restype = ctypes.c_int
+    L.sgl_plan_grid.argtypes = [vp, ctypes.POINTER(GridInfo)]
+    L.sgl_plan_grid.restype = ctypes.c_int
+    L.sgl_adjoint_spread.argtypes = [vp, vp, vp]
+    L.sgl_adjoint_spread.restype = ctypes.c_int
+    L.sgl_adjoint_slab_fft.argtypes = [vp, i32, i32, vp, vp]
+    L.sgl_adjoint_slab_fft.restype = ctypes.c_int
+    L.sgl_adjoint_from_packed.argtypes = [vp, vp, vp, vp]
+    L.sgl_adjoint_from_packed.restype = ctypes.c_int
     L.sgl_version.argtypes = []
     L.sgl_version.restype = ctypes.c_char_p
     _LIB = L

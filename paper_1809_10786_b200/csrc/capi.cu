@@ -70,6 +70,8 @@ void free_plan(Plan *p) {
         cufftDestroy(p->fft1);
     }
     if (p->fft_work) cudaFree(p->fft_work);
+    for (auto &e : p->slab_ffts) cufftDestroy(e.second);
+    if (p->dist_fft1) cufftDestroy(p->dist_fft1);
     if (p->done) cudaEventDestroy(p->done);
     if (p->ev_a) cudaEventDestroy(p->ev_a);
     if (p->ev_b) cudaEventDestroy(p->ev_b);
@@ -504,6 +506,8 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
                 if (made2) cufftDestroy(p->fft2);
                 if (made1) cufftDestroy(p->fft1);
                 if (p->fft_work) cudaFree(p->fft_work);
+    for (auto &e : p->slab_ffts) cufftDestroy(e.second);
+    if (p->dist_fft1) cufftDestroy(p->dist_fft1);
                 p->fft_work = nullptr;
             }
         }

@@ -189,6 +189,10 @@ struct Plan {
     unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
     double lap_ms = -1.0;          // SGL_FLAG_I8_PROF: plan-construction stage clock (plan_lap)
 
+    // grid-partitioned multi-GPU adjoint (dist.cu): slab 2-D plans by plane count, axis-0 plan
+    std::vector<std::pair<int, cufftHandle>> slab_ffts;
+    cufftHandle dist_fft1 = 0;
+
     StageTimer timers[2];
     float stage_ms[2][SGL_STAGE_COUNT] = {{0}};
 

@@ -27,7 +27,10 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "nodes/s"
     assert d["metric"] == "NFSGLFT nodes/sec fwd at B=16" and d["config"]["direction"] == "fwd"
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the unmodified reference (baseline/_ref) when installed, else the oracle port
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_port"]["kind"] == "port" and d["extrapolated"] is True
+    assert set(d["config"]) == {"workload", "B", "M", "q", "sigma", "direction", "vectors"}
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert abs(d["ms_per_step"] - 1e3 * 3000 / d["value"]) < 1e-6 * d["ms_per_step"]
 
