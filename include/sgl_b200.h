@@ -126,6 +126,7 @@ typedef struct {
     int64_t guard_adj_fallbacks;  /* adjoint calls likewise                     */
     double guard_est_fwd;     /* last forward's digit-split error estimate     */
     double guard_est_adj;     /* last adjoint's estimate                       */
+    int32_t n_gpus;           /* devices of the plan (sgl_plan_create_multi)   */
 } sgl_plan_info;
 
 /* stage indices for sgl_plan_stage_ms (valid with SGL_FLAG_PROFILE) */
@@ -143,6 +144,19 @@ enum {
  * stream may be NULL (legacy default stream). */
 int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, int32_t q,
                     double rho, uint32_t flags, void *stream, sgl_plan **out);
+
+/* The same plan over n_gpus devices of this process (devices: n_gpus ids, or
+ * NULL for 0 .. n_gpus-1): the points are split into contiguous,
+ * count-balanced shards, one sub-plan per device, all on the global rho
+ * (rho <= 0: max r over ALL points).  sgl_forward / sgl_adjoint /
+ * sgl_forward_adjoint / sgl_plan_get_info / sgl_plan_destroy accept the
+ * result: the forward evaluates each shard on its device into its slice of
+ * the values; the adjoint sums the shards' coefficient vectors.  One host
+ * thread per device per call; device-resident caller buffers are staged
+ * through host memory.  Reference signature: transform.plan
+ * (transform.py:320-330) + SURVEY 8(b)'s n_gpus. */
+int sgl_plan_create_multi(int32_t B, int64_t M, const double *points, int32_t sigma, int32_t q, double rho,
+                          uint32_t flags, int32_t n_gpus, const int32_t *devices, sgl_plan **out);
 
 /* Forward: coeffs is K x coeff_count(B) complex128 (mu order), values is
  * K x M complex128 in the caller's point order. */

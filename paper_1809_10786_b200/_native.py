@@ -36,6 +36,7 @@ EXPORTS = (
     "sgl_direct_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
     "sgl_plan_grid", "sgl_adjoint_spread", "sgl_adjoint_slab_fft", "sgl_adjoint_from_packed",
+    "sgl_plan_create_multi",
 )
 
 
@@ -79,6 +80,7 @@ class PlanInfo(ctypes.Structure):
         ("guard_adj_fallbacks", ctypes.c_int64),
         ("guard_est_fwd", ctypes.c_double),
         ("guard_est_adj", ctypes.c_double),
+        ("n_gpus", ctypes.c_int32),
     ]
 
 
@@ -102,6 +104,8 @@ def lib() -> ctypes.CDLL:
     vp, i32, i64, u32, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double
     L.sgl_plan_create.argtypes = [i32, i64, vp, i32, i32, dbl, u32, vp, ctypes.POINTER(vp)]
     L.sgl_plan_create.restype = ctypes.c_int
+    L.sgl_plan_create_multi.argtypes = [i32, i64, vp, i32, i32, dbl, u32, i32, vp, ctypes.POINTER(vp)]
+    L.sgl_plan_create_multi.restype = ctypes.c_int
     L.sgl_forward.argtypes = [vp, vp, i64, vp, vp]
     L.sgl_forward.restype = ctypes.c_int
     L.sgl_adjoint.argtypes = [vp, vp, vp, vp]

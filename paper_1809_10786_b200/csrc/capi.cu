@@ -53,6 +53,11 @@ int fft_check(cufftResult r, const char *what) {
 
 void free_plan(Plan *p) {
     if (!p) return;
+    if (!p->subs.empty()) {   // multi-GPU plan: only its sub-plans own device state
+        for (Plan *s : p->subs) free_plan(s);
+        delete p;
+        return;
+    }
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
@@ -679,6 +684,28 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
         return SGL_EINVAL;
     }
     const Plan &p = *reinterpret_cast<const Plan *>(plan);
+    if (!p.subs.empty()) {   // multi-GPU plan: sub-plan 0's geometry, node totals over the shards
+        int rc = sgl_plan_get_info(reinterpret_cast<const sgl_plan *>(p.subs[0]), info);
+        if (rc) return rc;
+        info->M = p.M;
+        info->n_gpus = (int32_t)p.subs.size();
+        for (size_t k = 1; k < p.subs.size(); ++k) {
+            sgl_plan_info s;
+            rc = sgl_plan_get_info(reinterpret_cast<const sgl_plan *>(p.subs[k]), &s);
+            if (rc) return rc;
+            info->n_tiles += s.n_tiles;
+            info->tile_nodes += s.tile_nodes;
+            info->tile_dmma += s.tile_dmma;
+            info->i8_tiles += s.i8_tiles;
+            info->i8_ksteps += s.i8_ksteps;
+            info->i8_sksteps += s.i8_sksteps;
+            info->plan_ms = std::max(info->plan_ms, s.plan_ms);
+            info->guard_fwd_fallbacks += s.guard_fwd_fallbacks;
+            info->guard_adj_fallbacks += s.guard_adj_fallbacks;
+        }
+        return SGL_OK;
+    }
+    info->n_gpus = 1;
     info->B = p.B;
     info->M = p.M;
     info->rho = p.rho;
@@ -742,6 +769,7 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
         return SGL_EINVAL;
     }
     Plan &p = *reinterpret_cast<Plan *>(plan);
+    if (!p.subs.empty()) return multi_forward(p, coeffs, K, values, stream);
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
     PlanGuard guard(p, (cudaStream_t)stream);
     if (K < 1 || !coeffs || (!values && p.M > 0)) {
@@ -800,6 +828,7 @@ int sgl_adjoint(sgl_plan *plan, const sgl_cdouble *values, sgl_cdouble *coeffs, 
         return SGL_EINVAL;
     }
     Plan &p = *reinterpret_cast<Plan *>(plan);
+    if (!p.subs.empty()) return multi_adjoint(p, values, coeffs, stream);
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
     PlanGuard guard(p, (cudaStream_t)stream);
     if (!coeffs || (!values && p.M > 0)) {
@@ -837,6 +866,10 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
         return SGL_EINVAL;
     }
     Plan &p = *reinterpret_cast<Plan *>(plan);
+    if (!p.subs.empty()) {
+        const int rc = multi_forward(p, coeffs, 1, values_out, stream);
+        return rc ? rc : multi_adjoint(p, values_in, coeffs_out, stream);
+    }
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
     PlanGuard guard(p, (cudaStream_t)stream);
     if (!coeffs || !coeffs_out || (p.M > 0 && (!values_out || !values_in))) {

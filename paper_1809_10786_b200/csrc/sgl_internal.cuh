@@ -189,6 +189,11 @@ struct Plan {
     unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
     double lap_ms = -1.0;          // SGL_FLAG_I8_PROF: plan-construction stage clock (plan_lap)
 
+    // single-process multi-GPU plan (multi.cu): one sub-plan per device over a
+    // contiguous node shard [sub_start[k], sub_start[k + 1]); empty otherwise
+    std::vector<Plan *> subs;
+    std::vector<int64_t> sub_start;
+
     // grid-partitioned multi-GPU adjoint (dist.cu): slab 2-D plans by plane count, axis-0 plan
     std::vector<std::pair<int, cufftHandle>> slab_ffts;
     cufftHandle dist_fft1 = 0;
@@ -261,6 +266,8 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
 int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaStream_t st);
 int setup_scatter_i8(Plan &p);
 int setup_guard(Plan &p);
+int multi_forward(Plan &p, const sgl_cdouble *coeffs, int64_t K, sgl_cdouble *values, void *stream);
+int multi_adjoint(Plan &p, const sgl_cdouble *values, sgl_cdouble *coeffs, void *stream);
 // SGL_FLAG_I8_PROF: synchronise and print the host time since the previous lap
 // of this plan's construction to stderr (diagnostics of plan time)
 void plan_lap(Plan &p, cudaStream_t st, const char *what);

@@ -146,7 +146,7 @@ def _stream_ptr(x) -> int | None:
 def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
          exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
          precompute: bool = True, device: int | None = None, profile: bool = False,
-         precise_tables: bool | None = None, flags: int = 0) -> SglPlan:
+         precise_tables: bool | None = None, flags: int = 0, devices=None) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
     ``backend``: "auto" (q <= 16: the int8 tensor-core gather for the
@@ -161,7 +161,10 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     "numba" / "numpy" are accepted as aliases of "auto".  ``precompute`` is
     accepted for compatibility: window weights are always evaluated on the
     fly on the device.  ``exact_last_stage=True`` replaces the window
-    evaluation by the direct NDFT on the device (O(M n^3): verification)."""
+    evaluation by the direct NDFT on the device (O(M n^3): verification).
+    ``devices``: a list of CUDA device ids -- one plan over all of them in
+    this process (node shards, one sub-plan per device, sgl_plan_create_multi);
+    the one-process-per-GPU path is `distributed.ShardedPlan`."""
     if B < 1:
         raise ValueError("bandwidth must be >= 1")
     if backend not in _BACKENDS:
@@ -218,8 +221,18 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_FP64_TABLES
     h = ctypes.c_void_p(0)
     stream = _stream_ptr(pts)
-    _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q or 0),
-                                    float(rho) if rho is not None else 0.0, flags, stream, ctypes.byref(h)))
+    if devices is not None and len(devices) > 1:
+        devs = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        _native.check(L.sgl_plan_create_multi(int(B), M, ptr if M else None, int(sigma), int(q or 0),
+                                              float(rho) if rho is not None else 0.0, flags, len(devices), devs,
+                                              ctypes.byref(h)))
+        dev = int(devices[0])
+    else:
+        if devices is not None and len(devices) == 1:
+            dev = int(devices[0])
+            _native.check(L.sgl_set_device(dev))
+        _native.check(L.sgl_plan_create(int(B), M, ptr if M else None, int(sigma), int(q or 0),
+                                        float(rho) if rho is not None else 0.0, flags, stream, ctypes.byref(h)))
     info = _native.PlanInfo()
     _native.check(L.sgl_plan_get_info(h, ctypes.byref(info)))
     nf = None if exact_last_stage else NfftInfo(

@@ -78,3 +78,31 @@ def test_two_ranks_on_one_gpu_match_single_process(name, partition, backend, tmp
         assert rel(x["a"], a1) <= 1e-11 and rel(x["a"], g["adj"]) <= 1e-10
         assert rel(x["ad"], x["a"]) <= 1e-12
     assert np.array_equal(r[0]["a"], r[1]["a"])
+
+
+@pytest.mark.parametrize("name", ["b12_q12", "cfg2_sub20k"])
+def test_single_process_multi_device_plan(name):
+    """sgl_plan_create_multi (the C ABI's n_gpus): two sub-plans -- on one
+    GPU here (devices [0, 0]); on a multi-GPU box, [0, 1] -- over node shards;
+    forward slices and summed adjoint equal the single plan and the goldens."""
+    import torch
+    import paper_1809_10786_b200 as sgl
+    g = load_golden(name)
+    kw = dict(q=int(g["q"]), rho=float(g["rho"]))
+    pm = sgl.plan(int(g["B"]), g["points"], devices=[0, 0], **kw)
+    assert pm._info.n_gpus == 2 and pm.m_points == g["points"].shape[0]
+    p1 = sgl.plan(int(g["B"]), g["points"], **kw)
+    f, a = sgl.forward(pm, g["coeffs"]), sgl.adjoint(pm, g["values"])
+    assert rel(f, sgl.forward(p1, g["coeffs"])) <= 1e-11 and rel(f, g["fwd"]) <= 1e-10
+    assert rel(a, sgl.adjoint(p1, g["values"])) <= 1e-11 and rel(a, g["adj"]) <= 1e-10
+    C = np.stack([g["coeffs"], 2 * g["coeffs"]])
+    F = sgl.forward(pm, C)
+    assert F.shape == (2, f.size) and rel(F[1], 2 * f) <= 1e-12
+    dev = torch.device("cuda", 0)
+    fd = sgl.forward(pm, torch.as_tensor(g["coeffs"], device=dev))
+    ad = sgl.adjoint(pm, torch.as_tensor(g["values"], device=dev))
+    assert rel(fd.cpu().numpy(), f) <= 1e-13 and rel(ad.cpu().numpy(), a) <= 1e-13
+    f2, a2 = sgl.forward_adjoint(pm, g["coeffs"], g["values"])
+    assert rel(f2, f) <= 1e-13 and rel(a2, a) <= 1e-13
+    with pytest.raises(ValueError):
+        sgl.plan(4, g["points"][:10], devices=[0, 99])
