@@ -11,6 +11,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libsgl_b200.so")
+# tests / tools only: SGL_LIBRARY=<path> loads another build of the same ABI
+# (the bounds-checked libsgl_b200_checked.so, build.py --checked)
+LIB_PATH = os.environ.get("SGL_LIBRARY", LIB_PATH)
 
 SGL_OK, SGL_EINVAL, SGL_ECUDA, SGL_ENOMEM, SGL_EUNSUPPORTED = 0, 1, 2, 3, 4
 FLAG_COMPACT_K1 = 1 << 0

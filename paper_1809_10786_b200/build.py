@@ -28,19 +28,26 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the B200 library cannot be built")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+CHECKED_LIB = os.path.join(LIBDIR, "libsgl_b200_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: a separate library with device-side bounds checks
+    (-DSGL_CHECKED, SGL_DCHECK in the kernels), loaded when SGL_LIBRARY points
+    at it (tests/tools only); the product library never carries them."""
+    lib = CHECKED_LIB if checked else LIB
+    if not force and not _stale(lib):
+        return lib
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj_checked" if checked else "obj")
     os.makedirs(objdir, exist_ok=True)
     base = [nvcc()]
     # /usr/bin/g++ is the host compiler with a complete toolchain in this image
@@ -48,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         base += ["-ccbin", "/usr/bin/g++"]
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-             "-I", os.path.join(HERE, "..", "include")]
+             "-I", os.path.join(HERE, "..", "include")] + (["-DSGL_CHECKED"] if checked else [])
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
@@ -66,16 +73,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed compiling {src}")
         if verbose:
             sys.stderr.write(res.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     res = subprocess.run(base + ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] +
                          [obj for _, obj, _ in results] + ["-lcufft", "-lpthread"],
                          capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libsgl_b200.so")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -135,6 +135,11 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int kc = 2 * s + h, al = kc / CHUNKS, cc = kc - CHUNKS * al;
+                        // the tile's live cells inside the padded plane (box parts beyond it are
+                        // TMA out-of-bounds reads: zero-filled, and their weights are zero)
+                        SGL_DCHECK(bb >= 0 && bb + t.e1 <= wp.N1p && t.o2 + wp.pad >= 0 &&
+                                   t.o2 + wp.pad + t.e2 <= wp.N2p && (cb >> 4) + cc >= 0 && al <= t.e0 &&
+                                   wrap1(t.o0 + al, wp.N0) >= 0 && wrap1(t.o0 + al, wp.N0) < wp.N0);
                         tma_load_4d(S.b[stg] + h * B_CHUNK, &dmap, 4 * bb, 0, (cb >> 4) + cc, wrap1(t.o0 + al, wp.N0),
                                     &S.fullB[stg]);
                     }
@@ -337,6 +342,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
             umma::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.tempty);
+            SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
             if (live) out[nodes.perm[si]] = make_double2(acc_re, acc_im);
         }
     }

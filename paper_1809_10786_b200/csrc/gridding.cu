@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(GT, GCPS)
             for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
                 const Tile t = tiles[ti];
                 const int c0 = 2 * (t.o2 + wp.pad), c1 = t.o1 + wp.pad;
+                SGL_DCHECK(c0 >= 0 && c0 + 2 * t.e2 <= 2 * wp.N2p && c1 >= 0 && c1 + t.e1 <= wp.N1p &&
+                           t.e0 <= kBox0Max);
                 for (int a = 0; a < t.e0; ++a, ++q) {
                     const int buf = (int)(q % NST);
                     const uint32_t use = q / NST;
@@ -399,6 +401,9 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     const int c = ct * 8 + 2 * kk + j;
+                    SGL_DCHECK(c >= t.e2 || (g0 >= 0 && g0 < wp.N0 && t.o1 + b + wp.pad >= 0 &&
+                                             t.o1 + b + wp.pad < wp.N1p && t.o2 + wp.pad + c >= 0 &&
+                                             t.o2 + wp.pad + c < wp.N2p));
                     if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
                 }
             }
@@ -574,6 +579,7 @@ __global__ void __launch_bounds__(NW_GEN * 32)
         ar += __shfl_xor_sync(0xffffffffu, ar, o);
         ai += __shfl_xor_sync(0xffffffffu, ai, o);
     }
+    SGL_DCHECK(nodes.perm[i] >= 0 && nodes.perm[i] < M);
     if (lane == 0) out[nodes.perm[i]] = make_double2(ar, ai);
 }
 

@@ -317,6 +317,7 @@ int order_and_tile(Plan &p, const double *a0, const double *a1, const double *a2
         SGL_CUDA_CHECK(cudaMalloc(&ns.u2, sizeof(double) * (M ? M : 1)));
         SGL_CUDA_CHECK(cudaMalloc(&ns.perm, sizeof(int32_t) * (M ? M : 1)));
     }
+    ns.n = M;
     if (M == 0) return SGL_OK;
     KeyGeom kg{p.grid[0], p.grid[1], p.grid[2], W1, W2, (p.grid[2] + W2 - 1) / W2, 0, p.q};
     const uint64_t regular = (uint64_t)((p.grid[1] + W1 - 1) / W1) * kg.P2 * (uint64_t)p.grid[0];

@@ -122,6 +122,7 @@ __global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSe
             const bool live = kn < t.count;
             const int64_t si = (int64_t)t.start + kn;
             const double u1 = live ? nodes.u1[si] : -1e9;
+            SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
             const double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
             int lo1, hi1;
             window_cells(u1, wp.q, lo1, hi1);
@@ -405,6 +406,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     for (int b = eh * (ROWS / 4); b < min(t.e1, (eh + 1) * (ROWS / 4)); ++b) {
                         const double re = S.stage[2 * b][m], im = S.stage[2 * b + 1][m];
                         double *q = gp + 2 * (size_t)b * wp.N2p;
+                        SGL_DCHECK(wrap1(t.o0 + al, wp.N0) < wp.N0 && t.o1 + wp.pad + b < wp.N1p &&
+                                   kst + cl >= 0 && kst + cl < wp.N2p);
                         if (re != 0.0) red_add(q, re);
                         if (im != 0.0) red_add(q + 1, im);
                     }

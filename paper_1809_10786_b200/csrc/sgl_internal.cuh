@@ -45,6 +45,7 @@ struct NodeSet {
     // sorted order (tile order); u_j = N_j * tau_j / (2 pi) in [0, N_j)
     double *u0 = nullptr, *u1 = nullptr, *u2 = nullptr;
     int32_t *perm = nullptr;   // sorted position -> caller index
+    int64_t n = 0;             // node count (bounds of perm / the caller arrays)
 };
 
 // The oversampled grid is stored with a periodic halo of q cells on both
@@ -214,6 +215,25 @@ struct Plan {
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
     double2 *val_buf2 = nullptr;
 };
+
+// Checked builds (python -m paper_1809_10786_b200.build --checked, -DSGL_CHECKED):
+// device-side bounds checks of every grid / TMA / output index the window
+// kernels form, trapping with the failing condition -- the stand-in for
+// compute-sanitizer memcheck, which this GPU pool does not allow.
+#ifdef SGL_CHECKED
+#define SGL_DCHECK(cond)                                                                    \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("SGL_CHECKED: %s failed at %s:%d (block %d thread %d)\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                            \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define SGL_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 // error state
 void set_error(const std::string &msg);
