@@ -122,6 +122,36 @@ __device__ __forceinline__ void digits16(double w0, const double (&w)[16], uint3
     }
 }
 
+// digits16 with an entry mask (bit e: entry e inside the node's window): the
+// bytes of masked-out entries are cleared with the same LOP3 that rebalances
+// the digits, instead of a compare + select per entry on the FP64 inputs
+// (outside the window the weights are finite, smaller than inside, and their
+// digits are discarded)
+__device__ __forceinline__ void digits16_masked(double w0, const double (&w)[16], uint32_t mask16,
+                                                uint32_t (&dw)[ND][4]) {
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t L[4], H[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double y = fma(w0, w[q4 * 4 + e], MAGIC_BAL);
+            L[e] = (uint32_t)__double2loint(y);
+            H[e] = (uint32_t)__double2hiint(y);
+        }
+        // 4 mask bits -> 4 byte masks: bit i lands at 8 i, times 0xff
+        const uint32_t bm = ((((mask16 >> (4 * q4)) & 0xfu) * 0x00204081u) & 0x01010101u) * 0xffu;
+        const uint32_t t0 = prmt(L[0], L[1], 0x5140), t1 = prmt(L[2], L[3], 0x5140);
+        const uint32_t t2 = prmt(L[0], L[1], 0x7362), t3 = prmt(L[2], L[3], 0x7362);
+        const uint32_t h0 = prmt(H[0], H[1], 0x5140), h1 = prmt(H[2], H[3], 0x5140);
+        dw[0][q4] = (prmt(t0, t1, 0x5410) ^ 0x80808080u) & bm;
+        dw[1][q4] = (prmt(t0, t1, 0x7632) ^ 0x80808080u) & bm;
+        dw[2][q4] = (prmt(t2, t3, 0x5410) ^ 0x80808080u) & bm;
+        dw[3][q4] = (prmt(t2, t3, 0x7632) ^ 0x80808080u) & bm;
+        dw[4][q4] = (prmt(h0, h1, 0x5410) ^ 0x80808080u) & bm;
+        dw[5][q4] = (prmt(h0, h1, 0x7632) ^ 0x80808080u) & bm;
+    }
+}
+
 // the 6 diagonal accumulators of one column, D_k weighted 256^k, as a double
 // in units of 256^DMIN (two exact int64 halves, two conversions)
 __device__ __forceinline__ double combine6(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4, int32_t d5,

@@ -350,9 +350,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
 #pragma unroll
                     for (int j = 8; j < 16; ++j) pw[j] = pw[j - 8] * f8;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) w2[j] = (j >= jlo && j <= jhi) ? pw[j] * g2[j] : 0.0;
+                    for (int j = 0; j < 16; ++j) w2[j] = pw[j] * g2[j];
+                    // the node's window [jlo, jhi] inside this 16-cell chunk as an entry mask
+                    const uint32_t mask = (jhi < 0 || jlo > 15)
+                                              ? 0u
+                                              : ((2u << min(15, jhi)) - 1u) & ~((1u << max(0, jlo)) - 1u);
                     uint32_t dw[ND][4];
-                    digits16(w0, w2, dw);
+                    digits16_masked(w0, w2, mask, dw);
                     const long long x2 = clock64();
                     if (use) mbar_wait(&S.emptyA[stg], (use - 1) & 1);
                     qe += clock64() - x2;
