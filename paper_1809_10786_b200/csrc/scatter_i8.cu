@@ -59,7 +59,8 @@ constexpr int A_STAGE = ND * A_DIGIT;
 constexpr int B_KBLK = ND * (ROWS / 16) * 128;   // one 8-node block of all 6 value digits
 constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (global and smem layout)
 constexpr int NWG = 8 * NGRP;            // weight generator warps (per group: 32 nodes x 8 cell groups)
-constexpr int NEW = 8;                   // epilogue warps: 2 per TMEM lane quarter, half the columns each
+constexpr int NEW = 8;                   // epilogue warps: EPW per TMEM lane quarter, 1/EPW of the columns each
+constexpr int EPW = NEW / 4;
 constexpr int ST = (2 + NWG + NEW) * 32;
 
 struct SSmem {
@@ -392,22 +393,34 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                                              wp.N2p + (kst + cl));
                 mbar_wait(&S.tfull, mc & 1);
                 umma::fence_after();
-#pragma unroll 1
-                for (int cb = eh * (ROWS / 16); cb < (eh + 1) * (ROWS / 16); ++cb) {   // 8 columns = 4 axis-1 cells x (re, im)
-                    int32_t D[NBLK][8];
-                    __syncwarp();   // tcgen05.ld is .sync.aligned
+                // software-pipelined drain, 4 columns (2 axis-1 cells x re|im) per step:
+                // the TMEM loads of step i+1 are in flight while step i converts
+                constexpr int CB4 = ROWS / 4 / EPW;   // 4-column steps of this warp
+                const int c0 = eh * CB4;
+                int32_t D[2][NBLK][4];
+                __syncwarp();   // tcgen05.ld is .sync.aligned
 #pragma unroll
-                    for (int k = 0; k < NBLK; ++k) umma::tmem_ld8(tl + (uint32_t)(k * ROWS + cb * 8), D[k]);
+                for (int k = 0; k < NBLK; ++k) umma::tmem_ld4(tl + (uint32_t)(k * ROWS + c0 * 4), D[0][k]);
+                umma::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < CB4; ++i) {
+                    const int cur = i & 1;
+                    if (i + 1 < CB4) {
+#pragma unroll
+                        for (int k = 0; k < NBLK; ++k)
+                            umma::tmem_ld4(tl + (uint32_t)(k * ROWS + (c0 + i + 1) * 4), D[cur ^ 1][k]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        S.stage[(c0 + i) * 4 + j][m] = combine6(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
+                                                                D[cur][4][j], D[cur][5][j], unit);
                     umma::tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        S.stage[cb * 8 + j][m] = combine6(D[0][j], D[1][j], D[2][j], D[3][j], D[4][j], D[5][j], unit);
                 }
                 umma::fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
                 if (inbox) {
-                    for (int b = eh * (ROWS / 4); b < min(t.e1, (eh + 1) * (ROWS / 4)); ++b) {
+                    for (int b = eh * (ROWS / 2 / EPW); b < min(t.e1, (eh + 1) * (ROWS / 2 / EPW)); ++b) {
                         const double re = S.stage[2 * b][m], im = S.stage[2 * b + 1][m];
                         double *q = gp + 2 * (size_t)b * wp.N2p;
                         SGL_DCHECK(wrap1(t.o0 + al, wp.N0) < wp.N0 && t.o1 + wp.pad + b < wp.N1p &&
