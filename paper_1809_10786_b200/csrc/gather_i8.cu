@@ -311,25 +311,27 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
             mbar_wait(&S.tfull, tc & 1, 6);
             umma::fence_after();
             double acc_re = 0.0, acc_im = 0.0;
-#pragma unroll 1
-            for (int cb = 0; cb < ROWS / 8; ++cb) {   // 8 columns = 4 axis-1 cells (re, im)
-                int32_t D[NBLK][8];
-                __syncwarp();   // tcgen05.ld is .sync.aligned: the warp must be converged
+            // software-pipelined drain, 4 columns (2 axis-1 cells x re|im) per step:
+            // the TMEM loads of step i+1 are in flight while step i converts
+            int32_t D[2][NBLK][4];
+            __syncwarp();   // tcgen05.ld is .sync.aligned: the warp must be converged
 #pragma unroll
-                for (int k = 0; k < NBLK; ++k) umma::tmem_ld8(tl + (uint32_t)(k * ROWS + cb * 8), D[k]);
-                umma::tmem_ld_wait();
-                double v[8];
+            for (int k = 0; k < NBLK; ++k) umma::tmem_ld4(tl + (uint32_t)(k * ROWS), D[0][k]);
+            umma::tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    // sum_k D_k 256^k exactly in two int64 halves, then two conversions
-                    const long long lo = (long long)D[0][j] + (long long)D[1][j] * 256 + (long long)D[2][j] * 65536 +
-                                         (long long)D[3][j] * 16777216;
-                    const long long hi = (long long)D[4][j] + (long long)D[5][j] * 256;
-                    v[j] = fma((double)hi, 4294967296.0 * unit, (double)lo * unit);
+            for (int i = 0; i < ROWS / 4; ++i) {
+                const int cur = i & 1;
+                if (i + 1 < ROWS / 4) {
+#pragma unroll
+                    for (int k = 0; k < NBLK; ++k) umma::tmem_ld4(tl + (uint32_t)(k * ROWS + (i + 1) * 4), D[cur ^ 1][k]);
                 }
+                double v[4];
 #pragma unroll
-                for (int jb = 0; jb < 4; ++jb) {
-                    const int b = cb * 4 + jb;
+                for (int j = 0; j < 4; ++j) v[j] = combine6(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
+                                                            D[cur][4][j], D[cur][5][j], unit);
+#pragma unroll
+                for (int jb = 0; jb < 2; ++jb) {
+                    const int b = i * 2 + jb;
                     const double w = (live && b >= bfirst && b <= blast) ? w1 : 0.0;
                     if (b >= bfirst) {
                         w1 *= r1;
@@ -338,6 +340,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
                     acc_re = fma(w, v[2 * jb], acc_re);
                     acc_im = fma(w, v[2 * jb + 1], acc_im);
                 }
+                umma::tmem_ld_wait();
             }
             umma::fence_before();
             __syncwarp();
