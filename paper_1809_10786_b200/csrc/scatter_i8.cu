@@ -52,7 +52,7 @@ constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
 constexpr int NGRP = 2;                  // generator groups, alternating K-steps (group = ring stage)
 constexpr int NSTG = NGRP < 2 ? 2 : NGRP;              // weight-digit ring (one stage per generator group) (K-steps of 32 nodes)
-constexpr int NSTGB = 2;                 // value-digit ring
+constexpr int NSTGB = 3;                 // value-digit ring
 constexpr int KST = 32;                  // nodes per K-step
 constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 4 node blocks x 8 cell blocks x 128 B (MN-major)
 constexpr int A_STAGE = ND * A_DIGIT;
