@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--partition", default="auto", choices=["auto", "coeffs", "grid"])
     ap.add_argument("--no-stock", action="store_true", help="skip timing the stock reference package")
+    ap.add_argument("--backend", default="auto", choices=["auto", "tiled", "i8"],
+                    help="window engines (experiments; the default is the library's own choice)")
     return ap.parse_args()
 
 
@@ -337,12 +339,12 @@ def main():
     v_d = torch.as_tensor(w.values, device=dev)
     t0 = time.perf_counter()
     # rho is global (all-reduce max over the ranks' shards) -- distributed.ShardedPlan
-    sp = ShardedPlan(w.B, pts_d, device=local, partition=args.partition) if world > 1 else None
-    p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local)
+    sp = ShardedPlan(w.B, pts_d, device=local, partition=args.partition, backend=args.backend) if world > 1 else None
+    p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local, backend=args.backend)
     rho = sp.rho if sp is not None else p.rho
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - t0
-    pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True)
+    pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True, backend=args.backend)
     stream = torch.cuda.current_stream(dev)
 
     def step(pl):

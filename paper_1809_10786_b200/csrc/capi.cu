@@ -43,6 +43,17 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory
+bool is_pinned_host(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 int fft_check(cufftResult r, const char *what) {
     if (r != CUFFT_SUCCESS) {
         set_error(std::string("cuFFT error ") + std::to_string((int)r) + " in " + what);
@@ -81,6 +92,7 @@ void free_plan(Plan *p) {
     if (p->ev_a) cudaEventDestroy(p->ev_a);
     if (p->ev_b) cudaEventDestroy(p->ev_b);
     if (p->ev_c) cudaEventDestroy(p->ev_c);
+    if (p->ev_d) cudaEventDestroy(p->ev_d);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     if (p->val_buf2) cudaFree(p->val_buf2);
     for (auto &t : p->timers)
@@ -155,6 +167,7 @@ cudaError_t ensure_side(Plan &p) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_a, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_b, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_c, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_d, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking);
     return e;
 }
@@ -227,6 +240,20 @@ int adjoint_tail(Plan &p, double2 *c, cudaStream_t st, StageRec *rec) {
     return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
 }
 
+// the int8 scatter's accuracy decision (after guard_adjoint_estimate): read
+// the flag on the host; above the bound, rerun the adjoint on the FP64 scatter
+int adjoint_guard_resolve(Plan &p, const double2 *v, double2 *c, cudaStream_t st) {
+    if (!(p.i8s && p.guard_on && p.guard_ap > 0.0 && p.M > 0)) return SGL_OK;
+    int redo = 0;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(&redo, &p.guard->adj_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (!redo) return SGL_OK;
+    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
+    int rc = launch_scatter(p, v, p.grid_buf, st);
+    if (rc) return rc;
+    return adjoint_tail(p, c, st, nullptr);
+}
+
 // may_sync: the int8 scatter's accuracy check reads its flag on the host
 // (not possible inside a CUDA-graph capture, where it is skipped)
 int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRec *rec, bool may_sync = true) {
@@ -249,14 +276,7 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
     // int8 scatter accuracy check (guard.cu): estimate from the result, rerun on FP64 above the bound
     rc = guard_adjoint_estimate(p, v, c, st);
     if (rc || !(p.guard_on && may_sync)) return rc;
-    int redo = 0;
-    SGL_CUDA_CHECK(cudaMemcpyAsync(&redo, &p.guard->adj_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SGL_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (!redo) return SGL_OK;
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    rc = launch_scatter(p, v, p.grid_buf, st);
-    if (rc) return rc;
-    return adjoint_tail(p, c, st, nullptr);
+    return adjoint_guard_resolve(p, v, c, st);
 }
 
 }  // namespace
@@ -779,10 +799,22 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
     cudaStream_t st = (cudaStream_t)stream;
     const bool cdev = is_device_ptr(coeffs), vdev = values ? is_device_ptr(values) : true;
     // K > 1 into host memory: double-buffer the values and download vector k
-    // on the side stream while vector k+1 is computed
+    // on the side stream while vector k+1 is computed.  Vector k+1 is enqueued
+    // BEFORE the download of vector k is issued: with pageable (not pinned)
+    // user memory the download call blocks the host until it completes, and
+    // the GPU must already hold the next vector's work by then.
     const bool overlap = !vdev && p.M > 0 && K > 1;
     if (overlap) SGL_CUDA_CHECK(ensure_side(p));
     StageRec rec(p, 0, st);
+    cudaEvent_t drained[2] = {p.ev_a, p.ev_b}, computed[2] = {p.ev_c, p.ev_d};
+    auto download = [&](int64_t k) -> int {   // vector k: val_buf / val_buf2 -> host, side stream
+        double2 *v = (k & 1) ? p.val_buf2 : p.val_buf;
+        SGL_CUDA_CHECK(cudaStreamWaitEvent(p.copy_stream, computed[k & 1], 0));
+        SGL_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<double2 *>(values) + k * p.M, v, sizeof(double2) * p.M,
+                                       cudaMemcpyDeviceToHost, p.copy_stream));
+        SGL_CUDA_CHECK(cudaEventRecord(drained[k & 1], p.copy_stream));
+        return SGL_OK;
+    };
     for (int64_t k = 0; k < K; ++k) {
         rec.mark(SGL_STAGE_H2D);
         const double2 *c = reinterpret_cast<const double2 *>(coeffs) + k * p.count;
@@ -790,29 +822,27 @@ int sgl_forward(sgl_plan *plan, const sgl_cdouble *coeffs, int64_t K, sgl_cdoubl
             SGL_CUDA_CHECK(cudaMemcpyAsync(p.coef_buf, c, sizeof(double2) * p.count, cudaMemcpyHostToDevice, st));
             c = p.coef_buf;
         }
-        double2 *host_v = vdev ? nullptr : reinterpret_cast<double2 *>(values) + k * p.M;
-        double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : p.val_buf;
-        cudaEvent_t drained = p.ev_a;
-        if (overlap && (k & 1)) {
-            v = p.val_buf2;
-            drained = p.ev_b;
-        }
-        if (overlap && k >= 2) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, drained, 0));   // download of k-2 done
+        double2 *v = vdev ? reinterpret_cast<double2 *>(values) + k * p.M : ((overlap && (k & 1)) ? p.val_buf2 : p.val_buf);
+        if (overlap && k >= 2) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, drained[k & 1], 0));   // download of k-2 done
         const int rc = forward_core(p, c, v, st, &rec);
         if (rc) return rc;
         rec.mark(SGL_STAGE_D2H);
         if (overlap) {
-            SGL_CUDA_CHECK(cudaEventRecord(p.ev_c, st));
-            SGL_CUDA_CHECK(cudaStreamWaitEvent(p.copy_stream, p.ev_c, 0));
-            SGL_CUDA_CHECK(cudaMemcpyAsync(host_v, v, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, p.copy_stream));
-            SGL_CUDA_CHECK(cudaEventRecord(drained, p.copy_stream));
+            SGL_CUDA_CHECK(cudaEventRecord(computed[k & 1], st));
+            if (k >= 1) {
+                const int r = download(k - 1);
+                if (r) return r;
+            }
         } else if (!vdev && p.M > 0) {
-            SGL_CUDA_CHECK(cudaMemcpyAsync(host_v, v, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, st));
+            SGL_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<double2 *>(values) + k * p.M, v, sizeof(double2) * p.M,
+                                           cudaMemcpyDeviceToHost, st));
         }
         rec.mark(SGL_STAGE_COUNT);
         rec.flush();
     }
-    if (overlap) {   // join the side stream back into st
+    if (overlap) {   // the last vector, then join the side stream back into st
+        const int r = download(K - 1);
+        if (r) return r;
         SGL_CUDA_CHECK(cudaEventRecord(p.ev_c, p.copy_stream));
         SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_c, 0));
     }
@@ -882,6 +912,12 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
     const bool cdev = is_device_ptr(coeffs), codev = is_device_ptr(coeffs_out);
     const bool vodev = values_out ? is_device_ptr(values_out) : true;
     const bool videv = values_in ? is_device_ptr(values_in) : true;
+    // Pinned host buffers: copies are truly asynchronous, queued on the side
+    // stream up front.  Pageable ones: cudaMemcpyAsync blocks the host until
+    // the copy is done, so each is issued only after the kernels it should
+    // overlap are enqueued (value upload after the forward, value download
+    // after the adjoint).
+    const bool vin_pinned = !videv && is_pinned_host(values_in), vout_pinned = !vodev && is_pinned_host(values_out);
     // coefficients first: a copy queued behind the large value upload would
     // hold up the forward (copies in one direction share an engine queue)
     const double2 *c = reinterpret_cast<const double2 *>(coeffs);
@@ -889,27 +925,43 @@ int sgl_forward_adjoint(sgl_plan *plan, const sgl_cdouble *coeffs, sgl_cdouble *
         SGL_CUDA_CHECK(cudaMemcpyAsync(p.coef_buf, c, sizeof(double2) * p.count, cudaMemcpyHostToDevice, st));
         c = p.coef_buf;
     }
-    // adjoint input: H2D on the side stream, overlapped with the forward
     const double2 *vin = reinterpret_cast<const double2 *>(values_in);
-    if (!videv && p.M > 0) {
+    auto upload = [&]() -> int {   // adjoint input: H2D on the side stream, overlapped with the forward
         SGL_CUDA_CHECK(cudaEventRecord(p.ev_a, st));   // the plan's previous work is ordered before
         SGL_CUDA_CHECK(cudaStreamWaitEvent(cs, p.ev_a, 0));
-        SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf2, vin, sizeof(double2) * p.M, cudaMemcpyHostToDevice, cs));
+        SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf2, values_in, sizeof(double2) * p.M, cudaMemcpyHostToDevice, cs));
         SGL_CUDA_CHECK(cudaEventRecord(p.ev_a, cs));   // the adjoint waits on this upload only
+        return SGL_OK;
+    };
+    if (!videv && p.M > 0) {
+        if (vin_pinned) {
+            const int r = upload();
+            if (r) return r;
+        }
         vin = p.val_buf2;
     }
     double2 *vout = vodev ? reinterpret_cast<double2 *>(values_out) : p.val_buf;
     int rc = forward_core(p, c, vout, st, nullptr);
     if (rc) return rc;
+    if (!videv && p.M > 0 && !vin_pinned) {
+        rc = upload();   // pageable: blocks the host while the GPU runs the forward
+        if (rc) return rc;
+    }
     // forward output: D2H on the side stream, overlapped with the adjoint
     SGL_CUDA_CHECK(cudaEventRecord(p.ev_b, st));
     SGL_CUDA_CHECK(cudaStreamWaitEvent(cs, p.ev_b, 0));
-    if (!vodev && p.M > 0)
+    if (!vodev && p.M > 0 && vout_pinned)
         SGL_CUDA_CHECK(cudaMemcpyAsync(values_out, p.val_buf, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, cs));
     if (!videv && p.M > 0) SGL_CUDA_CHECK(cudaStreamWaitEvent(st, p.ev_a, 0));
     double2 *cout = codev ? reinterpret_cast<double2 *>(coeffs_out) : p.coef_buf;
-    rc = adjoint_core(p, vin, cout, st, nullptr, !guard.capturing);
+    rc = adjoint_core(p, vin, cout, st, nullptr, false);   // enqueue only; the guard decision follows
     if (rc) return rc;
+    if (!vodev && p.M > 0 && !vout_pinned)   // pageable: blocks the host while the GPU runs the adjoint
+        SGL_CUDA_CHECK(cudaMemcpyAsync(values_out, p.val_buf, sizeof(double2) * p.M, cudaMemcpyDeviceToHost, cs));
+    if (!guard.capturing) {
+        rc = adjoint_guard_resolve(p, vin, cout, st);
+        if (rc) return rc;
+    }
     if (!codev)
         SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs_out, p.coef_buf, sizeof(double2) * p.count, cudaMemcpyDeviceToHost, st));
     // join the side stream back into st (the next call on this plan reuses val_buf)

@@ -212,7 +212,7 @@ struct Plan {
     // host memory): side stream for the host copies, events, a second value
     // buffer; created on first use
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr;
     double2 *val_buf2 = nullptr;
 };
 

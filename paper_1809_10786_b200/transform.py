@@ -311,7 +311,11 @@ def forward_adjoint(p: SglPlan, coeffs, values):
 
     The two inputs are independent; with host (numpy) arrays the library
     overlaps the value upload with the forward and the value download with
-    the adjoint (sgl_forward_adjoint).  Same checks as `forward`/`adjoint`."""
+    the adjoint (sgl_forward_adjoint): fully asynchronously for page-locked
+    arrays (e.g. ``torch.empty(..., pin_memory=True).numpy()``); for ordinary
+    pageable arrays each copy is issued after the kernels it overlaps are
+    enqueued (the copy call blocks the host, the GPU keeps computing).  Same
+    checks as `forward`/`adjoint`."""
     cnt, M = p.count, p.m_points
     L = _native.lib()
     if _is_torch(coeffs) or _is_torch(values):
