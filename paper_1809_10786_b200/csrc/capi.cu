@@ -76,7 +76,7 @@ void free_plan(Plan *p) {
     void *bufs[] = {p->nodes.u0, p->nodes.u1, p->nodes.u2, p->nodes.perm, p->snodes.u0, p->snodes.u1, p->snodes.u2,
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
-                    p->coef_buf, p->val_buf, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
+                    p->coef_buf, p->val_buf, p->zeta, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
                     p->itiles, p->digits, p->gmax, p->istiles, p->tsv, p->svoff, p->vdig, p->guard, p->prof};
     for (void *b : bufs)
         if (b) cudaFree(b);
@@ -491,7 +491,10 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         if (cudaMalloc(&p->grid_buf, sizeof(double2) * p->grid_elems) != cudaSuccess ||
             cudaMalloc(&p->beta, sizeof(double2) * (size_t)std::max(1, p->B * p->B * 4 * p->B)) != cudaSuccess ||
             cudaMalloc(&p->coef_buf, sizeof(double2) * p->count) != cudaSuccess ||
-            cudaMalloc(&p->val_buf, sizeof(double2) * (M ? M : 1)) != cudaSuccess) {
+            cudaMalloc(&p->val_buf, sizeof(double2) * (M ? M : 1)) != cudaSuccess ||
+            (!p->raw &&
+             cudaMalloc(&p->zeta, sizeof(double2) * (size_t)(2 * p->B - 1) * p->n_axis[1] * (4 * p->B)) !=
+                 cudaSuccess)) {
             cudaGetLastError();
             set_error("out of device memory for the plan's grid / staging buffers");
             rc = SGL_ENOMEM;

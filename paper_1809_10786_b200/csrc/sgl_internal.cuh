@@ -148,6 +148,7 @@ struct Plan {
     alignas(64) CUtensorMap tmap;  // TMA descriptor of grid_buf (FLOAT64 view)
     bool tmap_ready = false;
     double2 *beta = nullptr;       // B^2 x 4B complex
+    double2 *zeta = nullptr;       // (2B-1) x n1 x 4B complex: the adjoint's cropped spectrum, m-major
     double2 *coef_buf = nullptr;   // count complex (staging)
     double2 *val_buf = nullptr;    // M complex (staging)
     size_t grid_elems = 0;
