@@ -309,7 +309,9 @@ int sgl_device_count(int32_t *n) {
     return SGL_OK;
 }
 
-const char *sgl_version(void) { return "sgl-b200 0.1.0 (sm_100a, FP64 DMMA gridding)"; }
+const char *sgl_version(void) {
+    return "sgl-b200 0.2.0 (sm_100a: int8 tcgen05 window engines with an FP64 accuracy guard, FP64 DMMA gridding)";
+}
 
 int sgl_plan_create(int32_t B, int64_t M, const double *points, int32_t sigma, int32_t q, double rho,
                     uint32_t flags, void *stream, sgl_plan **out) {
