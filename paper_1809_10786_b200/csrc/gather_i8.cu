@@ -239,7 +239,11 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
             const int a_first = max(0, lo0 - t.o0), a_last = hi0 - t.o0;
             const int sGt = __ldg(tsh + ti);
             double wcur = 0.0, rcur = 0.0;
+            // slab shifts loaded one slab ahead (their L1/L2 latency off the digit chain)
+            int sh_next = __ldg(gsh + wrap1(t.o0, wp.N0));
             for (int kc = cc, al = 0; kc < 2 * ns; kc += CHUNKS, ++al) {
+                const int sh_al = sh_next;
+                if (kc + CHUNKS < 2 * ns) sh_next = __ldg(gsh + wrap1(t.o0 + al + 1, wp.N0));
                 // W0 of slab al (recurrence from the node's first window slab)
                 if (al == a_first) {
                     const double d0 = u0 - (double)(t.o0 + al);
@@ -249,7 +253,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
                     wcur *= rcur;
                     rcur *= wp.r0_1;
                 }
-                const double fslab = pow2n(sGt - __ldg(gsh + wrap1(t.o0 + al, wp.N0)));   // slab -> tile scale
+                const double fslab = pow2n(sGt - sh_al);   // slab -> tile scale
                 const double w0 = (live && al >= a_first && al <= a_last) ? wcur * fslab : 0.0;
                 const uint32_t gs = g + (uint32_t)(kc >> 1);
                 const int stg = (int)(gs % NSTG), h = kc & 1;
