@@ -89,6 +89,13 @@ __device__ __forceinline__ void st_async_v4(void *dst, const uint32_t (&v)[4], u
 
 __device__ __forceinline__ int64_t tile_steps(const Tile &t) { return (CHUNKS * t.e0 + 1) >> 1; }
 
+template <bool P>
+__device__ __forceinline__ long long tick() {
+    if constexpr (P) return clock64();
+    else return 0;
+}
+
+template <bool PROF>   // PROF: clock64 wait counters (SGL_FLAG_I8_PROF); compiled out otherwise
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
     k_gather_i8(const __grid_constant__ CUtensorMap dmap, const Tile *__restrict__ tiles, int64_t ntiles,
                 NodeSet nodes, WindowParams wp, double s0, double s2, int sA,
@@ -153,21 +160,21 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
         const uint64_t a0 = umma::desc_kmajor(umma::smem_addr(S.a[0]), A_CHUNK, 128);
         const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_CHUNK, 128);
         uint32_t g = 0, tc = 0;
-        long long pw_a = 0, pw_b = 0, pw_e = 0, pt0 = clock64();
+        long long pw_a = 0, pw_b = 0, pw_e = 0, pt0 = tick<PROF>();
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tc) {
             const int ns = (int)tile_steps(tiles[ti]);
-            long long t0 = clock64();
+            long long t0 = tick<PROF>();
             if (tc) mbar_wait(&S.tempty, (tc - 1) & 1, 2);
             umma::fence_after();
-            long long t1 = clock64();
+            long long t1 = tick<PROF>();
             pw_e += t1 - t0;
             for (int s = 0; s < ns; ++s, ++g) {
                 const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
-                t0 = clock64();
+                t0 = tick<PROF>();
                 mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1, 3);
-                t1 = clock64();
+                t1 = tick<PROF>();
                 mbar_wait(&S.fullA[stg], (g / NSTG) & 1, 4);
-                long long t2 = clock64();
+                long long t2 = tick<PROF>();
                 pw_b += t1 - t0;
                 pw_a += t2 - t1;
                 umma::fence_after();
@@ -199,8 +206,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
             if (umma::elect_one()) umma::commit(&S.tfull);
             __syncwarp();
         }
-        if (prof && lane == 0) {
-            prof[blockIdx.x * 4 + 0] = clock64() - pt0;
+        if (PROF && prof && lane == 0) {
+            prof[blockIdx.x * 4 + 0] = tick<PROF>() - pt0;
             prof[blockIdx.x * 4 + 1] = pw_a;
             prof[blockIdx.x * 4 + 2] = pw_b;
             prof[blockIdx.x * 4 + 3] = pw_e;
@@ -534,11 +541,12 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     int sA;
     i8_scales(p, s0, s2, sA);
     const size_t sm = sizeof(I8Smem);
-    SGL_CUDA_CHECK(cudaFuncSetAttribute(k_gather_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
     unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
     const bool want_prof = prof != nullptr;
-    k_gather_i8<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA, gsh,
+    auto kern = want_prof ? k_gather_i8<true> : k_gather_i8<false>;
+    SGL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_itiles, sms));
+    kern<<<(unsigned)blocks, IT, sm, st>>>(p.dmap, p.itiles, p.n_itiles, p.inodes, p.wp, s0, s2, sA, gsh,
                                                   tsh, values, prof, &p.guard->fwd);
     if (want_prof) {
         std::vector<unsigned long long> h(4 * blocks);

@@ -151,6 +151,13 @@ __global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSe
     }
 }
 
+template <bool P>
+__device__ __forceinline__ long long tick() {
+    if constexpr (P) return clock64();
+    else return 0;
+}
+
+template <bool PROF>   // PROF: clock64 wait counters (SGL_FLAG_I8_PROF); compiled out otherwise
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
                  double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
@@ -186,22 +193,22 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);    // block, SBO = 16 rows
         constexpr uint32_t MN = (1u << 15) | (1u << 16);                                // A, B MN-major
         uint32_t g = 0, mc = 0;
-        long long q0 = clock64(), qa = 0, qb = 0, qe = 0;
+        long long q0 = tick<PROF>(), qa = 0, qb = 0, qe = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
-                long long x0 = clock64();
+                long long x0 = tick<PROF>();
                 if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
-                qe += clock64() - x0;
+                qe += tick<PROF>() - x0;
                 umma::fence_after();
                 for (int ks = 0; ks < nks; ++ks, ++g) {
                     const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
-                    long long x1 = clock64();
+                    long long x1 = tick<PROF>();
                     mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1);
-                    long long x2 = clock64();
+                    long long x2 = tick<PROF>();
                     mbar_wait(&S.fullA[stg], (g / NSTG) & 1);
-                    qa += clock64() - x2;
+                    qa += tick<PROF>() - x2;
                     qb += x2 - x1;
                     umma::fence_after();
                     if (umma::elect_one()) {
@@ -232,8 +239,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 __syncwarp();
             }
         }
-        if (prof && lane == 0) {
-            prof[blockIdx.x * 8 + 0] = clock64() - q0;
+        if (PROF && prof && lane == 0) {
+            prof[blockIdx.x * 8 + 0] = tick<PROF>() - q0;
             prof[blockIdx.x * 8 + 1] = qa;
             prof[blockIdx.x * 8 + 2] = qb;
             prof[blockIdx.x * 8 + 3] = qe;
@@ -274,10 +281,10 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         const int gt = tid - 64, hg = gt >> 8, wi = (gt >> 5) & 7;
         const int kl = (wi & 3) * 8 + (lane & 7), grp = (wi >> 2) * 4 + (lane >> 3);
         uint32_t g = 0;
-        long long q0 = clock64(), qe = 0, qt = 0, qw = 0;
+        long long q0 = tick<PROF>(), qe = 0, qt = 0, qw = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
-            const long long x0 = clock64();
+            const long long x0 = tick<PROF>();
             gen_sync();   // the previous tile's readers of the node tables are done
             const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
             const int kcount = ksteps(t) * KST;
@@ -308,11 +315,11 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 }
             }
             gen_sync();
-            qt += clock64() - x0;
+            qt += tick<PROF>() - x0;
             const int nmb = mblocks(t), nks = ksteps(t);
             int nxt = 0;   // next slab of the W0 walk
             for (int mb = 0; mb < nmb; ++mb) {
-                const long long x1 = clock64();
+                const long long x1 = tick<PROF>();
                 // W0 of the slabs this M-block adds (slabs a_mb .. a_mb + 3, each
                 // computed once per tile, in order, by the walk; zero beyond e0)
                 const int a_mb = (mb * 8) / CHUNKS;
@@ -336,7 +343,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     nxt = a_mb + 4;
                     gen_sync();
                 }
-                qw += clock64() - x1;
+                qw += tick<PROF>() - x1;
                 const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
                 // this thread's node tables for the M-block (padding nodes have e = 0)
                 const double *w0p = S.w0t[al & 3] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
@@ -369,9 +376,9 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                                               : ((2u << min(15, jhi)) - 1u) & ~((1u << max(0, jlo)) - 1u);
                     uint32_t dw[ND][4];
                     digits16_masked(w0, w2, mask, dw);
-                    const long long x2 = clock64();
+                    const long long x2 = tick<PROF>();
                     if (use) mbar_wait(&S.emptyA[stg], (use - 1) & 1);
-                    qe += clock64() - x2;
+                    qe += tick<PROF>() - x2;
                     if ((gt & 255) == 0) mbar_expect_tx(&S.fullA[stg], A_STAGE);
                     uint8_t *dst = S.a[stg] + (kl >> 3) * 1024 + grp * 128 + (kl & 7) * 16;
 #pragma unroll
@@ -379,8 +386,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 }
             }
         }
-        if (prof && gt == 0) {
-            prof[blockIdx.x * 8 + 4] = clock64() - q0;
+        if (PROF && prof && gt == 0) {
+            prof[blockIdx.x * 8 + 4] = tick<PROF>() - q0;
             prof[blockIdx.x * 8 + 5] = qe;
             prof[blockIdx.x * 8 + 6] = qt;
             prof[blockIdx.x * 8 + 7] = qw;
@@ -554,13 +561,14 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
     const int sA = 46 - e, a0 = sA / 2;
     const size_t sm = sizeof(SSmem);
-    SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
+    const bool want = prof != nullptr;
+    auto kern = want ? k_scatter_i8<true> : k_scatter_i8<false>;
+    SGL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
-    unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
-    const bool want = prof != nullptr;
-    k_scatter_i8<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
+    kern<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
                                                   reinterpret_cast<double *>(grid), g2, prof, skip);
     SGL_CUDA_CHECK(cudaGetLastError());
