@@ -52,8 +52,8 @@ using namespace i8;
 
 constexpr int IM = kI8Nodes;              // MMA M (nodes)
 constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
-constexpr int NSTG = 5;                   // weight-digit ring depth (K-steps of 32)
-constexpr int NSTGB = 7;                  // grid-digit (TMA) ring depth: hides the L2 latency
+constexpr int NSTG = 4;                   // weight-digit ring depth (K-steps of 32)
+constexpr int NSTGB = 8;                  // grid-digit (TMA) ring depth: hides the L2 latency
 constexpr int A_DIGIT = IM * 16;          // one K-chunk of one weight digit (2048 B)
 constexpr int A_CHUNK = ND * A_DIGIT;
 constexpr int A_STAGE = 2 * A_CHUNK;

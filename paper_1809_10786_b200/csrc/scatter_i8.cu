@@ -193,6 +193,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         const uint64_t b0 = umma::desc_kmajor(umma::smem_addr(S.b[0]), B_KBLK, 128);    // block, SBO = 16 rows
         constexpr uint32_t MN = (1u << 15) | (1u << 16);                                // A, B MN-major
         uint32_t g = 0, mc = 0;
+        int stgb = 0;            // value ring slot and phase, stepped (NSTGB is not a power of 2)
+        uint32_t phb = 0;
         long long q0 = tick<PROF>(), qa = 0, qb = 0, qe = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
             const Tile t = tiles[ti];
@@ -203,9 +205,9 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 qe += tick<PROF>() - x0;
                 umma::fence_after();
                 for (int ks = 0; ks < nks; ++ks, ++g) {
-                    const int stg = (int)(g % NSTG), stgb = (int)(g % NSTGB);
+                    const int stg = (int)(g % NSTG);
                     long long x1 = tick<PROF>();
-                    mbar_wait(&S.fullB[stgb], (g / NSTGB) & 1);
+                    mbar_wait(&S.fullB[stgb], phb);
                     long long x2 = tick<PROF>();
                     mbar_wait(&S.fullA[stg], (g / NSTG) & 1);
                     qa += tick<PROF>() - x2;
@@ -234,6 +236,10 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                         umma::commit(&S.emptyB[stgb]);
                     }
                     __syncwarp();
+                    if (++stgb == NSTGB) {
+                        stgb = 0;
+                        phb ^= 1;
+                    }
                 }
                 if (umma::elect_one()) umma::commit(&S.tfull);
                 __syncwarp();
@@ -249,6 +255,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         // ---- value-digit producer: one bulk copy per K-step (re-read from L2 per M-block)
         if (lane == 0) {
             uint32_t g = 0;
+            int pstg = 0;        // ring slot and the phase of its current use
+            uint32_t pph = 0;
             for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
                 const Tile t = tiles[ti];
                 const int nmb = mblocks(t), nks = ksteps(t);
@@ -266,11 +274,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 }
                 for (int mb = 0; mb < nmb; ++mb)
                     for (int ks = 0; ks < nks; ++ks, ++g) {
-                        const int stg = (int)(g % NSTGB);
-                        const uint32_t use = g / NSTGB;
-                        if (use) mbar_wait(&S.emptyB[stg], (use - 1) & 1);
-                        mbar_expect_tx(&S.fullB[stg], B_STAGE);
-                        bulk_load(S.b[stg], src + ks * (int64_t)B_STAGE, B_STAGE, &S.fullB[stg]);
+                        if (g >= (uint32_t)NSTGB) mbar_wait(&S.emptyB[pstg], pph ^ 1);   // its previous use
+                        mbar_expect_tx(&S.fullB[pstg], B_STAGE);
+                        bulk_load(S.b[pstg], src + ks * (int64_t)B_STAGE, B_STAGE, &S.fullB[pstg]);
+                        if (++pstg == NSTGB) {
+                            pstg = 0;
+                            pph ^= 1;
+                        }
                     }
             }
         }
