@@ -108,17 +108,22 @@ __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1
 
 // value digits of every K-step of every tile (once per adjoint): thread =
 // (node of the K-step, 16-column group = 8 axis-1 cells x re|im)
-__global__ void k_vdigits(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
-                          const double2 *__restrict__ values, const int *__restrict__ tsv,
-                          const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig, const int *__restrict__ skip) {
+__global__ void k_vdigits(const Tile *__restrict__ tiles, const int *__restrict__ ktile, int64_t nksteps,
+                          NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
+                          const int *__restrict__ tsv, const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig,
+                          const int *__restrict__ skip) {
     if (*skip) return;   // non-finite values: the gated FP64 scatter runs instead (guard.cu)
     const int kl = threadIdx.x & 31, vg = threadIdx.x >> 5;   // 5 warps = 5 column groups
-    for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    // one K-step per block iteration over the flat K-step index of all tiles
+    // (many K-steps in flight: the value gather through perm is latency-bound)
+    for (int64_t gk = blockIdx.x; gk < nksteps; gk += gridDim.x) {
+        const int64_t ti = ktile[gk];
         const Tile t = tiles[ti];
         const int svt = tsv[ti];
         const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);
         const int bb = t.o1 + vg * 8;
-        for (int ks = 0; ks < ksteps(t); ++ks) {
+        {
+            const int ks = (int)(gk - voff[ti]);
             const int kn = ks * KST + kl;
             const bool live = kn < t.count;
             const int64_t si = (int64_t)t.start + kn;
@@ -470,6 +475,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     }
 }
 
+// tile index of every K-step (the inverse of voff)
+__global__ void k_ktile(const int64_t *__restrict__ voff, int64_t ntiles, int *__restrict__ ktile) {
+    const int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ti >= ntiles) return;
+    for (int64_t k = voff[ti]; k < voff[ti + 1]; ++k) ktile[k] = (int)ti;
+}
+
 // K-steps of 32 nodes per tile (0 past the end: the scan's last entry is the total)
 __global__ void k_tile_ksteps(const Tile *__restrict__ tiles, int64_t n, int64_t *ks) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -551,9 +563,17 @@ int setup_scatter_i8(Plan &p) {
         SGL_CUDA_CHECK(cudaMalloc(&tmp, tb));
         cub::DeviceScan::ExclusiveSum(tmp, tb, ks, p.svoff, (int)(p.n_istiles + 1));
         SGL_CUDA_CHECK(cudaGetLastError());
-        SGL_CUDA_CHECK(cudaDeviceSynchronize());
+        SGL_CUDA_CHECK(cudaMemcpy(&p.n_sksteps, p.svoff + p.n_istiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
         cudaFree(tmp);
         cudaFree(ks);
+        if (cudaMalloc(&p.sktile, sizeof(int) * std::max<int64_t>(1, p.n_sksteps)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("out of device memory for the int8 scatter K-step map");
+            return SGL_ENOMEM;
+        }
+        k_ktile<<<(unsigned)((p.n_istiles + 255) / 256), 256>>>(p.svoff, p.n_istiles, p.sktile);
+        SGL_CUDA_CHECK(cudaGetLastError());
+        SGL_CUDA_CHECK(cudaDeviceSynchronize());
     }
     return SGL_OK;
 }
@@ -565,8 +585,8 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
                                                          skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int sms = num_sms();
-    k_vdigits<<<(unsigned)std::min<int64_t>(p.n_istiles, (int64_t)sms * 12), (ROWS / 16) * 32, 0, st>>>(
-        p.istiles, p.n_istiles, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig, skip);
+    k_vdigits<<<(unsigned)std::min<int64_t>(p.n_sksteps, (int64_t)sms * 64), (ROWS / 16) * 32, 0, st>>>(
+        p.istiles, p.sktile, p.n_sksteps, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig, skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
     const int sA = 46 - e, a0 = sA / 2;
