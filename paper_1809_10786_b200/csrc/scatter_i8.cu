@@ -266,17 +266,6 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 const Tile t = tiles[ti];
                 const int nmb = mblocks(t), nks = ksteps(t);
                 const uint8_t *src = vdig + voff[ti] * (int64_t)B_STAGE;
-                // warm L2 with the NEXT tile's value digits (its first M-block would
-                // otherwise stream them from DRAM): one bulk L2 prefetch per K-step
-                const int64_t tn = ti + gridDim.x;
-                if (tn < ntiles) {
-                    const uint8_t *nsrc = vdig + voff[tn] * (int64_t)B_STAGE;
-                    const int nks_n = ksteps(tiles[tn]);
-                    for (int ks = 0; ks < nks_n; ++ks)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nsrc + ks * (int64_t)B_STAGE),
-                                     "r"((uint32_t)B_STAGE)
-                                     : "memory");
-                }
                 for (int mb = 0; mb < nmb; ++mb)
                     for (int ks = 0; ks < nks; ++ks, ++g) {
                         if (g >= (uint32_t)NSTGB) mbar_wait(&S.emptyB[pstg], pph ^ 1);   // its previous use
