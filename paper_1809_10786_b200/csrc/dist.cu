@@ -62,6 +62,24 @@ __global__ void k_unpack_crop(const double2 *__restrict__ in, WindowParams wp, i
     }
 }
 
+// The plan's call serialisation (as PlanGuard in capi.cu): host threads by the
+// mutex, streams by waiting on the previous call's completion event.
+struct StageGuard {
+    Plan &p;
+    cudaStream_t st;
+    std::lock_guard<std::mutex> lock;
+    bool capturing = false;
+    StageGuard(Plan &pl, cudaStream_t s) : p(pl), st(s), lock(pl.mu) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) cudaGetLastError();
+        capturing = cs != cudaStreamCaptureStatusNone;
+        if (p.done && !capturing) cudaStreamWaitEvent(st, p.done, 0);
+    }
+    ~StageGuard() {
+        if (p.done && !capturing) cudaEventRecord(p.done, st);
+    }
+};
+
 int check_sgl(const Plan &p) {
     if (p.raw || p.exact || p.M < 0) {
         set_error("the partitioned adjoint needs a fast SGL plan (not an NFFT or exact-stage plan)");
@@ -117,8 +135,8 @@ int sgl_adjoint_spread(sgl_plan *plan, const sgl_cdouble *values, void *stream) 
         return SGL_EINVAL;
     }
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
-    std::lock_guard<std::mutex> lock(p.mu);
     cudaStream_t st = (cudaStream_t)stream;
+    StageGuard guard(p, st);
     const double2 *v = reinterpret_cast<const double2 *>(values);
     cudaPointerAttributes a;
     const bool dev = values && cudaPointerGetAttributes(&a, values) == cudaSuccess &&
@@ -151,8 +169,8 @@ int sgl_adjoint_slab_fft(sgl_plan *plan, int32_t a0, int32_t a1, sgl_cdouble *pa
     }
     if (a1 == a0) return SGL_OK;
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
-    std::lock_guard<std::mutex> lock(p.mu);
     cudaStream_t st = (cudaStream_t)stream;
+    StageGuard guard(p, st);
     const int planes = a1 - a0;
     // 2-D plans over the slab's planes, cached by plane count
     cufftHandle h = 0;
@@ -198,8 +216,8 @@ int sgl_adjoint_from_packed(sgl_plan *plan, const sgl_cdouble *packed, sgl_cdoub
         return SGL_EINVAL;
     }
     SGL_CUDA_CHECK(cudaSetDevice(p.device));
-    std::lock_guard<std::mutex> lock(p.mu);
     cudaStream_t st = (cudaStream_t)stream;
+    StageGuard guard(p, st);
     SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
     const int n1 = p.n_axis[1], n2c = 2 * p.B;
     k_unpack_crop<<<num_sms() * 8, 256, 0, st>>>(reinterpret_cast<const double2 *>(packed), p.wp, n1, n2c, p.B,
