@@ -50,12 +50,13 @@ def test_forward_adjoint_match_reference(sgl, name, backend):
 
 
 # Config 4 (B = 128, rho = 22) is ill-conditioned in FP64: the adjoint entries
-# span 1 .. 1e95 and rounding is amplified by the radial functions.  Measured
-# spread between FP64 implementations of the SAME sums on this input:
-# reference fast path vs direct summation 2.6e-9, oracle restatement vs
-# reference 5.1e-9, oracle vs direct 4.7e-9.  The bar for this config is
-# therefore the demonstrated FP64 floor x 4.
-TOL_CFG4 = 2e-8
+# span 1 .. 1e95 and rounding is amplified by the radial functions.  Against
+# the extended-precision truth (tests/golden/ref_cfg4_truth.npz,
+# test_parity_scale_gpu.py) the reference's own fast adjoint is 2.56e-9 off
+# and ours 1.22e-9 (basal matrices built in extended precision); two values
+# that far from the truth can differ from each other by up to their sum, so
+# the bar against the reference's output is 2 x its own error.
+TOL_CFG4 = 2 * 2.56e-9
 
 
 def test_config4_adjoint_matches_reference(sgl):
