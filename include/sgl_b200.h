@@ -226,6 +226,17 @@ int sgl_adjoint_spread(sgl_plan *plan, const sgl_cdouble *values, void *stream);
 int sgl_adjoint_slab_fft(sgl_plan *plan, int32_t a0, int32_t a1, sgl_cdouble *packed, void *stream);
 /* `packed`: all N0 planes (N0 x crop1 x crop2, device) -> coeff_count(B) */
 int sgl_adjoint_from_packed(sgl_plan *plan, const sgl_cdouble *packed, sgl_cdouble *coeffs, void *stream);
+/* The all-to-all variant: the axis-0 planes this plan's node
+ * windows touch (mask: N0 bytes, host; the caller ORs the ranks' masks and
+ * reduce-scatters only those planes); after an all-to-all of the packed box
+ * by columns, the 1-D FFT along axis 0 of a column block (cols: N0 x ncols,
+ * columns col0 .. col0+ncols-1 of the crop1 x crop2 box, device), cropped to
+ * kappa0 in [-2B, 2B) and deconvolved -> eta (4B x ncols, device); and the
+ * basal adjoint from the gathered eta (4B x crop1 x crop2, device). */
+int sgl_plan_planes(const sgl_plan *plan, uint8_t *mask);
+int sgl_adjoint_axis0(sgl_plan *plan, const sgl_cdouble *cols, int64_t ncols, int64_t col0, sgl_cdouble *eta,
+                      void *stream);
+int sgl_adjoint_from_eta(sgl_plan *plan, const sgl_cdouble *eta, sgl_cdouble *coeffs, void *stream);
 
 /* per-stage device milliseconds of the last forward / adjoint call
  * (dir 0 = forward, 1 = adjoint); needs SGL_FLAG_PROFILE */

@@ -39,7 +39,7 @@ EXPORTS = (
     "sgl_direct_adjoint", "sgl_plan_destroy", "sgl_plan_get_info",
     "sgl_plan_stage_ms", "sgl_last_error", "sgl_set_device", "sgl_device_count", "sgl_version",
     "sgl_plan_grid", "sgl_adjoint_spread", "sgl_adjoint_slab_fft", "sgl_adjoint_from_packed",
-    "sgl_plan_create_multi",
+    "sgl_plan_create_multi", "sgl_plan_planes", "sgl_adjoint_axis0", "sgl_adjoint_from_eta",
 )
 
 
@@ -141,6 +141,12 @@ def lib() -> ctypes.CDLL:
     L.sgl_adjoint_slab_fft.restype = ctypes.c_int
     L.sgl_adjoint_from_packed.argtypes = [vp, vp, vp, vp]
     L.sgl_adjoint_from_packed.restype = ctypes.c_int
+    L.sgl_plan_planes.argtypes = [vp, vp]
+    L.sgl_plan_planes.restype = ctypes.c_int
+    L.sgl_adjoint_axis0.argtypes = [vp, vp, i64, i64, vp, vp]
+    L.sgl_adjoint_axis0.restype = ctypes.c_int
+    L.sgl_adjoint_from_eta.argtypes = [vp, vp, vp, vp]
+    L.sgl_adjoint_from_eta.restype = ctypes.c_int
     L.sgl_version.argtypes = []
     L.sgl_version.restype = ctypes.c_char_p
     _LIB = L

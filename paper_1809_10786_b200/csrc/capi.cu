@@ -87,6 +87,7 @@ void free_plan(Plan *p) {
     }
     if (p->fft_work) cudaFree(p->fft_work);
     for (auto &e : p->slab_ffts) cufftDestroy(e.second);
+    for (auto &e : p->axis0_ffts) cufftDestroy(e.second);
     if (p->dist_fft1) cufftDestroy(p->dist_fft1);
     if (p->done) cudaEventDestroy(p->done);
     if (p->ev_a) cudaEventDestroy(p->ev_a);
@@ -537,6 +538,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
                 if (made1) cufftDestroy(p->fft1);
                 if (p->fft_work) cudaFree(p->fft_work);
     for (auto &e : p->slab_ffts) cufftDestroy(e.second);
+    for (auto &e : p->axis0_ffts) cufftDestroy(e.second);
     if (p->dist_fft1) cufftDestroy(p->dist_fft1);
                 p->fft_work = nullptr;
             }

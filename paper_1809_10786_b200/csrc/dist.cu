@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "sgl_internal.cuh"
 
@@ -59,6 +60,50 @@ __global__ void k_unpack_crop(const double2 *__restrict__ in, WindowParams wp, i
         const int a = (int)(i / ((int64_t)n2c * n1));
         const int g1 = wrapk(p1 - n1 / 2, wp.N1), g2 = wrapk(p2 - B, wp.N2);
         grid[((size_t)a * wp.N1p + g1 + wp.pad) * wp.N2p + g2 + wp.pad] = in[i];
+    }
+}
+
+// axis-0 planes a node's window touches (the reference's taps, nfft.py:131-141)
+__global__ void k_planes(NodeSet nodes, int64_t M, WindowParams wp, int *__restrict__ mask) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    int lo, hi;
+    window_cells(nodes.u0[i], wp.qa0, lo, hi);
+    for (int a = lo; a <= hi; ++a) {
+        const int w = wrapk(a, wp.N0);
+        if (!mask[w]) mask[w] = 1;   // benign race: every writer stores 1
+    }
+}
+
+// eta_t columns [col0, col0 + nc) of the cropped, deconvolved spectrum after
+// the 1-D FFT along axis 0: eta[k0][j] = X[(k0 - 2B) mod N0][j] d0 d1 d2
+// (nfft.py:268-273), column j = p1 * crop2 + p2 of the packed box
+__global__ void k_axis0_crop(const double2 *__restrict__ X, int64_t nc, int64_t col0, int N0, int B, int crop2,
+                             const double *__restrict__ d0, const double *__restrict__ d1,
+                             const double *__restrict__ d2, double2 *__restrict__ eta) {
+    const int64_t total = (int64_t)4 * B * nc;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i % nc;
+        const int k0 = (int)(i / nc);
+        const int64_t col = col0 + j;
+        const int p1 = (int)(col / crop2), p2 = (int)(col % crop2);
+        const double2 x = X[(int64_t)wrapk(k0 - 2 * B, N0) * nc + j];
+        const double s = d0[k0] * d1[p1] * d2[p2];
+        eta[i] = make_double2(x.x * s, x.y * s);
+    }
+}
+
+// eta[k0][p1][p2] (deconvolved) -> zeta[mi][p1][k0], m = p2 - B (the layout k_sph_adj reads)
+__global__ void k_eta_to_zeta(const double2 *__restrict__ eta, int B, int n1, double2 *__restrict__ zeta) {
+    const int W = 4 * B, NM = 2 * B - 1, C2 = 2 * B;
+    const int64_t total = (int64_t)NM * n1 * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int k0 = (int)(i % W);
+        const int p1 = (int)((i / W) % n1);
+        const int mi = (int)(i / ((int64_t)W * n1));
+        zeta[i] = eta[((int64_t)k0 * n1 + p1) * C2 + (mi + 1)];   // p2 = m + B = mi + 1
     }
 }
 
@@ -199,6 +244,109 @@ int sgl_adjoint_slab_fft(sgl_plan *plan, int32_t a0, int32_t a1, sgl_cdouble *pa
     const int n1 = p.n_axis[1], n2c = 2 * p.B;
     k_pack_crop<<<num_sms() * 8, 256, 0, st>>>(p.grid_buf, p.wp, n1, n2c, p.B, a0, planes,
                                                reinterpret_cast<double2 *>(packed));
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int sgl_plan_planes(const sgl_plan *plan, uint8_t *mask) {
+    if (!plan || !mask) {
+        set_error("NULL plan or mask");
+        return SGL_EINVAL;
+    }
+    const Plan &p = *reinterpret_cast<const Plan *>(plan);
+    int rc = check_sgl(p);
+    if (rc) return rc;
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    std::vector<int> h(p.wp.N0, 0);
+    if (p.M > 0) {
+        int *d = nullptr;
+        SGL_CUDA_CHECK(cudaMalloc(&d, sizeof(int) * p.wp.N0));
+        SGL_CUDA_CHECK(cudaMemset(d, 0, sizeof(int) * p.wp.N0));
+        k_planes<<<(unsigned)((p.M + 255) / 256), 256>>>(p.nodes, p.M, p.wp, d);
+        const cudaError_t e = cudaMemcpy(h.data(), d, sizeof(int) * p.wp.N0, cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        SGL_CUDA_CHECK(e);
+    }
+    for (int a = 0; a < p.wp.N0; ++a) mask[a] = h[a] ? 1 : 0;
+    return SGL_OK;
+}
+
+int sgl_adjoint_axis0(sgl_plan *plan, const sgl_cdouble *cols, int64_t ncols, int64_t col0, sgl_cdouble *eta,
+                      void *stream) {
+    if (!plan) {
+        set_error("NULL plan");
+        return SGL_EINVAL;
+    }
+    Plan &p = *reinterpret_cast<Plan *>(plan);
+    int rc = check_sgl(p);
+    if (rc) return rc;
+    const int64_t C = (int64_t)p.n_axis[1] * 2 * p.B;
+    if (ncols < 0 || col0 < 0 || col0 + ncols > C || (ncols > 0 && (!cols || !eta))) {
+        set_error("column block outside the packed spectral box");
+        return SGL_EINVAL;
+    }
+    if (ncols == 0) return SGL_OK;
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    StageGuard guard(p, st);
+    // the plan's grid serves as scratch (N0 x ncols <= N0 x C fits it)
+    double2 *X = p.grid_buf;
+    SGL_CUDA_CHECK(cudaMemcpyAsync(X, cols, sizeof(double2) * (size_t)p.wp.N0 * ncols, cudaMemcpyDeviceToDevice, st));
+    cufftHandle h = 0;
+    for (auto &e : p.axis0_ffts)
+        if (e.first == ncols) h = e.second;
+    if (!h) {
+        long long n1d[1] = {p.wp.N0};
+        size_t work = 0;
+        rc = fft_rc(cufftCreate(&h), "cufftCreate");
+        if (rc) return rc;
+        rc = fft_rc(cufftMakePlanMany64(h, 1, n1d, n1d, ncols, 1, n1d, ncols, 1, CUFFT_Z2Z, ncols, &work),
+                    "cufftMakePlanMany64(axis 0 columns)");
+        if (rc) {
+            cufftDestroy(h);
+            return rc;
+        }
+        p.axis0_ffts.emplace_back(ncols, h);
+    }
+    rc = fft_rc(cufftSetStream(h, st), "cufftSetStream");
+    if (rc) return rc;
+    cufftDoubleComplex *x = reinterpret_cast<cufftDoubleComplex *>(X);
+    rc = fft_rc(cufftExecZ2Z(h, x, x, CUFFT_FORWARD), "cufftExecZ2Z(axis 0 columns)");
+    if (rc) return rc;
+    k_axis0_crop<<<num_sms() * 8, 256, 0, st>>>(X, ncols, col0, p.wp.N0, p.B, 2 * p.B, p.dec0, p.dec1, p.dec2,
+                                                reinterpret_cast<double2 *>(eta));
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
+int sgl_adjoint_from_eta(sgl_plan *plan, const sgl_cdouble *eta, sgl_cdouble *coeffs, void *stream) {
+    if (!plan) {
+        set_error("NULL plan");
+        return SGL_EINVAL;
+    }
+    Plan &p = *reinterpret_cast<Plan *>(plan);
+    int rc = check_sgl(p);
+    if (rc) return rc;
+    if (!eta || !coeffs) {
+        set_error("NULL spectrum or coefficient array");
+        return SGL_EINVAL;
+    }
+    SGL_CUDA_CHECK(cudaSetDevice(p.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    StageGuard guard(p, st);
+    k_eta_to_zeta<<<num_sms() * 8, 256, 0, st>>>(reinterpret_cast<const double2 *>(eta), p.B, p.n_axis[1], p.zeta);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    cudaPointerAttributes a;
+    const bool dev = cudaPointerGetAttributes(&a, coeffs) == cudaSuccess &&
+                     (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    double2 *c = dev ? reinterpret_cast<double2 *>(coeffs) : p.coef_buf;
+    rc = launch_basal_adjoint_from_zeta(p, c, st);
+    if (rc) return rc;
+    if (!dev) {
+        SGL_CUDA_CHECK(cudaMemcpyAsync(coeffs, p.coef_buf, sizeof(double2) * p.count, cudaMemcpyDeviceToHost, st));
+        SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }

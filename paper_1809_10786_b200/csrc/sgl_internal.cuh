@@ -200,6 +200,7 @@ struct Plan {
 
     // grid-partitioned multi-GPU adjoint (dist.cu): slab 2-D plans by plane count, axis-0 plan
     std::vector<std::pair<int, cufftHandle>> slab_ffts;
+    std::vector<std::pair<int64_t, cufftHandle>> axis0_ffts;   // 1-D axis-0 plans by column count
     cufftHandle dist_fft1 = 0;
 
     StageTimer timers[2];
@@ -277,6 +278,7 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
 int launch_basal_forward(const Plan &p, const double2 *coeffs, double2 *grid, cudaStream_t st,
                          cudaEvent_t mid);
 int launch_basal_adjoint(const Plan &p, const double2 *grid, double2 *coeffs, cudaStream_t st);
+int launch_basal_adjoint_from_zeta(const Plan &p, double2 *coeffs, cudaStream_t st);
 int make_grid_tmap(Plan &p);
 int launch_exact_forward(const Plan &p, const double2 *eta, double2 *values, cudaStream_t st);
 int launch_exact_adjoint(const Plan &p, const double2 *values, double2 *eta, cudaStream_t st);

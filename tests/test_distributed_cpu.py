@@ -1,6 +1,8 @@
 """World-size-2 and -3 gloo runs of the multi-GPU host logic (node shards,
 global rho, both adjoint partitions: coefficient all-reduce, and the grid
-reduce-scatter -> slab 2-D FFT -> gather -> root finish) with the CPU oracle
+reduce-scatter over the touched planes -> slab 2-D FFT -> all-to-all planes
+to columns -> 1-D FFT along axis 0 -> eta gathered to the root -> basal
+adjoint, or the packed planes gathered to the root) with the CPU oracle
 standing in for the per-rank device compute.  The sharded forward
 concatenates to, and the sharded adjoint sums to, the reference's
 single-process result."""
@@ -42,15 +44,30 @@ def oracle_compute():
         g = np.fft.fft(np.asarray(packed), axis=0)[(np.arange(n0) - n0 // 2) % p.grid[0]]
         return o.basal_adjoint(p, o._deconvolve(g / np.prod(p.grid), p.deconv))
 
+    def planes(p):
+        mask = np.zeros(p.grid[0], dtype=np.uint8)
+        for off in range(-p.q, p.q + 1):
+            mask[(p.base[0] + off) % p.grid[0]] = 1
+        return mask
+
+    def axis0(p, cols, col0):
+        n0 = p.n_axis[0]
+        crop2 = p.n_axis[2]
+        X = np.fft.fft(np.asarray(cols), axis=0)[(np.arange(n0) - n0 // 2) % p.grid[0]]
+        j = col0 + np.arange(X.shape[1])
+        s = (2 * np.pi) ** 3 / np.prod(p.grid) * p.deconv[1][j // crop2] * p.deconv[2][j % crop2]
+        return X * p.deconv[0][:, None] * s[None, :]
+
     return Compute(plan=lambda B, pts, rho, **kw: o.oracle_plan(B, pts, rho=rho, **kw),
                    forward=lambda p, c: o.oracle_forward(p, c, threads=1),
                    adjoint=lambda p, v: o.oracle_adjoint(p, v, threads=1),
                    spread=lambda p, v: o.scatter(p.grid, p.base, p.win, np.asarray(v, complex), p.q, threads=1),
                    grid_info=lambda p: (p.grid[0], p.n_axis[1], p.n_axis[2]),
-                   slab_fft=slab_fft, from_packed=from_packed)
+                   slab_fft=slab_fft, from_packed=from_packed, planes=planes, axis0=axis0,
+                   from_eta=lambda p, eta: o.basal_adjoint(p, np.asarray(eta)))
 
 
-def _worker(rank, world, port, name, outdir, partition):
+def _worker(rank, world, port, name, outdir, partition, exchange="alltoall"):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -62,19 +79,22 @@ def _worker(rank, world, port, name, outdir, partition):
     g = load_golden(name)
     s, e = shard_bounds(g["points"].shape[0], rank, world)
     sp = ShardedPlan(int(g["B"]), g["points"][s:e], compute=oracle_compute(), q=int(g["q"]), partition=partition,
-                     compact_k1=bool(g["compact"]))
+                     exchange=exchange, compact_k1=bool(g["compact"]))
     f = sp.forward(g["coeffs"])
     a = sp.adjoint(g["values"][s:e])
-    np.savez(os.path.join(outdir, f"r{rank}.npz"), f=f, a=a, rho=sp.rho, s=s, e=e, part=sp.partition)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), f=f, a=a, rho=sp.rho, s=s, e=e, part=sp.partition,
+             pieces=np.array(sp.last_pieces or [], dtype=np.int64).reshape(-1, 4))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world,partition", [("b8_q16", 2, "coeffs"), ("b5_q10", 2, "coeffs"),
-                                                  ("b8_q16", 2, "grid"), ("b5_q10", 3, "grid"),
-                                                  ("b6_q6_compact", 2, "grid")])
-def test_rank_shards_match_single_process(name, world, partition, tmp_path, oracle_built):
-    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), partition), nprocs=world, join=True)
+@pytest.mark.parametrize("name,world,partition,exchange", [
+    ("b8_q16", 2, "coeffs", "alltoall"), ("b5_q10", 2, "coeffs", "alltoall"),
+    ("b8_q16", 2, "grid", "alltoall"), ("b5_q10", 3, "grid", "alltoall"), ("b6_q6_compact", 2, "grid", "alltoall"),
+    ("b8_q16", 3, "grid", "gather"), ("b6_q6_compact", 2, "grid", "gather")])
+def test_rank_shards_match_single_process(name, world, partition, exchange, tmp_path, oracle_built):
+    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), partition, exchange), nprocs=world,
+             join=True)
     g = load_golden(name)
     r = [np.load(tmp_path / f"r{k}.npz") for k in range(world)]
     # rho is the all-reduce max over shards == the single-process choose_rho
@@ -85,6 +105,49 @@ def test_rank_shards_match_single_process(name, world, partition, tmp_path, orac
         assert str(x["part"]) == partition
         assert np.max(np.abs(x["a"] - g["adj"])) <= 1e-12 * np.max(np.abs(g["adj"]))
     assert all(np.array_equal(r[0]["a"], x["a"]) for x in r)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_plane_pieces_own_every_touched_plane_once(world):
+    """plane_pieces / owned_planes: every touched plane has exactly one owner,
+    every widened block lies inside [0, N0) and blocks of different pieces do
+    not overlap (the in-place reduce-scatter writes whole blocks)."""
+    from paper_1809_10786_b200.distributed import owned_planes, plane_pieces
+    rng = np.random.default_rng(world)
+    masks = []
+    for n0 in (16, 64, 512):
+        for lo, hi in ((0, n0 // 2 + 5), (n0 - 3, n0 // 2 + 7), (3, 9)):   # plain, wrapping, narrow arcs
+            m = np.zeros(n0, bool)
+            idx = np.arange(lo, lo + ((hi - lo) % n0)) % n0
+            m[idx] = True
+            masks.append(m)
+        masks.append(rng.random(n0) < 0.3)
+        masks.append(np.ones(n0, bool))
+        masks.append(np.zeros(n0, bool))
+    for m in masks:
+        n0 = m.size
+        pieces = plane_pieces(m, world)
+        if not m.any():
+            assert pieces == []
+            continue
+        cnt = np.zeros(n0, int)
+        for k in range(world):
+            for a0, a1 in owned_planes(pieces, k, world):
+                cnt[a0:a1] += 1
+        assert np.all(cnt[m] == 1) and cnt.max() == 1
+        spans = []
+        for s0, blk, ps, pe in pieces:
+            assert 0 <= s0 <= ps < pe <= n0 and s0 + blk * world >= pe
+            if s0 + blk * world <= n0:
+                spans.append((s0, s0 + blk * world))
+        if len(spans) == 2:
+            assert max(spans[0][0], spans[1][0]) >= min(spans[0][1], spans[1][1])
+    # the BASELINE geometry (B = 64, q = 16): half the planes plus the windows
+    m = np.zeros(512, bool)
+    m[:273] = True
+    m[-16:] = True
+    pieces = plane_pieces(m, 8)
+    assert sum(pe - ps for _, _, ps, pe in pieces) == 289
 
 
 def test_partition_model_prefers_the_coefficient_allreduce_on_nvswitch():

@@ -2,9 +2,11 @@
 (`distributed.cuda_compute`): both ranks on GPU 0 with the gloo backend (the
 box has one GPU; the collectives go through host copies), node shards of one
 transform, both adjoint partitions -- the coefficient all-reduce and the
-north star's grid reduce-scatter -> slab 2-D FFT -> gather -> root finish
-through the C ABI stage entry points (sgl_adjoint_spread / _slab_fft /
-_from_packed).  The sharded results must equal the single-process ones and
+north star's grid reduce-scatter over the touched planes -> slab 2-D FFT ->
+all-to-all (planes to columns) -> 1-D FFT along axis 0 -> eta to the root ->
+basal adjoint, through the C ABI stage entry points (sgl_adjoint_spread /
+_slab_fft / sgl_plan_planes / _axis0 / _from_eta, and _from_packed for the
+gather exchange).  The sharded results must equal the single-process ones and
 the reference goldens."""
 import os
 import socket
@@ -26,7 +28,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, outdir, partition, backend):
+def _worker(rank, world, port, name, outdir, partition, backend, exchange):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -43,6 +45,7 @@ def _worker(rank, world, port, name, outdir, partition, backend):
     s, e = shard_bounds(M, rank, world)
     # rho: the golden's (pinned to the full config's node set for the cfg subsets)
     sp = ShardedPlan(int(g["B"]), g["points"][s:e], q=int(g["q"]), partition=partition, backend=backend,
+                     exchange=exchange,
                      device=0, compact_k1=bool(g["compact"]), rho=float(g["rho"]))
     f = sp.forward(c)
     a = sp.adjoint(g["values"][s:e])
@@ -58,14 +61,17 @@ def rel(x, ref):
     return float(np.max(np.abs(np.asarray(x) - ref)) / np.max(np.abs(ref)))
 
 
-@pytest.mark.parametrize("name,partition,backend", [("b12_q12", "grid", "auto"), ("b12_q12", "coeffs", "auto"),
-                                                    ("cfg2_sub20k", "grid", "i8"), ("cfg2_sub20k", "coeffs", "tiled"),
-                                                    ("b6_q6_compact", "grid", "auto")])
-def test_two_ranks_on_one_gpu_match_single_process(name, partition, backend, tmp_path):
+@pytest.mark.parametrize("name,partition,backend,exchange", [
+    ("b12_q12", "grid", "auto", "alltoall"), ("b12_q12", "grid", "auto", "gather"),
+    ("b12_q12", "coeffs", "auto", "alltoall"), ("cfg2_sub20k", "grid", "i8", "alltoall"),
+    ("cfg2_sub20k", "coeffs", "tiled", "alltoall"), ("b6_q6_compact", "grid", "auto", "alltoall"),
+    ("b6_q6_compact", "grid", "auto", "gather")])
+def test_two_ranks_on_one_gpu_match_single_process(name, partition, backend, exchange, tmp_path):
     import paper_1809_10786_b200 as sgl
     g = load_golden(name)
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), partition, backend), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path), partition, backend, exchange), nprocs=world,
+             join=True)
     r = [np.load(tmp_path / f"r{k}.npz") for k in range(world)]
     assert all(str(x["part"]) == partition for x in r)
     assert all(float(x["rho"]) == float(g["rho"]) for x in r)
