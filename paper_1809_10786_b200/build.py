@@ -39,15 +39,22 @@ def _stale(lib: str = LIB) -> bool:
 CHECKED_LIB = os.path.join(LIBDIR, "libsgl_b200_checked.so")
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
     """checked=True: a separate library with device-side bounds checks
     (-DSGL_CHECKED, SGL_DCHECK in the kernels), loaded when SGL_LIBRARY points
-    at it (tests/tools only); the product library never carries them."""
+    at it (tests/tools only); the product library never carries them.
+    variant="name", defines=("-DX=1", ...): an experimental build in
+    _lib/variants/ (kernel A/B measurements via SGL_LIBRARY)."""
     lib = CHECKED_LIB if checked else LIB
+    if variant:
+        lib = os.path.join(LIBDIR, "variants", f"libsgl_{variant}.so")
     if not force and not _stale(lib):
         return lib
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     objdir = os.path.join(LIBDIR, "obj_checked" if checked else "obj")
+    if variant:
+        objdir = os.path.join(LIBDIR, "variants", "obj_" + variant)
     os.makedirs(objdir, exist_ok=True)
     base = [nvcc()]
     # /usr/bin/g++ is the host compiler with a complete toolchain in this image
@@ -55,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
         base += ["-ccbin", "/usr/bin/g++"]
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-             "-I", os.path.join(HERE, "..", "include")] + (["-DSGL_CHECKED"] if checked else [])
+             "-I", os.path.join(HERE, "..", "include")] + (["-DSGL_CHECKED"] if checked else []) + list(defines)
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
@@ -85,4 +92,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))
+    # python -m paper_1809_10786_b200.build [--force] [-v] [--checked] [--variant NAME -DX=1 ...]
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv,
+                variant=var, defines=tuple(a for a in sys.argv if a.startswith("-D"))))

@@ -261,7 +261,7 @@ __global__ void k_rate2(int N, int iters, int lay, int32_t *sink) {
         const uint32_t id = umma::idesc_i8(128, N, true, true);
         uint64_t da, db;
         uint32_t kadv_a, kadv_b;
-        if (lay == 0 || lay == 1) {
+        if (lay == 0 || lay == 1 || lay == 5) {
             const uint32_t ex = lay == 1 ? 16 : 0;
             da = umma::desc_kmajor(sa, 128 * 16 + ex, 128);
             db = umma::desc_kmajor(sb, N * 16 + ex, 128);
@@ -284,6 +284,12 @@ __global__ void k_rate2(int N, int iters, int lay, int32_t *sink) {
             kadv_b = 4 * (N / 16 * 128);
         }
         const uint32_t idm = lay == 4 ? (id | (1u << 15) | (1u << 16)) : id;
+        if (lay == 5) {   // A from TMEM (columns 256 + 8 kb), B interleave K-major
+            for (int it = 0; it < iters; ++it)
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb)
+                    umma::mma_i8_ts(td, td + 256 + 8 * kb, db + ((kb * kadv_b) >> 4), idm, true);
+        } else
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb)
@@ -430,8 +436,9 @@ int main() {
             printf("rate M=128 N=%d K/issue-block=%d: %.1f int8 TOPS (%.3f ms) %s\n", N, Kr, ops / ms / 1e9, ms,
                    cudaGetErrorString(cudaGetLastError()));
         }
-    for (int lay = 0; lay < 5; lay += (lay == 0 ? 4 : 1))
+    for (int lay = 0; lay < 6; lay += (lay == 0 ? 4 : 1))
         for (int N : {80, 160, 240, 256}) {
+            if (lay == 5 && N == 256) continue;   // D (N columns) + A (32 columns) within 512
             cudaFuncSetAttribute(k_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             const int iters = 5000;
             k_rate2<<<sms, 128, 96 * 1024>>>(N, 100, lay, sink);

@@ -15,9 +15,11 @@ ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--m", type=int, default=2_000_000)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--backend", default="auto")
+ap.add_argument("--profile", action="store_true", help="SGL_FLAG_I8_PROF: int8 kernel wait counters on stderr")
 a = ap.parse_args()
 w = workloads.config(a.config, M=a.m)
-p = sgl.plan(w.B, w.points, rho=w.rho, backend=a.backend)
+p = sgl.plan(w.B, w.points, rho=w.rho, backend=a.backend,
+             flags=(1 << 12) if a.profile else 0)   # SGL_FLAG_I8_PROF
 c = w.coeffs if w.coeffs.ndim == 1 else w.coeffs[0]
 for _ in range(a.reps):
     f = sgl.forward(p, c)
