@@ -170,3 +170,39 @@ def test_repeated_calls_race_free(sgl):
     a0 = sgl.adjoint(p, g["values"])
     for _ in range(10):
         assert rel(sgl.adjoint(p, g["values"]), a0) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["b12_q12", "cfg3_sub600"])
+def test_fused_call_on_int8_scatter(sgl, name):
+    """sgl_forward_adjoint on a plan with the int8 scatter: same results as
+    the separate calls for pageable, pinned and device inputs, repeated calls
+    (side-stream copies and plan buffers reused), and a non-finite adjoint
+    input (the guard's FP64 path, cleared again on the next call)."""
+    import torch
+    g = load_golden(name)
+    kw = dict(q=int(g["q"]), rho=float(g["rho"]), compact_k1=bool(g["compact"]))
+    p = _plan_i8s(sgl, int(g["B"]), g["points"], **kw)
+    assert p.stats["i8_scatter"]
+    c = g["coeffs"] if g["coeffs"].ndim == 1 else g["coeffs"][0]
+    v = g["values"]
+    f0, a0 = sgl.forward(p, c), sgl.adjoint(p, v)
+    f, a = sgl.forward_adjoint(p, c, v)
+    assert np.array_equal(f, f0) and rel(a, a0) <= 1e-13 and rel(a, g["adj"]) <= TOL_I8
+    vp = torch.empty(v.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    vp[:] = v
+    for _ in range(3):   # pinned input, repeated
+        f2, a2 = sgl.forward_adjoint(p, c, vp)
+        assert np.array_equal(f2, f0) and rel(a2, a0) <= 1e-13
+    dev = torch.device("cuda", 0)
+    cd, vd = torch.as_tensor(c, device=dev), torch.as_tensor(v, device=dev)
+    for k in range(3):   # device input (scaled by 2^k: exact in fixed point), alternating with separate calls
+        fd, ad = sgl.forward_adjoint(p, cd, vd * 2.0 ** k)
+        assert np.array_equal(fd.cpu().numpy(), f0) and rel(ad.cpu().numpy() / 2.0 ** k, a0) <= 1e-13
+        assert rel(sgl.adjoint(p, v), a0) <= 1e-13
+    vn = v.copy()
+    vn[len(vn) // 2] = np.nan
+    fn, an = sgl.forward_adjoint(p, c, vn)
+    assert np.array_equal(fn, f0) and np.isnan(an).any()
+    assert np.isnan(sgl.adjoint(p, vn)).any()
+    f3, a3 = sgl.forward_adjoint(p, c, v)   # the flag is cleared again
+    assert np.all(np.isfinite(a3)) and rel(a3, a0) <= 1e-13
