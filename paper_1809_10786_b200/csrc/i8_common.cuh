@@ -161,5 +161,16 @@ __device__ __forceinline__ double combine6(int32_t d0, int32_t d1, int32_t d2, i
     return fma((double)hi, 4294967296.0 * unit, (double)lo * unit);
 }
 
+// combine6 for sums of at most 512 products (the int8 scatter's K = one tile's
+// nodes): |operands| < 2^46 in balanced digits bound the diagonal sum by
+// 2^(92 + 9 - 40) = 2^61, so the 6 diagonals combine exactly in one int64 and
+// convert once (one rounding, as combine6)
+__device__ __forceinline__ double combine6_k512(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4, int32_t d5,
+                                                double unit) {
+    const long long x = (long long)d0 + ((long long)d1 << 8) + ((long long)d2 << 16) + ((long long)d3 << 24) +
+                        ((long long)d4 << 32) + ((long long)d5 << 40);
+    return (double)x * unit;
+}
+
 }  // namespace i8
 }  // namespace sgl

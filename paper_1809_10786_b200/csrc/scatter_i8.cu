@@ -47,6 +47,11 @@ namespace {
 
 using namespace i8;
 
+#ifndef SGL_COMBINE
+#define SGL_COMBINE combine6_k512   // SN = 512 products per diagonal sum (see i8_common.cuh)
+#endif
+static_assert(kI8SNodes <= 512, "combine6_k512 needs at most 512 nodes per tile");
+
 constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
@@ -434,7 +439,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     }
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        S.stage[(c0 + i) * 4 + j][m] = combine6(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
+                        S.stage[(c0 + i) * 4 + j][m] = SGL_COMBINE(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
                                                                 D[cur][4][j], D[cur][5][j], unit);
                     umma::tmem_ld_wait();
                 }
