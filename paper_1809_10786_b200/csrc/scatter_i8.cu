@@ -47,6 +47,7 @@ namespace {
 
 using namespace i8;
 
+
 #ifndef SGL_COMBINE
 #define SGL_COMBINE combine6_k512   // SN = 512 products per diagonal sum (see i8_common.cuh)
 #endif
@@ -111,40 +112,43 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 __device__ __forceinline__ int mblocks(const Tile &t) { return (t.e0 * CHUNKS * 16 + MR - 1) / MR; }
 __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1) / KST; }
 
-// value digits of every K-step of every tile (once per adjoint): thread =
-// (node of the K-step, 16-column group = 8 axis-1 cells x re|im)
+// value digits of every K-step of every tile (once per adjoint): thread = node
+// of the K-step, walking all 40 axis-1 cells (the Gaussian recurrence runs on
+// across the 5 16-column groups: one exp pair per node; 1.07 ms at config 3
+// against 1.2 ms with a thread per column group); warp = K-step, 4 K-steps
+// per block
 __global__ void k_vdigits(const Tile *__restrict__ tiles, const int *__restrict__ ktile, int64_t nksteps,
-                          NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
-                          const int *__restrict__ tsv, const int64_t *__restrict__ voff, uint8_t *__restrict__ vdig,
-                          const int *__restrict__ skip) {
+                               NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
+                               const int *__restrict__ tsv, const int64_t *__restrict__ voff,
+                               uint8_t *__restrict__ vdig, const int *__restrict__ skip) {
     if (*skip) return;   // non-finite values: the gated FP64 scatter runs instead (guard.cu)
-    const int kl = threadIdx.x & 31, vg = threadIdx.x >> 5;   // 5 warps = 5 column groups
-    // one K-step per block iteration over the flat K-step index of all tiles
-    // (many K-steps in flight: the value gather through perm is latency-bound)
-    for (int64_t gk = blockIdx.x; gk < nksteps; gk += gridDim.x) {
+    const int kl = threadIdx.x & 31, wk = threadIdx.x >> 5;
+    for (int64_t gk = (int64_t)blockIdx.x * 4 + wk; gk < nksteps; gk += (int64_t)gridDim.x * 4) {
         const int64_t ti = ktile[gk];
         const Tile t = tiles[ti];
         const int svt = tsv[ti];
         const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);
-        const int bb = t.o1 + vg * 8;
-        {
-            const int ks = (int)(gk - voff[ti]);
-            const int kn = ks * KST + kl;
-            const bool live = kn < t.count;
-            const int64_t si = (int64_t)t.start + kn;
-            const double u1 = live ? nodes.u1[si] : -1e9;
-            SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
-            const double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
-            int lo1, hi1;
-            window_cells(u1, wp.q, lo1, hi1);
-            const int bf = max(0, lo1 - bb);
-            const double d = u1 - (double)(bb + bf);
-            double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
+        const int ks = (int)(gk - voff[ti]);
+        const int kn = ks * KST + kl;
+        const bool live = kn < t.count;
+        const int64_t si = (int64_t)t.start + kn;
+        const double u1 = live ? nodes.u1[si] : -1e9;
+        SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
+        const double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
+        int lo1, hi1;
+        window_cells(u1, wp.q, lo1, hi1);
+        const int bf = max(0, lo1 - t.o1);   // first window cell, relative to the box
+        const double d = u1 - (double)(t.o1 + bf);
+        double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
+        uint8_t *dst = vdig + (voff[ti] + ks) * (int64_t)B_STAGE + (kl >> 3) * B_KBLK + (kl & 7) * 16;
+#pragma unroll 1
+        for (int vg = 0; vg < ROWS / 16; ++vg) {
             double wv[16];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const double w1 = (live && j >= bf && bb + j <= hi1) ? w : 0.0;
-                if (j >= bf) {
+                const int b = vg * 8 + j;
+                const double w1 = (live && b >= bf && t.o1 + b <= hi1) ? w : 0.0;
+                if (b >= bf) {
                     w *= r;
                     r *= wp.r1_1;
                 }
@@ -153,10 +157,10 @@ __global__ void k_vdigits(const Tile *__restrict__ tiles, const int *__restrict_
             }
             uint32_t dw[ND][4];
             digits16(vsc, wv, dw);
-            uint8_t *dst = vdig + (voff[ti] + ks) * (int64_t)B_STAGE + (kl >> 3) * B_KBLK + vg * 128 + (kl & 7) * 16;
 #pragma unroll
             for (int q = 0; q < ND; ++q)
-                *reinterpret_cast<uint4 *>(dst + q * (ROWS / 16) * 128) = make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
+                *reinterpret_cast<uint4 *>(dst + vg * 128 + q * (ROWS / 16) * 128) =
+                    make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
         }
     }
 }
@@ -579,7 +583,7 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
                                                          skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int sms = num_sms();
-    k_vdigits<<<(unsigned)std::min<int64_t>(p.n_sksteps, (int64_t)sms * 64), (ROWS / 16) * 32, 0, st>>>(
+    k_vdigits<<<(unsigned)std::min<int64_t>((p.n_sksteps + 3) / 4, (int64_t)sms * 32), 128, 0, st>>>(
         p.istiles, p.sktile, p.n_sksteps, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig, skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
