@@ -244,10 +244,12 @@ int adjoint_tail(Plan &p, double2 *c, cudaStream_t st, StageRec *rec) {
 // the int8 scatter's accuracy decision (after guard_adjoint_estimate): read
 // the flag on the host; above the bound, rerun the adjoint on the FP64 scatter
 int adjoint_guard_resolve(Plan &p, const double2 *v, double2 *c, cudaStream_t st) {
-    if (!(p.i8s && p.guard_on && p.guard_ap > 0.0 && p.M > 0)) return SGL_OK;
+    if (!(p.i8s_live() && p.guard_on && p.guard_ap > 0.0 && p.M > 0)) return SGL_OK;
     int redo = 0;
     SGL_CUDA_CHECK(cudaMemcpyAsync(&redo, &p.guard->adj_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
     SGL_CUDA_CHECK(cudaStreamSynchronize(st));
+    p.i8s_streak = redo ? p.i8s_streak + 1 : 0;
+    if (p.i8s_auto && p.i8s_streak >= 2) p.i8s_off = true;   // the FP64 scatter from the next call on
     if (!redo) return SGL_OK;
     SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
     int rc = launch_scatter(p, v, p.grid_buf, st);
@@ -270,10 +272,10 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
         return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
     }
     SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    rc = p.i8s ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
+    rc = p.i8s_live() ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
     if (rc) return rc;
     rc = adjoint_tail(p, c, st, rec);
-    if (rc || !(p.i8s && p.guard_ap > 0.0 && p.M > 0)) return rc;
+    if (rc || !(p.i8s_live() && p.guard_ap > 0.0 && p.M > 0)) return rc;
     // int8 scatter accuracy check (guard.cu): estimate from the result, rerun on FP64 above the bound
     rc = guard_adjoint_estimate(p, v, c, st);
     if (rc || !(p.guard_on && may_sync)) return rc;

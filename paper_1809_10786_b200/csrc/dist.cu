@@ -192,7 +192,7 @@ int sgl_adjoint_spread(sgl_plan *plan, const sgl_cdouble *values, void *stream) 
         v = p.val_buf;
     }
     SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    rc = p.i8s ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
+    rc = p.i8s_live() ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
     if (rc) return rc;
     rc = launch_halo_fold(p, p.grid_buf, st);
     if (rc) return rc;

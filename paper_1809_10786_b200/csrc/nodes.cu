@@ -584,15 +584,19 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
             rc = reorder_tiles(p.istiles, p.n_istiles, st);
             if (rc) return rc;
             if (!p.i8s) {
-                // automatic choice: the int8 scatter costs ~2700 SM-cycles per
-                // K-step (32 nodes x 128 cells), the FP64 DMMA scatter ~1400 per
-                // node (config 3, r01): take it for large dense node sets only (config 2,
-                // 1e6 lattice nodes: 6.9 vs 5.2 ms, its per-M-block drain dominates)
+                // automatic choice: the int8 scatter beats the FP64 DMMA scatter on
+                // every measured node set of >= 1.5e5 nodes up to 1.3 int8 K-steps
+                // per node (config-3 subsamples, i.e. the node shards of a
+                // strong-scaling run: 1.2-1.7x, profiles/r02/scatter_crossover.txt;
+                // config 3: 29.7 vs 50 ms); below ~1e5 nodes its per-plan setup
+                // (value-digit buffers, guard calibration) is not worth it.  Inputs
+                // the accuracy guard keeps rejecting switch the plan to FP64 at run
+                // time (Plan::i8s_off, capi.cu)
                 TileStats ts;
                 rc = tile_stats(p.istiles, p.n_istiles, 2, p.wp, st, &ts);
                 if (rc) return rc;
                 const double ks = (double)ts.work;
-                p.i8s = p.M >= 5000000 && ks < 0.5 * (double)p.M;   // config 3 (1e7): 0.45, 46.8 vs 50.1 ms
+                p.i8s = p.M >= 100000 && ks < 1.5 * (double)p.M;
                 if (!p.i8s) {
                     cudaFree(p.istiles);
                     p.istiles = nullptr;

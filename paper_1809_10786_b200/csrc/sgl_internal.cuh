@@ -170,6 +170,12 @@ struct Plan {
     int64_t i8_ksteps = 0;         // K-steps of one gather pass (sum over tiles)
     bool i8s = false;              // int8 tensor-core scatter (scatter_i8.cu), same node order
     bool i8s_auto = false;         // decide i8s from the tiles' density at plan time
+    // run time: an automatically chosen int8 scatter whose accuracy guard made
+    // two calls in a row recompute on FP64 (inputs it cannot resolve, e.g. the
+    // config-2 lattice) is switched off for the plan's later adjoints
+    bool i8s_off = false;
+    int i8s_streak = 0;
+    bool i8s_live() const { return i8s && !i8s_off; }
     Tile *istiles = nullptr;       // its 512-node tiles
     int64_t n_istiles = 0;
     int *tsv = nullptr;            // per scatter tile: value fixed-point shift

@@ -149,8 +149,33 @@ def test_scatter_engine_selection_and_full_size_parity(sgl):
     assert not p64.stats["i8_scatter"]
     a8, a64 = sgl.adjoint(p, w.values), sgl.adjoint(p64, w.values)
     assert rel(a8, a64) <= TOL_I8, rel(a8, a64)
+    # mid-size node sets of the same distribution (the node shards of a
+    # strong-scaling run) take it too; small ones keep the FP64 scatter
     w2 = workloads.config(3, M=1_000_000)
-    assert not sgl.plan(w2.B, w2.points, rho=w2.rho).stats["i8_scatter"]
+    assert sgl.plan(w2.B, w2.points, rho=w2.rho).stats["i8_scatter"]
+    w3 = workloads.config(3, M=50_000)
+    assert not sgl.plan(w3.B, w3.points, rho=w3.rho).stats["i8_scatter"]
+
+
+def test_auto_int8_scatter_switches_off_when_the_guard_keeps_rejecting(sgl):
+    """Config 2's lattice: the automatically chosen int8 scatter's accuracy
+    estimate exceeds the bound on every call, so each call recomputes on FP64;
+    after two such calls the plan uses the FP64 scatter directly.  A plan that
+    forces backend="i8" keeps the int8 engine (and its per-call fallback)."""
+    from paper_1809_10786_b200 import workloads
+    w = workloads.config(2)
+    p = sgl.plan(w.B, w.points, rho=w.rho)
+    if not p.stats["i8_scatter"]:
+        pytest.skip("the int8 scatter is not chosen for config 2")
+    ref = sgl.adjoint(sgl.plan(w.B, w.points, rho=w.rho, backend="tiled"), w.values)
+    for k in range(4):
+        a = sgl.adjoint(p, w.values)
+        assert rel(a, ref) <= 1e-12, (k, rel(a, ref))
+    assert p.guard["adj_fallbacks"] == 2
+    p8 = sgl.plan(w.B, w.points, rho=w.rho, backend="i8")
+    for _ in range(3):
+        assert rel(sgl.adjoint(p8, w.values), ref) <= 1e-12
+    assert p8.guard["adj_fallbacks"] == 3
 
 
 def test_repeated_calls_race_free(sgl):
