@@ -48,6 +48,27 @@ def shard_bounds(M: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
+def shard_indices(points, rank: int, world: int, mode: str = "radial") -> np.ndarray:
+    """Caller indices of rank's node shard (ascending), count-balanced.
+
+    "contiguous": [start, stop) of the caller order (`shard_bounds`): for
+    unordered inputs a random subsample, 1/world of the node density.
+    "radial": the rank-th of `world` equal-count shells in r.  The warped
+    radius is grid axis 0 (transform.py:46-55), so a shell covers one band of
+    axis-0 planes at the full node density: the int8 window tiles stay as
+    full as on one GPU (config 3 at 8 ranks: `tools/shard_probe.py`), and a
+    rank's spread touches only its band plus q planes."""
+    if mode not in ("contiguous", "radial"):
+        raise ValueError("mode must be 'contiguous' or 'radial'")
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    M = pts.shape[0]
+    s0, s1 = shard_bounds(M, rank, world)
+    if mode == "contiguous":
+        return np.arange(s0, s1)
+    order = np.argsort(pts[:, 0], kind="stable")
+    return np.sort(order[s0:s1])
+
+
 @dataclass
 class Compute:
     """The per-rank transform implementation (default: this package's CUDA

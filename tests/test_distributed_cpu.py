@@ -168,3 +168,22 @@ def test_shard_bounds_cover():
             assert spans[0][0] == 0 and spans[-1][1] == M
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(e - s for s, e in spans) - min(e - s for s, e in spans) <= 1
+
+
+def test_shard_indices_partition():
+    """Both shard modes partition the node indices into count-balanced,
+    ascending shards; radial shards are ordered shells in r."""
+    import numpy as np
+    from paper_1809_10786_b200.distributed import shard_indices, shard_bounds
+    rng = np.random.default_rng(3)
+    pts = rng.random((1001, 3)) * [7.0, 3.0, 6.0]
+    for mode in ("contiguous", "radial"):
+        parts = [shard_indices(pts, k, 4, mode) for k in range(4)]
+        assert [len(x) for x in parts] == [b - a for a, b in (shard_bounds(1001, k, 4) for k in range(4))]
+        assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(1001))
+        assert all(np.all(np.diff(x) > 0) for x in parts)
+    rad = [shard_indices(pts, k, 4, "radial") for k in range(4)]
+    assert all(pts[rad[k], 0].max() <= pts[rad[k + 1], 0].min() for k in range(3))
+    import pytest
+    with pytest.raises(ValueError):
+        shard_indices(pts, 0, 4, "spiral")
