@@ -11,9 +11,11 @@ the radius-16 ball, complex128).  Inputs are the seeded synthetic inputs of
 SURVEY 8(d) (no public dataset exists for this path).
 
 N > 1 (torchrun, one rank per GPU), default --scaling strong: every rank
-builds the SAME config (seed 0, same coefficients), takes its contiguous
-node shard (distributed.shard_bounds), rho is the all-reduce max over the
-shards (= the full set's); value = M_total / the slowest rank's step time.
+builds the SAME config (seed 0, same coefficients), takes its node shard
+(--shard theta: an equal-count band in the polar angle, full node density;
+contiguous / radial: distributed.shard_indices), rho is the all-reduce max
+over the shards (= the full set's); value = M_total / the slowest rank's
+step time.
 The adjoint's exchange is the partition `distributed.partition_model` picks
 (--partition overrides): the coefficient all-reduce or the north star's grid
 reduce-scatter + slab FFT.  --scaling weak: each rank its own M-node set.
@@ -63,6 +65,8 @@ def parse():
                     help="default: the config's own (3: both, 4: adj, 5: batched fwd)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--partition", default="auto", choices=["auto", "coeffs", "grid"])
+    ap.add_argument("--shard", default="theta", choices=["theta", "contiguous", "radial"],
+                    help="strong scaling: how the config's nodes are split over the ranks")
     ap.add_argument("--no-stock", action="store_true", help="skip timing the stock reference package")
     ap.add_argument("--backend", default="auto", choices=["auto", "tiled", "i8"],
                     help="window engines (experiments; the default is the library's own choice)")
@@ -306,7 +310,7 @@ def main():
 
     import paper_1809_10786_b200 as sgl
     from paper_1809_10786_b200 import _native, workloads
-    from paper_1809_10786_b200.distributed import ShardedPlan, shard_bounds
+    from paper_1809_10786_b200.distributed import ShardedPlan, shard_indices
 
     # test hooks: SGL_BENCH_DEVICE pins every rank to one GPU and
     # SGL_BENCH_BACKEND=gloo replaces NCCL, so the multi-rank logic can be
@@ -332,8 +336,11 @@ def main():
     if w.values is None:
         w.values = np.zeros(w.M, dtype=complex)
     if strong and world > 1:
-        s0, s1 = shard_bounds(w.M, rank, world)
-        w.points, w.values = w.points[s0:s1], w.values[s0:s1]
+        # theta bands (default): whole pencil rows of the window tiles at full
+        # node density on every rank (distributed.shard_indices; per-rank work
+        # at N = 8: profiles/r02/shard_probe.txt)
+        idx = shard_indices(w.points, rank, world, args.shard)
+        w.points, w.values = w.points[idx], w.values[idx]
     pts_d = torch.as_tensor(w.points, device=dev)
     c_d = torch.as_tensor(coeffs_h, device=dev)
     v_d = torch.as_tensor(w.values, device=dev)
@@ -553,7 +560,7 @@ def main():
             "data": "synthetic (seeded PCG64 inputs of SURVEY 8(d); no public dataset)",
             "config": bench_config(w, direction, K) | {"M": M_total},
             "config_extra": {"grid": list(p.nfft.grid_shape), "rho": rho, "l2": l2_note, "M_per_rank": w.M,
-                             "parallelism": (f"{world} GPU(s), node shards; adjoint exchange: "
+                             "parallelism": (f"{world} GPU(s), node shards ({args.shard if strong else 'own sets'}); adjoint exchange: "
                                              f"{sp.partition if sp is not None else 'none'}"
                                              + (" (coefficient all-reduce)" if sp is not None and
                                                 sp.partition == "coeffs" else

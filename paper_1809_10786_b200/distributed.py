@@ -57,15 +57,18 @@ def shard_indices(points, rank: int, world: int, mode: str = "radial") -> np.nda
     radius is grid axis 0 (transform.py:46-55), so a shell covers one band of
     axis-0 planes at the full node density: the int8 window tiles stay as
     full as on one GPU (config 3 at 8 ranks: `tools/shard_probe.py`), and a
-    rank's spread touches only its band plus q planes."""
-    if mode not in ("contiguous", "radial"):
-        raise ValueError("mode must be 'contiguous' or 'radial'")
+    rank's spread touches only its band plus q planes.
+    "theta": equal-count bands in the polar angle theta = grid axis 1: whole
+    rows of the window tiles' pencils, every radius and azimuth, i.e. full
+    node density and the global range of output magnitudes on every rank."""
+    if mode not in ("contiguous", "radial", "theta"):
+        raise ValueError("mode must be 'contiguous', 'radial' or 'theta'")
     pts = np.atleast_2d(np.asarray(points, dtype=float))
     M = pts.shape[0]
     s0, s1 = shard_bounds(M, rank, world)
     if mode == "contiguous":
         return np.arange(s0, s1)
-    order = np.argsort(pts[:, 0], kind="stable")
+    order = np.argsort(pts[:, 0 if mode == "radial" else 1], kind="stable")
     return np.sort(order[s0:s1])
 
 

@@ -15,7 +15,7 @@ from paper_1809_10786_b200.distributed import shard_indices
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 w = workloads.config(3)
 c = torch.as_tensor(w.coeffs, device="cuda")
-for mode in ("contiguous", "radial"):
+for mode in (sys.argv[2:] or ["contiguous", "radial", "theta"]):
     tot, win = [], []
     for k in range(N):
         idx = shard_indices(w.points, k, N, mode)
