@@ -372,17 +372,32 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
 
 // per slab a: max(|Re G|, |Im G|) (bits of a non-negative double order like
 // the double; NaN counts as +Inf); grid = (N0 slabs) x (blocks per slab)
-__global__ void k_slab_absmax(const double2 *__restrict__ g, size_t per_slab, unsigned long long *out) {
-    const double2 *s = g + (size_t)blockIdx.y * per_slab;
+__global__ void k_slab_absmax(const double2 *__restrict__ g, size_t per_slab, const int *__restrict__ plist,
+                              size_t i0, size_t i1, unsigned long long *out) {
+    const int a = plist[blockIdx.y];   // a plane of the gather's region, its rows [i0, i1) / N2p
+    const double2 *s = g + (size_t)a * per_slab;
     double m = 0.0;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per_slab; i += (size_t)gridDim.x * blockDim.x) {
+    for (size_t i = i0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < i1; i += (size_t)gridDim.x * blockDim.x) {
         const double2 v = s[i];
         const double a = fmax(fabs(v.x), fabs(v.y));
         m = (a != a) ? INFINITY : fmax(m, a);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out + blockIdx.y, (unsigned long long)__double_as_longlong(m));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + a, (unsigned long long)__double_as_longlong(m));
+}
+
+// the int8 gather's grid region (plan time): planes and padded rows its tiles'
+// TMA boxes read (slab e0 of a tile with an odd chunk count is read with zero
+// weights and needs no digits)
+__global__ void k_gather_region(const Tile *__restrict__ tiles, int64_t n, WindowParams wp, int *planes,
+                                int *rows) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Tile t = tiles[i];
+    for (int a = 0; a < t.e0; ++a) planes[wrap1(t.o0 + a, wp.N0)] = 1;
+    atomicMin(rows, t.o1 + wp.pad);
+    atomicMax(rows + 1, min(wp.N1p, t.o1 + wp.pad + kI8Box1));
 }
 
 // per tile: the shift of its largest slab (the tile's fixed-point reference)
@@ -411,16 +426,18 @@ __global__ void k_slab_shift(const unsigned long long *__restrict__ mx, int n, i
 // row is 1280 B (6 rows per box) instead of 480 rows of 16 B.  Thread = 4
 // consecutive cells.
 __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int ncb, const int *__restrict__ gsh,
+                             const int *__restrict__ plist, int nplanes, int row0, int nrows,
                              uint8_t *__restrict__ dig) {
-    const int64_t total = (int64_t)wp.N0 * ncb * wp.N1p * 4;
+    // the gather's region only: planes plist[0 .. nplanes), rows row0 .. row0 + nrows
+    const int64_t total = (int64_t)nplanes * ncb * nrows * 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int c4 = (int)(i & 3);
         int64_t r = i >> 2;
-        const int b = (int)(r % wp.N1p);
-        r /= wp.N1p;
+        const int b = row0 + (int)(r % nrows);
+        r /= nrows;
         const int cb = (int)(r % ncb);
-        const int a = (int)(r / ncb);
+        const int a = plist[r / ncb];
         const int sh = gsh[a];
         const double sc = sh == NOSLAB ? 0.0 : ldexp(1.0, sh);
         const double2 *row = g + ((size_t)a * wp.N1p + b) * wp.N2p;
@@ -491,6 +508,30 @@ int setup_i8(Plan &p) {
         p.i8s = false;
         return SGL_OK;
     }
+    // the grid region the tiles read
+    p.n_gplanes = 0;
+    p.grow0 = 0;
+    p.grow1 = 0;
+    if (p.n_itiles > 0) {
+        int *d = nullptr;
+        SGL_CUDA_CHECK(cudaMalloc(&d, sizeof(int) * (w.N0 + 2)));
+        std::vector<int> h(w.N0 + 2, 0);
+        h[w.N0] = w.N1p;   // row min, row max
+        SGL_CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(int) * (w.N0 + 2), cudaMemcpyHostToDevice));
+        k_gather_region<<<(unsigned)((p.n_itiles + 255) / 256), 256>>>(p.itiles, p.n_itiles, w, d, d + w.N0);
+        const cudaError_t e = cudaMemcpy(h.data(), d, sizeof(int) * (w.N0 + 2), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        SGL_CUDA_CHECK(e);
+        std::vector<int> pl;
+        for (int a = 0; a < w.N0; ++a)
+            if (h[a]) pl.push_back(a);
+        p.n_gplanes = (int)pl.size();
+        p.grow0 = h[w.N0];
+        p.grow1 = std::max(h[w.N0 + 1], h[w.N0]);
+        SGL_CUDA_CHECK(cudaMalloc(&p.gplist, sizeof(int) * std::max<size_t>(1, pl.size())));
+        if (!pl.empty())
+            SGL_CUDA_CHECK(cudaMemcpy(p.gplist, pl.data(), sizeof(int) * pl.size(), cudaMemcpyHostToDevice));
+    }
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult qr;
         void *fn = nullptr;
@@ -527,12 +568,17 @@ int launch_gather_i8(const Plan &p, const double2 *grid, double2 *values, cudaSt
     int *gsh = reinterpret_cast<int *>(mx + p.wp.N0);
     SGL_CUDA_CHECK(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * p.wp.N0, st));
     const size_t per_slab = (size_t)p.wp.N1p * p.wp.N2p;
-    const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (per_slab + 8191) / 8192));
-    k_slab_absmax<<<dim3(bx, p.wp.N0), 256, 0, st>>>(grid, per_slab, mx);
+    const int nrows = p.grow1 - p.grow0;
+    const size_t region = (size_t)nrows * p.wp.N2p;   // slab elements the gather reads
+    const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>(64, (region + 8191) / 8192));
+    if (p.n_gplanes > 0 && nrows > 0)
+        k_slab_absmax<<<dim3(bx, p.n_gplanes), 256, 0, st>>>(grid, per_slab, p.gplist, (size_t)p.grow0 * p.wp.N2p,
+                                                             (size_t)p.grow1 * p.wp.N2p, mx);
     SGL_CUDA_CHECK(cudaGetLastError());
     k_slab_shift<<<(p.wp.N0 + 255) / 256, 256, 0, st>>>(mx, p.wp.N0, gsh, &p.guard->fwd);
     SGL_CUDA_CHECK(cudaGetLastError());
-    k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.digits);   // P2 = column blocks
+    if (p.n_gplanes > 0 && nrows > 0)   // P2 = column blocks
+        k_slice_grid<<<sms * 16, 256, 0, st>>>(grid, p.wp, p.P2, gsh, p.gplist, p.n_gplanes, p.grow0, nrows, p.digits);
     SGL_CUDA_CHECK(cudaGetLastError());
     int *tsh = gsh + p.wp.N0;
     k_tile_shift<<<(unsigned)((p.n_itiles + 255) / 256), 256, 0, st>>>(p.itiles, p.n_itiles, p.wp, gsh, tsh);

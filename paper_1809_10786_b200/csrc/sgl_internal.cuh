@@ -187,6 +187,11 @@ struct Plan {
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
     int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
+    // the grid region the int8 gather's tiles read (plan time): their axis-0
+    // planes (device list) and padded axis-1 rows [grow0, grow1); slab maxima
+    // and digit planes are made for it only
+    int *gplist = nullptr;
+    int n_gplanes = 0, grow0 = 0, grow1 = 0;
     alignas(64) CUtensorMap dmap;  // TMA descriptor of the digit planes
 
     // int8 accuracy guard and debug counters (guard.cu)
