@@ -89,6 +89,7 @@ void free_plan(Plan *p) {
     for (auto &e : p->slab_ffts) cufftDestroy(e.second);
     for (auto &e : p->axis0_ffts) cufftDestroy(e.second);
     if (p->dist_fft1) cufftDestroy(p->dist_fft1);
+    for (int k = 0; k < p->n_fft1r; ++k) cufftDestroy(p->fft1r[k]);
     if (p->done) cudaEventDestroy(p->done);
     if (p->ev_a) cudaEventDestroy(p->ev_a);
     if (p->ev_b) cudaEventDestroy(p->ev_b);
@@ -198,11 +199,22 @@ int grid_fft(Plan &p, cudaStream_t st, int dir) {
         }
         return r;
     };
+    auto axis0 = [&]() {   // all columns, or only the rows the window stages touch
+        if (!(p.fft_rows_on && p.n_fft1r > 0))
+            return fft_check(cufftExecZ2Z(p.fft1, all, all, dir), "cufftExecZ2Z(1d)");
+        int r = SGL_OK;
+        for (int k = 0; k < p.n_fft1r && !r; ++k) {
+            r = fft_check(cufftSetStream(p.fft1r[k], st), "cufftSetStream");
+            cufftDoubleComplex *rows = all + (size_t)p.fft1r_row0[k] * p.wp.N2p;
+            if (!r) r = fft_check(cufftExecZ2Z(p.fft1r[k], rows, rows, dir), "cufftExecZ2Z(1d rows)");
+        }
+        return r;
+    };
     if (dir == CUFFT_INVERSE) {
         rc = planes();
-        if (!rc) rc = fft_check(cufftExecZ2Z(p.fft1, all, all, dir), "cufftExecZ2Z(1d)");
+        if (!rc) rc = axis0();
     } else {
-        rc = fft_check(cufftExecZ2Z(p.fft1, all, all, dir), "cufftExecZ2Z(1d)");
+        rc = axis0();
         if (!rc) rc = planes();
     }
     return rc;
@@ -581,6 +593,7 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         if (rc == SGL_OK) rc = read_absmax(*p, p->coef_buf, p->count, st, &p->guard_ap);
         plan_lap(*p, st, "guard calibration");
     }
+    p->fft_rows_on = p->n_fft1r > 0;   // (after the guard calibration's full-grid transform)
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");
         rc = SGL_ECUDA;

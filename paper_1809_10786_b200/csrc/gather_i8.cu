@@ -479,6 +479,64 @@ void i8_scales(const Plan &p, double &s0, double &s2, int &sA) {
 
 }  // namespace
 
+// The pruned FFT's axis-0 pass over the rows the window stages can touch:
+// the region rows inside the interior, and the interior rows whose periodic
+// images are the region's halo rows (k_halo_fill / k_halo_fold).  The FP64
+// tiled gather (the guard's fallback) loads 36-row TMA boxes that may end up
+// to a few rows past its nodes' windows; the region gets that margin.  Rows
+// outside are never read by a window kernel after the forward and never
+// written with nonzero values by the adjoint's spread, so their axis-0
+// transforms are skipped (the adjoint's are transforms of zeros).
+void setup_fft_rows(Plan &p) {
+    const WindowParams &w = p.wp;
+    if (!p.pruned || p.raw) return;
+    const int pad = w.pad, N1 = p.grid[1];
+    const int g0 = std::max(0, p.grow0 - 4), g1 = std::min(w.N1p, p.grow1 + 4);
+    std::vector<std::pair<int, int>> iv;
+    auto add = [&](int a, int b) {
+        a = std::max(a, pad);
+        b = std::min(b, pad + N1);
+        if (b > a) iv.emplace_back(a, b);
+    };
+    add(g0, g1);
+    add(g0 + N1, std::min(g1, pad) + N1);            // images of the low halo rows
+    add(std::max(g0, pad + N1) - N1, g1 - N1);      // images of the high halo rows
+    std::sort(iv.begin(), iv.end());
+    std::vector<std::pair<int, int>> m;
+    for (auto &x : iv) {
+        if (!m.empty() && x.first <= m.back().second) m.back().second = std::max(m.back().second, x.second);
+        else m.push_back(x);
+    }
+    int rows = 0;
+    for (auto &x : m) rows += x.second - x.first;
+    if (m.empty() || m.size() > 3 || rows > N1 * 9 / 10) return;   // little to gain
+    long long n1[1] = {p.grid[0]}, e1[1] = {p.grid[0]};
+    const long long pl = (long long)w.N1p * w.N2p;
+    size_t wfull = 0;
+    cufftGetSize(p.fft1, &wfull);
+    int k = 0;
+    for (auto &x : m) {
+        cufftHandle h = 0;
+        size_t ws = 0;
+        bool ok = cufftCreate(&h) == CUFFT_SUCCESS;
+        ok = ok && cufftSetAutoAllocation(h, 0) == CUFFT_SUCCESS &&
+             cufftMakePlanMany64(h, 1, n1, e1, pl, 1, e1, pl, 1, CUFFT_Z2Z, (long long)(x.second - x.first) * w.N2p,
+                                 &ws) == CUFFT_SUCCESS &&
+             ws <= wfull && cufftSetWorkArea(h, p.fft_work) == CUFFT_SUCCESS;
+        if (!ok) {   // keep the full axis-0 pass
+            if (h) cufftDestroy(h);
+            for (int j = 0; j < k; ++j) cufftDestroy(p.fft1r[j]);
+            p.n_fft1r = 0;
+            cudaGetLastError();
+            return;
+        }
+        p.fft1r[k] = h;
+        p.fft1r_row0[k] = x.first;
+        ++k;
+    }
+    p.n_fft1r = k;
+}
+
 int setup_i8(Plan &p) {
     const WindowParams &w = p.wp;
     if (p.n_itiles > 0) {
@@ -531,6 +589,7 @@ int setup_i8(Plan &p) {
         SGL_CUDA_CHECK(cudaMalloc(&p.gplist, sizeof(int) * std::max<size_t>(1, pl.size())));
         if (!pl.empty())
             SGL_CUDA_CHECK(cudaMemcpy(p.gplist, pl.data(), sizeof(int) * pl.size(), cudaMemcpyHostToDevice));
+        setup_fft_rows(p);
     }
     static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
         cudaDriverEntryPointQueryResult qr;

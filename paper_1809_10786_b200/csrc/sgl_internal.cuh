@@ -192,6 +192,14 @@ struct Plan {
     // and digit planes are made for it only
     int *gplist = nullptr;
     int n_gplanes = 0, grow0 = 0, grow1 = 0;
+    // the pruned FFT's axis-0 pass over those rows only (plus the interior rows
+    // whose images fill the region's halo rows): no window stage reads or
+    // writes the other rows.  Plans per row interval (setup_i8); enabled after
+    // the adjoint guard's calibration, which transforms the full grid.
+    cufftHandle fft1r[3] = {0, 0, 0};
+    int fft1r_row0[3] = {0, 0, 0};
+    int n_fft1r = 0;
+    bool fft_rows_on = false;
     alignas(64) CUtensorMap dmap;  // TMA descriptor of the digit planes
 
     // int8 accuracy guard and debug counters (guard.cu)
