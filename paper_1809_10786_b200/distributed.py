@@ -69,7 +69,17 @@ def shard_indices(points, rank: int, world: int, mode: str = "radial") -> np.nda
     if mode == "contiguous":
         return np.arange(s0, s1)
     order = np.argsort(pts[:, 0 if mode == "radial" else 1], kind="stable")
-    return np.sort(order[s0:s1])
+    if mode == "radial" or M == 0:
+        return np.sort(order[s0:s1])
+    # theta: equal shares of estimated work rather than of nodes.  Near the
+    # poles the nodes spread over more window tiles per node (the bands are
+    # wider in theta and sparser in the grid): weight 1 + 0.25 (1 - sin theta)
+    # evens the ranks' times at config 3, N = 8 (tools/shard_probe.py)
+    wgt = 1.0 + 0.25 * (1.0 - np.sin(pts[order, 1]))
+    cum = np.cumsum(wgt)
+    edges = np.searchsorted(cum, cum[-1] * np.arange(world + 1) / world, side="left")
+    edges[0], edges[-1] = 0, M
+    return np.sort(order[edges[rank]:edges[rank + 1]])
 
 
 @dataclass

@@ -177,11 +177,15 @@ def test_shard_indices_partition():
     from paper_1809_10786_b200.distributed import shard_indices, shard_bounds
     rng = np.random.default_rng(3)
     pts = rng.random((1001, 3)) * [7.0, 3.0, 6.0]
-    for mode in ("contiguous", "radial"):
+    for mode in ("contiguous", "radial", "theta"):
         parts = [shard_indices(pts, k, 4, mode) for k in range(4)]
-        assert [len(x) for x in parts] == [b - a for a, b in (shard_bounds(1001, k, 4) for k in range(4))]
+        if mode != "theta":   # (theta: equal shares of weighted work)
+            assert [len(x) for x in parts] == [b - a for a, b in (shard_bounds(1001, k, 4) for k in range(4))]
         assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(1001))
         assert all(np.all(np.diff(x) > 0) for x in parts)
+    th = [shard_indices(pts, k, 4, "theta") for k in range(4)]
+    assert all(pts[th[k], 1].max() <= pts[th[k + 1], 1].min() for k in range(3))
+    assert abs(len(th[0]) - 1001 / 4) < 60
     rad = [shard_indices(pts, k, 4, "radial") for k in range(4)]
     assert all(pts[rad[k], 0].max() <= pts[rad[k + 1], 0].min() for k in range(3))
     import pytest
