@@ -116,7 +116,10 @@ typedef struct {
     int64_t i8_ksteps;        /* K-steps of 32 per gather pass (9 MMAs each,
                                  M = 128, N = 1680 digit columns in total)     */
     int32_t i8_scatter;       /* 1 if the adjoint window stage runs on the int8
-                                 tensor cores (dense node sets, or forced)     */
+                                 tensor cores (chosen for >= 1e5 nodes at < 1.5
+                                 K-steps per node, or forced); 0 again once an
+                                 automatic choice switched itself off after two
+                                 consecutive accuracy-guard fallbacks          */
     int64_t i8_sksteps;       /* its K-steps (32 nodes x 128 cells) per pass   */
     int32_t guard;            /* 1 if the int8 accuracy guard is on            */
     double guard_ap;          /* adjoint guard: the tail's noise response (plan time) */

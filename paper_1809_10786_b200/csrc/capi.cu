@@ -770,7 +770,7 @@ int sgl_plan_get_info(const sgl_plan *plan, sgl_plan_info *info) {
     info->i8_gather = p.i8 ? 1 : 0;
     info->i8_tiles = p.n_itiles;
     info->i8_ksteps = p.i8_ksteps;
-    info->i8_scatter = p.i8s ? 1 : 0;
+    info->i8_scatter = p.i8s_live() ? 1 : 0;   // the engine the adjoint uses now (Plan::i8s_off)
     info->i8_sksteps = p.i8_sksteps;
     info->guard = p.guard_on ? 1 : 0;
     info->guard_ap = p.guard_ap;

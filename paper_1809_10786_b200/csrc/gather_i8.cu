@@ -489,7 +489,9 @@ void i8_scales(const Plan &p, double &s0, double &s2, int &sA) {
 // transforms are skipped (the adjoint's are transforms of zeros).
 void setup_fft_rows(Plan &p) {
     const WindowParams &w = p.wp;
-    if (!p.pruned || p.raw) return;
+    // small grids: the extra cuFFT launches outweigh the skipped rows
+    // (config 1, 128 x 128 x 64: 0.253 -> 0.271 ms per forward)
+    if (!p.pruned || p.raw || p.grid_elems < ((size_t)1 << 24)) return;
     const int pad = w.pad, N1 = p.grid[1];
     const int g0 = std::max(0, p.grow0 - 4), g1 = std::min(w.N1p, p.grow1 + 4);
     std::vector<std::pair<int, int>> iv;

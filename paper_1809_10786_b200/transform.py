@@ -101,7 +101,10 @@ class SglPlan:
 
     @property
     def stats(self) -> dict:
-        i = self._info
+        """Plan statistics; `i8_scatter` is the adjoint's current engine (an
+        automatic int8 choice can switch itself off at run time)."""
+        i = _native.PlanInfo()
+        _native.check(_native.lib().sgl_plan_get_info(self._handle, ctypes.byref(i)))
         return {"n_tiles": int(i.n_tiles), "tile_nodes": int(i.tile_nodes), "tile_dmma": int(i.tile_dmma),
                 "generic": bool(i.generic), "plan_ms": float(i.plan_ms), "i8_gather": bool(i.i8_gather),
                 "i8_tiles": int(i.i8_tiles), "i8_ksteps": int(i.i8_ksteps), "i8_scatter": bool(i.i8_scatter),
