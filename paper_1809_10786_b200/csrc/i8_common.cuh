@@ -122,23 +122,23 @@ __device__ __forceinline__ void digits16(double w0, const double (&w)[16], uint3
     }
 }
 
-// digits16 with an entry mask (bit e: entry e inside the node's window): the
-// bytes of masked-out entries are cleared with the same LOP3 that rebalances
-// the digits, instead of a compare + select per entry on the FP64 inputs
-// (outside the window the weights are finite, smaller than inside, and their
-// digits are discarded)
-__device__ __forceinline__ void digits16_masked(double w0, const double (&w)[16], uint32_t mask16,
+// 16 entries y_e = fma(a[e], b[e], MAGIC_BAL) -> digit planes as digits16,
+// with an entry mask (bit e: entry e inside the node's window): the bytes of
+// masked-out entries are cleared with the same LOP3 that rebalances the
+// digits, instead of a compare + select per entry on the FP64 inputs (outside
+// the window the weights are finite, smaller than inside, and their digits
+// are discarded)
+__device__ __forceinline__ void digits16_masked(const double (&a)[16], const double (&b)[16], uint32_t mask16,
                                                 uint32_t (&dw)[ND][4]) {
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4) {
         uint32_t L[4], H[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const double y = fma(w0, w[q4 * 4 + e], MAGIC_BAL);
+            const double y = fma(a[q4 * 4 + e], b[q4 * 4 + e], MAGIC_BAL);
             L[e] = (uint32_t)__double2loint(y);
             H[e] = (uint32_t)__double2hiint(y);
         }
-        // 4 mask bits -> 4 byte masks: bit i lands at 8 i, times 0xff
         const uint32_t bm = ((((mask16 >> (4 * q4)) & 0xfu) * 0x00204081u) & 0x01010101u) * 0xffu;
         const uint32_t t0 = prmt(L[0], L[1], 0x5140), t1 = prmt(L[2], L[3], 0x5140);
         const uint32_t t2 = prmt(L[0], L[1], 0x7362), t3 = prmt(L[2], L[3], 0x7362);
@@ -161,15 +161,21 @@ __device__ __forceinline__ double combine6(int32_t d0, int32_t d1, int32_t d2, i
     return fma((double)hi, 4294967296.0 * unit, (double)lo * unit);
 }
 
-// combine6 for sums of at most 512 products (the int8 scatter's K = one tile's
-// nodes): |operands| < 2^46 in balanced digits bound the diagonal sum by
-// 2^(92 + 9 - 40) = 2^61, so the 6 diagonals combine exactly in one int64 and
-// convert once (one rounding, as combine6)
-__device__ __forceinline__ double combine6_k512(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4, int32_t d5,
-                                                double unit) {
-    const long long x = (long long)d0 + ((long long)d1 << 8) + ((long long)d2 << 16) + ((long long)d3 << 24) +
-                        ((long long)d4 << 32) + ((long long)d5 << 40);
-    return (double)x * unit;
+// the 6 diagonals of a sum of at most 512 products (the int8 scatter's K =
+// one tile's nodes) as one exact int64 in units of 256^DMIN: |operands| <
+// 2^46 in balanced digits bound the diagonal sum by 2^(92 + 9 - 40) = 2^61
+// (the caller converts it once, after the TMEM release)
+__device__ __forceinline__ long long combine6_i64(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4,
+                                                  int32_t d5) {
+    // the sum fits an int64, so wrapping arithmetic is exact: three
+    // IMAD.WIDE for the low diagonals, d4 + 256 d5 added to the high word
+    // modulo 2^32 (no carry chains)
+    long long x = (long long)d0 + (long long)d1 * 256;
+    x += (long long)d2 * 65536;
+    x += (long long)d3 * 16777216;
+    const uint32_t hadd = (uint32_t)d4 + ((uint32_t)d5 << 8);
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)((unsigned long long)x >> 32) + hadd;
+    return (long long)(((unsigned long long)hi << 32) | lo);
 }
 
 }  // namespace i8

@@ -17,7 +17,7 @@
 // k_vdigits into global memory, already in the MN-major UMMA layout of a
 // K-step (15 KB per 32 nodes), and a producer warp streams them into shared
 // memory with 1-D bulk copies (cp.async.bulk, L2-resident across the tile's
-// M-blocks).  Only W is built on the fly, by 8 generator warps (node x
+// M-blocks).  Only W is built on the fly, by 16 generator warps (node x
 // 16-cell group, weights from per-node factors in shared memory), stored with
 // st.async.  The epilogue converts an M-block to FP64 into a per-thread
 // staging column, frees TMEM for the next block's MMAs and only then reduces
@@ -26,8 +26,9 @@
 // per node.
 //
 // CTA (one per SM, persistent, cluster of 1 for st.async): warp 0 MMA
-// issuer, warp 1 value-digit producer, warps 2-9 weight-digit generators,
-// warps 10-13 epilogue (TMEM lane quarters = cells).
+// issuer, warp 1 value-digit producer, warps 2-17 weight-digit generators (two
+// groups of 8 on alternating K-steps), warps 18-25 epilogue (two per TMEM lane
+// quarter = cells, half the columns each).
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -48,10 +49,7 @@ namespace {
 using namespace i8;
 
 
-#ifndef SGL_COMBINE
-#define SGL_COMBINE combine6_k512   // SN = 512 products per diagonal sum (see i8_common.cuh)
-#endif
-static_assert(kI8SNodes <= 512, "combine6_k512 needs at most 512 nodes per tile");
+static_assert(kI8SNodes <= 512, "combine6_i64 needs at most 512 nodes per tile");
 
 constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
@@ -72,7 +70,7 @@ constexpr int ST = (2 + NWG + NEW) * 32;
 struct SSmem {
     uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
     uint8_t b[NSTGB][B_STAGE];   // value digits  [node/8][digit][col/16][node%8][col%16]
-    double stage[ROWS][MR];      // epilogue: one M-block in FP64, [column][cell]
+    long long stage[ROWS][MR];   // epilogue: one M-block as exact int64 sums, [column][cell]
     double e2[CHUNKS][SN], f2[CHUNKS][SN];   // W2 of chunk cc: w(cb + j) = e2 f2^j exp(-h2 j^2)
     int win2[SN];                // axis-2 window relative to K column 0: lo | hi << 16 (signed)
     double w0t[4][SN];           // W0 of the current M-block's (<= 4) slabs, row = slab & 3
@@ -366,10 +364,18 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     const int stg = (int)(g % NSTG);
                     const uint32_t use = g / NSTG;
                     const int kn = ks * KST;
-                    // w2(cb + j) = e f^j g_j: powers of f by a depth-4 product tree
-                    const double w0 = w0p[kn], e = e2p[kn], f = f2p[kn];
+                    // W0 folded into the chunk factor: w0 w2(cb + j) = (w0 e) f^j g_j, so
+                    // the g_j product is the digit FMA itself (one DMUL per entry fewer;
+                    // scatter 29.67 -> 29.56 ms at config 3)
+                    const double e = w0p[kn] * e2p[kn], f = f2p[kn];
                     const int wn = win2p[kn], jlo = (int)(short)(wn & 0xffff) - 16 * cc, jhi = (wn >> 16) - 16 * cc;
-                    double pw[16], w2[16];
+                    // the node's window [jlo, jhi] inside this 16-cell chunk as an entry mask
+                    const uint32_t mask = (jhi < 0 || jlo > 15)
+                                              ? 0u
+                                              : ((2u << min(15, jhi)) - 1u) & ~((1u << max(0, jlo)) - 1u);
+                    uint32_t dw[ND][4];
+                    // powers of f by a depth-4 product tree
+                    double pw[16];
                     pw[0] = e;
                     pw[1] = e * f;
                     const double f2 = f * f, f4 = f2 * f2, f8 = f4 * f4;
@@ -381,14 +387,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     pw[7] = pw[3] * f4;
 #pragma unroll
                     for (int j = 8; j < 16; ++j) pw[j] = pw[j - 8] * f8;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) w2[j] = pw[j] * g2[j];
-                    // the node's window [jlo, jhi] inside this 16-cell chunk as an entry mask
-                    const uint32_t mask = (jhi < 0 || jlo > 15)
-                                              ? 0u
-                                              : ((2u << min(15, jhi)) - 1u) & ~((1u << max(0, jlo)) - 1u);
-                    uint32_t dw[ND][4];
-                    digits16_masked(w0, w2, mask, dw);
+                    digits16_masked(pw, g2.v, mask, dw);
                     const long long x2 = tick<PROF>();
                     if (use) mbar_wait(&S.emptyA[stg], (use - 1) & 1);
                     qe += tick<PROF>() - x2;
@@ -441,10 +440,12 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                         for (int k = 0; k < NBLK; ++k)
                             umma::tmem_ld4(tl + (uint32_t)(k * ROWS + (c0 + i + 1) * 4), D[cur ^ 1][k]);
                     }
+                    // the exact int64 only: its conversion to FP64 waits until after
+                    // the TMEM release (scatter 29.73 -> 29.29 ms at config 3)
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        S.stage[(c0 + i) * 4 + j][m] = SGL_COMBINE(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
-                                                                D[cur][4][j], D[cur][5][j], unit);
+                        S.stage[(c0 + i) * 4 + j][m] = combine6_i64(D[cur][0][j], D[cur][1][j], D[cur][2][j],
+                                                                    D[cur][3][j], D[cur][4][j], D[cur][5][j]);
                     umma::tmem_ld_wait();
                 }
                 umma::fence_before();
@@ -452,7 +453,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
                 if (inbox) {
                     for (int b = eh * (ROWS / 2 / EPW); b < min(t.e1, (eh + 1) * (ROWS / 2 / EPW)); ++b) {
-                        const double re = S.stage[2 * b][m], im = S.stage[2 * b + 1][m];
+                        const double re = (double)S.stage[2 * b][m] * unit, im = (double)S.stage[2 * b + 1][m] * unit;
                         double *q = gp + 2 * (size_t)b * wp.N2p;
                         SGL_DCHECK(wrap1(t.o0 + al, wp.N0) < wp.N0 && t.o1 + wp.pad + b < wp.N1p &&
                                    kst + cl >= 0 && kst + cl < wp.N2p);
