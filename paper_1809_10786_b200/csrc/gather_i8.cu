@@ -20,18 +20,20 @@
 // p + q share one int32 TMEM accumulator (6 "diagonals" x 80 columns = 480
 // of the 512 TMEM columns), and one MMA multiplies A digit p with up to
 // three consecutive B digits stacked along N (N = 240), 9 MMAs per K-step of
-// 32.  The epilogue converts the diagonals to FP64, applies the scale and the
-// axis-1 weights w1[n,b] and writes the node values in caller order.
+// 32.  The epilogue combines the diagonals of a column into one exact int64,
+// converts it, applies the axis-1 weights w1[n,b] and the scale and writes
+// the node values in caller order.
 //
 // Grid digits are produced once per forward (k_slice_grid, after the halo
 // fill) as [a][c/16][digit][b][re|im][c%16] and reach shared memory by TMA
 // (one 6-digit x 1280-byte box per K-chunk).  The weight digits are
-// built per tile by 8 generator warps directly in the UMMA K-major layout.
+// built per tile by 12 generator warps directly in the UMMA K-major layout.
 //
 // CTA (one per SM, persistent over tiles): warp 0 TMA producer, warp 1 MMA
 // issuer (one lane), warps 2-13 weight-digit generators, warps 14-17 epilogue
-// (TMEM lane quarters).  5-stage weight-digit ring and 7-stage grid-digit ring (full / empty mbarriers), TMEM
-// full / empty mbarriers between the MMA issuer and the epilogue.
+// (TMEM lane quarters).  4-stage weight-digit ring and 8-stage grid-digit
+// ring (full / empty mbarriers), TMEM full / empty mbarriers between the MMA
+// issuer and the epilogue.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -51,6 +53,7 @@ namespace {
 using namespace i8;
 
 constexpr int IM = kI8Nodes;              // MMA M (nodes)
+static_assert(kMaxQTiled <= 16, "combine6_i64 in the gather needs (2q + 1)^2 <= 2^11 window cells");
 constexpr int ROWS = 2 * kI8Box1;         // MMA N per digit: (b, re|im)
 constexpr int NSTG = 4;                   // weight-digit ring depth (K-steps of 32)
 constexpr int NSTGB = 8;                  // grid-digit (TMA) ring depth: hides the L2 latency
@@ -337,9 +340,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
                     for (int k = 0; k < NBLK; ++k) umma::tmem_ld4(tl + (uint32_t)(k * ROWS + (i + 1) * 4), D[cur ^ 1][k]);
                 }
                 double v[4];
+                // one exact int64 per column (a node's weights are nonzero on at most
+                // (2q + 1)^2 <= 33^2 cells, so |sum| < 2^(46 + 46 + 10.1 - 40) < 2^63
+                // for any K); the power-of-two unit is applied once per node
 #pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = combine6(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
-                                                            D[cur][4][j], D[cur][5][j], unit);
+                for (int j = 0; j < 4; ++j)
+                    v[j] = (double)combine6_i64(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j], D[cur][4][j],
+                                                D[cur][5][j]);
 #pragma unroll
                 for (int jb = 0; jb < 2; ++jb) {
                     const int b = i * 2 + jb;
@@ -357,7 +364,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(IT, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.tempty);
             SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
-            if (live) out[nodes.perm[si]] = make_double2(acc_re, acc_im);
+            if (live) out[nodes.perm[si]] = make_double2(acc_re * unit, acc_im * unit);
         }
     }
 

@@ -152,19 +152,11 @@ __device__ __forceinline__ void digits16_masked(const double (&a)[16], const dou
     }
 }
 
-// the 6 diagonal accumulators of one column, D_k weighted 256^k, as a double
-// in units of 256^DMIN (two exact int64 halves, two conversions)
-__device__ __forceinline__ double combine6(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4, int32_t d5,
-                                           double unit) {
-    const long long lo = (long long)d0 + (long long)d1 * 256 + (long long)d2 * 65536 + (long long)d3 * 16777216;
-    const long long hi = (long long)d4 + (long long)d5 * 256;
-    return fma((double)hi, 4294967296.0 * unit, (double)lo * unit);
-}
-
-// the 6 diagonals of a sum of at most 512 products (the int8 scatter's K =
-// one tile's nodes) as one exact int64 in units of 256^DMIN: |operands| <
-// 2^46 in balanced digits bound the diagonal sum by 2^(92 + 9 - 40) = 2^61
-// (the caller converts it once, after the TMEM release)
+// the 6 diagonal accumulators of one column, D_k weighted 256^k, as one exact
+// int64 in units of 256^DMIN (converted once by the caller).  |operands| <
+// 2^46 in balanced digits: the scatter's sums of <= 512 products are bounded
+// by 2^(92 + 9 - 40) = 2^61; the gather's by 2^(92 + 10.1 - 40) since a node's
+// weights are nonzero on at most (2q + 1)^2 <= 33^2 cells (q <= kMaxQTiled)
 __device__ __forceinline__ long long combine6_i64(int32_t d0, int32_t d1, int32_t d2, int32_t d3, int32_t d4,
                                                   int32_t d5) {
     // the sum fits an int64, so wrapping arithmetic is exact: three
