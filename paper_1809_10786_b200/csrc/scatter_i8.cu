@@ -359,10 +359,14 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 // this thread's node tables for the M-block (padding nodes have e = 0)
                 const double *w0p = S.w0t[al & 3] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
                 const int *win2p = S.win2 + kl;
-                for (int ks = 0; ks < nks; ++ks, ++g) {
-                    if ((int)(g % NGRP) != hg) continue;   // the other group's K-step
-                    const int stg = (int)(g % NSTG);
-                    const uint32_t use = g / NSTG;
+                // this group's K-steps of the M-block only (global K-step g0 + ks; a
+                // strided loop instead of skipping the other group's: 29.19 -> 29.08 ms)
+                const uint32_t g0 = g;
+                g += nks;
+                for (int ks = (int)(((uint32_t)hg + NGRP - g0 % NGRP) % NGRP); ks < nks; ks += NGRP) {
+                    const uint32_t gk = g0 + ks;
+                    const int stg = (int)(gk % NSTG);
+                    const uint32_t use = gk / NSTG;
                     const int kn = ks * KST;
                     // W0 folded into the chunk factor: w0 w2(cb + j) = (w0 e) f^j g_j, so
                     // the g_j product is the digit FMA itself (one DMUL per entry fewer;

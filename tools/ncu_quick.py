@@ -24,9 +24,21 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(src)))
 hi = [i for i, r in enumerate(rows[:5]) if "Source" in r][0]
 hdr = rows[hi]; isrc = hdr.index("Source"); ia = hdr.index("Address"); ws = hdr.index("Warp Stall Sampling (All Samples)")
+# per-PC stall reasons (sampled), the top three of each hot line
+reasons = [(i, h[6:]) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+
+
+def num(x):
+    try: return float(x.replace(",", ""))
+    except ValueError: return 0.0
+
+
 data = []
 for r in rows[hi + 1:]:
-    try: data.append((float(r[ws].replace(",", "")), r[ia][-5:], r[isrc][:90]))
+    try: data.append((float(r[ws].replace(",", "")), r[ia][-5:], r[isrc][:70], r))
     except ValueError: pass
 tot = sum(d[0] for d in data) or 1
-for s, a, t in sorted(data, reverse=True)[:top]: print(f"{100*s/tot:5.1f}% {a} {t}")
+for s, a, t, r in sorted(data, key=lambda d: -d[0])[:top]:
+    rs = sorted(((num(r[i]), n) for i, n in reasons), reverse=True)[:3]
+    why = " ".join(f"{n}={100 * v / s:.0f}%" for v, n in rs if v > 0) if s else ""
+    print(f"{100*s/tot:5.1f}% {a} {t:70s} {why}")
