@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-stock", action="store_true", help="skip timing the stock reference package")
     ap.add_argument("--backend", default="auto", choices=["auto", "tiled", "i8"],
                     help="window engines (experiments; the default is the library's own choice)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise reproducible adjoint (fixed-point grid reductions, SGL_FLAG_DETERMINISTIC)")
     return ap.parse_args()
 
 
@@ -353,12 +355,15 @@ def main():
     first_plan_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     # rho is global (all-reduce max over the ranks' shards) -- distributed.ShardedPlan
-    sp = ShardedPlan(w.B, pts_d, device=local, partition=args.partition, backend=args.backend) if world > 1 else None
-    p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local, backend=args.backend)
+    sp = ShardedPlan(w.B, pts_d, device=local, partition=args.partition, backend=args.backend,
+                     deterministic=args.deterministic) if world > 1 else None
+    p = sp.plan if sp is not None else sgl.plan(w.B, pts_d, device=local, backend=args.backend,
+                                                       deterministic=args.deterministic)
     rho = sp.rho if sp is not None else p.rho
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - t0
-    pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True, backend=args.backend)
+    pprof = sgl.plan(w.B, pts_d, rho=rho, device=local, profile=True, backend=args.backend,
+                    deterministic=args.deterministic)
     stream = torch.cuda.current_stream(dev)
 
     def step(pl):
@@ -560,6 +565,7 @@ def main():
             "data": "synthetic (seeded PCG64 inputs of SURVEY 8(d); no public dataset)",
             "config": bench_config(w, direction, K) | {"M": M_total},
             "config_extra": {"grid": list(p.nfft.grid_shape), "rho": rho, "l2": l2_note, "M_per_rank": w.M,
+                             "deterministic_adjoint": bool(args.deterministic),
                              "parallelism": (f"{world} GPU(s), node shards ({args.shard if strong else 'own sets'}); adjoint exchange: "
                                              f"{sp.partition if sp is not None else 'none'}"
                                              + (" (coefficient all-reduce)" if sp is not None and

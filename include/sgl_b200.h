@@ -85,11 +85,18 @@ enum {
     SGL_FLAG_NO_GUARD = 1u << 13,         /* disable the int8 accuracy guard (the
                                              per-call switch to the FP64 kernels;
                                              estimates are still recorded)          */
-    SGL_FLAG_FP64_TABLES = 1u << 14       /* build the basal matrices in FP64 (the
+    SGL_FLAG_FP64_TABLES = 1u << 14,      /* build the basal matrices in FP64 (the
                                              reference's default arithmetic) instead
                                              of x87 extended precision: config 4 is
                                              4.7e-9 from the truth this way, 1.2e-9
                                              with extended tables (reference: 2.6e-9) */
+    SGL_FLAG_DETERMINISTIC = 1u << 15     /* bitwise reproducible adjoint: the window
+                                             kernels reduce 64-bit fixed-point
+                                             integers into the grid (order-independent
+                                             sums; unit 2^-62 of max|v| x the window
+                                             density) instead of FP64 atomics, as the
+                                             reference's serial loop
+                                             (_gridding.py:77-95) is reproducible   */
 };
 
 typedef struct {

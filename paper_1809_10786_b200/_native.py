@@ -31,6 +31,7 @@ FLAG_SCATTER_NARROW = 1 << 11
 FLAG_I8_PROF = 1 << 12
 FLAG_NO_GUARD = 1 << 13
 FLAG_FP64_TABLES = 1 << 14
+FLAG_DETERMINISTIC = 1 << 15
 STAGES = ("h2d", "basal", "fft", "window", "d2h")
 
 # every symbol include/sgl_b200.h declares

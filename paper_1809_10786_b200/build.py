@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libsgl_b200.so")
 SOURCES = ["capi.cu", "nodes.cu", "basal.cu", "gridding.cu", "gather_i8.cu", "scatter_i8.cu", "exact.cu", "direct.cu",
-           "guard.cu", "dist.cu", "multi.cu"]
+           "guard.cu", "dist.cu", "multi.cu", "determ.cu"]
 HEADERS = ["sgl_internal.cuh", "umma.cuh", "i8_common.cuh", os.path.join("..", "..", "include", "sgl_b200.h")]
 
 

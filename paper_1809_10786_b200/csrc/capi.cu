@@ -77,7 +77,7 @@ void free_plan(Plan *p) {
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf, p->zeta, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
-                    p->itiles, p->digits, p->gmax, p->gplist, p->istiles, p->tsv, p->svoff, p->sktile, p->vdig, p->guard, p->prof};
+                    p->itiles, p->digits, p->gmax, p->gplist, p->istiles, p->tsv, p->svoff, p->sktile, p->vdig, p->guard, p->prof, p->det};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);
@@ -263,8 +263,7 @@ int adjoint_guard_resolve(Plan &p, const double2 *v, double2 *c, cudaStream_t st
     p.i8s_streak = redo ? p.i8s_streak + 1 : 0;
     if (p.i8s_auto && p.i8s_streak >= 2) p.i8s_off = true;   // the FP64 scatter from the next call on
     if (!redo) return SGL_OK;
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    int rc = launch_scatter(p, v, p.grid_buf, st);
+    int rc = spread_stage(p, v, st, false);
     if (rc) return rc;
     return adjoint_tail(p, c, st, nullptr);
 }
@@ -283,8 +282,7 @@ int adjoint_core(Plan &p, const double2 *v, double2 *c, cudaStream_t st, StageRe
         mark(SGL_STAGE_BASAL);
         return p.raw ? launch_crop_raw(p, p.grid_buf, c, st) : launch_basal_adjoint(p, p.grid_buf, c, st);
     }
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    rc = p.i8s_live() ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
+    rc = spread_stage(p, v, st, true);
     if (rc) return rc;
     rc = adjoint_tail(p, c, st, rec);
     if (rc || !(p.i8s_live() && p.guard_ap > 0.0 && p.M > 0)) return rc;
@@ -593,6 +591,8 @@ int plan_finish(Plan *p, const double *points, cudaStream_t st, sgl_plan **out,
         if (rc == SGL_OK) rc = read_absmax(*p, p->coef_buf, p->count, st, &p->guard_ap);
         plan_lap(*p, st, "guard calibration");
     }
+    if (rc == SGL_OK) rc = setup_det(*p, st);   // SGL_FLAG_DETERMINISTIC: window density (determ.cu)
+    plan_lap(*p, st, "deterministic-adjoint density");
     p->fft_rows_on = p->n_fft1r > 0;   // (after the guard calibration's full-grid transform)
     if (rc == SGL_OK && cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaEventCreate failed");

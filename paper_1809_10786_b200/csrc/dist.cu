@@ -191,8 +191,7 @@ int sgl_adjoint_spread(sgl_plan *plan, const sgl_cdouble *values, void *stream) 
         SGL_CUDA_CHECK(cudaMemcpyAsync(p.val_buf, v, sizeof(double2) * p.M, cudaMemcpyHostToDevice, st));
         v = p.val_buf;
     }
-    SGL_CUDA_CHECK(cudaMemsetAsync(p.grid_buf, 0, sizeof(double2) * p.grid_elems, st));
-    rc = p.i8s_live() ? launch_scatter_guarded(p, v, p.grid_buf, st) : launch_scatter(p, v, p.grid_buf, st);
+    rc = spread_stage(p, v, st, true);
     if (rc) return rc;
     rc = launch_halo_fold(p, p.grid_buf, st);
     if (rc) return rc;

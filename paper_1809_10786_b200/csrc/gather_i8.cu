@@ -386,8 +386,7 @@ __global__ void k_slab_absmax(const double2 *__restrict__ g, size_t per_slab, co
     double m = 0.0;
     for (size_t i = i0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < i1; i += (size_t)gridDim.x * blockDim.x) {
         const double2 v = s[i];
-        const double a = fmax(fabs(v.x), fabs(v.y));
-        m = (a != a) ? INFINITY : fmax(m, a);
+        m = fmax(m, cabsmax_naninf(v));   // NaN counts as +Inf
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -446,7 +445,9 @@ __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int
         const int cb = (int)(r % ncb);
         const int a = plist[r / ncb];
         const int sh = gsh[a];
-        const double sc = sh == NOSLAB ? 0.0 : ldexp(1.0, sh);
+        // 2^sh in two factors: slabs below ~1e-290 need sh > 1023
+        const int sh1 = min(sh, 960);
+        const double sc = sh == NOSLAB ? 0.0 : ldexp(1.0, sh1), sc2 = sh == NOSLAB ? 0.0 : ldexp(1.0, sh - sh1);
         const double2 *row = g + ((size_t)a * wp.N1p + b) * wp.N2p;
         uint32_t w[ND][2] = {};
 #pragma unroll
@@ -456,7 +457,7 @@ __global__ void k_slice_grid(const double2 *__restrict__ g, WindowParams wp, int
             if (c < wp.N2p) v = row[c];
 #pragma unroll
             for (int ri = 0; ri < 2; ++ri) {
-                const double y = fma(ri ? v.y : v.x, sc, MAGIC);
+                const double y = fma((ri ? v.y : v.x) * sc2, sc, MAGIC);
                 long long f = __double_as_longlong(y) - __double_as_longlong(MAGIC);   // rint(x 2^sG)
 #pragma unroll
                 for (int j = 0; j < ND; ++j) {

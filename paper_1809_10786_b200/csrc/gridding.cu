@@ -113,6 +113,30 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
 
+// SGL_FLAG_DETERMINISTIC (determ.cu): v rounded to the call's fixed-point
+// unit 2^-E and reduced as a 64-bit integer (order-independent).  2^E as two
+// factors (a, b) so that E beyond the FP64 exponent range of one factor (inputs
+// near 1e-300) scales exactly; a == 0: plain FP64 REDs.
+struct DScale {
+    double a, b;
+};
+
+__device__ __forceinline__ void red_add_det(double *addr, double v, DScale ds) {
+    if (ds.a != 0.0) {
+        const long long x = __double2ll_rn((v * ds.a) * ds.b);
+        if (x != 0) asm volatile("red.global.add.u64 [%0], %1;\n" ::"l"(addr), "l"(x) : "memory");
+    } else {
+        red_add(addr, v);
+    }
+}
+
+__device__ __forceinline__ DScale det_scale(const int *det) {
+    if (!det) return DScale{0.0, 0.0};
+    const int e = *det;
+    if (e == kDetOff) return DScale{0.0, 0.0};
+    return DScale{ldexp(1.0, e / 2), ldexp(1.0, e - e / 2)};
+}
+
 // ---------------------------------------------------------------------------
 // tiled gather
 //
@@ -369,7 +393,7 @@ struct ScatterSmem {
 template <int NCT, int G>
 __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double (*w0row)[WS], int mt0, int ks0, int ks1,
                                               int g0, const Tile &t, const WindowParams &wp, double *grid,
-                                              int lane) {
+                                              int lane, DScale dscale) {
     const int rb = lane >> 3, part = (lane >> 2) & 1, kk = lane & 3, cr = lane >> 2;
     double d[G][NCT][2];
 #pragma unroll
@@ -404,7 +428,7 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
                     SGL_DCHECK(c >= t.e2 || (g0 >= 0 && g0 < wp.N0 && t.o1 + b + wp.pad >= 0 &&
                                              t.o1 + b + wp.pad < wp.N1p && t.o2 + wp.pad + c >= 0 &&
                                              t.o2 + wp.pad + c < wp.N2p));
-                    if (c < t.e2) red_add(row + 2 * c + part, d[i][ct][j]);
+                    if (c < t.e2) red_add_det(row + 2 * c + part, d[i][ct][j], dscale);
                 }
             }
         }
@@ -415,8 +439,8 @@ __device__ __forceinline__ void scatter_group(const ScatterSmem &S, const double
 // last group of a short box) as template parameters: no DMMA on padding tiles
 __device__ __forceinline__ void scatter_group_any(int nct, int g, const ScatterSmem &S, const double (*w0row)[WS],
                                                   int mt0, int ks0, int ks1, int g0, const Tile &t,
-                                                  const WindowParams &wp, double *grid, int lane) {
-#define SGL_SG(NC, GG) scatter_group<NC, GG>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane)
+                                                  const WindowParams &wp, double *grid, int lane, DScale dscale) {
+#define SGL_SG(NC, GG) scatter_group<NC, GG>(S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane, dscale)
     switch (nct * 4 + g) {
     case 1 * 4 + 1: SGL_SG(1, 1); break;
     case 1 * 4 + 2: SGL_SG(1, 2); break;
@@ -439,8 +463,10 @@ __device__ __forceinline__ void scatter_group_any(int nct, int g, const ScatterS
 
 __global__ void __launch_bounds__(STH, 2)
     k_scatter_tiled(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp,
-                    const double2 *__restrict__ values, double *__restrict__ grid, const int *__restrict__ gate) {
+                    const double2 *__restrict__ values, double *__restrict__ grid, const int *__restrict__ gate,
+                    const int *__restrict__ det) {
     if (gate && *gate == 0) return;   // gated launch (fallback of the int8 scatter)
+    const DScale dscale = det_scale(det);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -529,7 +555,7 @@ __global__ void __launch_bounds__(STH, 2)
             const int ks0 = kfirst, ks1 = min(nks, klast + 1);
             const int g0 = wrapi(t.o0 + a, wp.N0);
             for (int mt0 = 0; mt0 < Mt; mt0 += SMT)
-                scatter_group_any(CT, min(SMT, Mt - mt0), S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane);
+                scatter_group_any(CT, min(SMT, Mt - mt0), S, w0row, mt0, ks0, ks1, g0, t, wp, grid, lane, dscale);
             __syncwarp();   // w0row is rewritten for the warp's next slab
         }
     }
@@ -585,8 +611,9 @@ __global__ void __launch_bounds__(NW_GEN * 32)
 
 __global__ void __launch_bounds__(NW_GEN * 32)
     k_scatter_generic(int64_t M, NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
-                      double *__restrict__ grid) {
+                      double *__restrict__ grid, const int *__restrict__ det) {
     extern __shared__ __align__(16) double gsm[];
+    const DScale dscale = det_scale(det);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P0 = 2 * wp.qa0 + 1, P1 = 2 * wp.qa1 + 1, P2 = 2 * wp.qa2 + 1;
     double *w0 = gsm + warp * (P0 + P1 + P2), *w1 = w0 + P0, *w2 = w1 + P1;
@@ -610,8 +637,8 @@ __global__ void __launch_bounds__(NW_GEN * 32)
             double *row = grid + 2 * (((size_t)g0 * wp.N1p + g1 + wp.pad) * wp.N2p + wp.pad);
             for (int c = lane; c < P2; c += 32) {
                 const int g2 = wrapi(l2 - wp.qa2 + c, wp.N2);
-                red_add(row + 2 * g2, w2[c] * tr);
-                red_add(row + 2 * g2 + 1, w2[c] * tim);
+                red_add_det(row + 2 * g2, w2[c] * tr, dscale);
+                red_add_det(row + 2 * g2 + 1, w2[c] * tim, dscale);
             }
         }
     }
@@ -811,7 +838,7 @@ int launch_scatter_tiled_gated(const Plan &p, const double2 *values, double2 *gr
     int64_t blocks = std::min<int64_t>(p.n_stiles, (int64_t)num_sms() * 2 * 8);
     if (blocks < 1) blocks = 1;
     k_scatter_tiled<<<(unsigned)blocks, STH, sm, st>>>(p.stiles, p.n_stiles, p.snodes, p.wp, values,
-                                                      reinterpret_cast<double *>(grid), gate);
+                                                      reinterpret_cast<double *>(grid), gate, p.det_e());
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;
 }
@@ -824,7 +851,7 @@ int launch_scatter(const Plan &p, const double2 *values, double2 *grid, cudaStre
         const size_t sm = (size_t)NW_GEN * (3 + 2 * (p.wp.qa0 + p.wp.qa1 + p.wp.qa2)) * sizeof(double);
         if (sm > 48 * 1024) SGL_CUDA_CHECK(cudaFuncSetAttribute(k_scatter_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_scatter_generic<<<(unsigned)((p.M + NW_GEN - 1) / NW_GEN), NW_GEN * 32, sm, st>>>(
-            p.M, p.nodes, p.wp, values, reinterpret_cast<double *>(grid));
+            p.M, p.nodes, p.wp, values, reinterpret_cast<double *>(grid), p.det_e());
     }
     SGL_CUDA_CHECK(cudaGetLastError());
     return SGL_OK;

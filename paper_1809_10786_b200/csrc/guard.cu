@@ -60,19 +60,33 @@ __global__ void k_absmax_c(const double2 *__restrict__ v, int64_t n, unsigned lo
     double m = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double2 x = v[i];
-        const double a = fmax(fabs(x.x), fabs(x.y));
-        m = (a != a) ? INFINITY : fmax(m, a);
+        m = fmax(m, cabsmax_naninf(x));   // NaN counts as +Inf
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-// sum |v|^2 (FP64 atomics, one per warp)
-__global__ void k_sumsq_c(const double2 *__restrict__ v, int64_t n, double *out) {
+// sum |v 2^-ev|^2 with max|v| < 2^ev (FP64 atomics, one per warp): scaled so
+// that neither tiny (1e-300) nor huge (1e300) values under- / overflow the sum
+// (r02 fix: the unscaled sum read 0 or Inf there, i.e. no check or a fallback
+// on every call)
+__device__ __forceinline__ int vmax_exp(unsigned long long bits) {
+    const double vm = __longlong_as_double((long long)bits);
+    int ev = 0;
+    if (vm > 0.0 && isfinite(vm)) frexp(vm, &ev);
+    return ev;
+}
+
+__global__ void k_sumsq_c(const double2 *__restrict__ v, int64_t n, const unsigned long long *__restrict__ vmax,
+                          double *out) {
+    const int ev = vmax_exp(*vmax);
+    const double f1 = ldexp(1.0, -(ev / 2)), f2 = ldexp(1.0, -(ev - ev / 2));
     double s = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 x = v[i];
+        double2 x = v[i];
+        x.x = (x.x * f1) * f2;
+        x.y = (x.y * f1) * f2;
         s = fma(x.x, x.x, fma(x.y, x.y, s));
     }
 #pragma unroll
@@ -102,11 +116,18 @@ __global__ void k_guard_fwd(GuardState *g, const unsigned long long *__restrict_
 // adjoint decision (one thread): rms of the values, max of the result
 __global__ void k_guard_adj(GuardState *g, const double *__restrict__ sumsq, double inv_m, double ak, int on) {
     const double cm = __longlong_as_double((long long)g->amax);
-    const double rms = sqrt(*sumsq * inv_m);
+    const double rms = sqrt(*sumsq * inv_m);   // in units of 2^ev (k_sumsq_c)
+    const int ev = vmax_exp(g->vmax);
     double est;
-    if (!isfinite(cm) || !isfinite(rms)) est = INFINITY;
-    else if (cm > 0.0) est = ak * rms / cm + (rms > 0.0 ? kGuardFloorA : 0.0);
-    else est = rms > 0.0 ? INFINITY : 0.0;
+    if (!isfinite(cm) || !isfinite(rms)) {
+        est = INFINITY;
+    } else if (cm > 0.0) {
+        int ec;
+        const double mc = frexp(cm, &ec);   // cm = mc 2^ec: the ratio without over- / underflow
+        est = ldexp(ak * rms / mc, ev - ec) + (rms > 0.0 ? kGuardFloorA : 0.0);
+    } else {
+        est = rms > 0.0 ? INFINITY : 0.0;
+    }
     g->est_adj = est;
     // (a non-finite input already ran on the FP64 scatter: nothing to redo)
     g->adj_redo = (on && est > kGuardBound && !g->adj) ? 1 : 0;
@@ -186,6 +207,12 @@ int launch_noise_grid(const Plan &p, double rms, cudaStream_t st) {
 }
 
 // host copy of max(|Re|, |Im|) over n device values (synchronises st)
+int launch_absmax(const double2 *v, int64_t n, unsigned long long *out, cudaStream_t st) {
+    k_absmax_c<<<256, 256, 0, st>>>(v, n, out);
+    SGL_CUDA_CHECK(cudaGetLastError());
+    return SGL_OK;
+}
+
 int read_absmax(const Plan &p, const double2 *v, int64_t n, cudaStream_t st, double *out) {
     SGL_CUDA_CHECK(cudaMemsetAsync(&p.guard->amax, 0, sizeof(unsigned long long), st));
     k_absmax_c<<<256, 256, 0, st>>>(v, n, &p.guard->amax);
@@ -217,7 +244,9 @@ int guard_adjoint_estimate(const Plan &p, const double2 *values, const double2 *
     double *ss = &g->vsumsq;
     SGL_CUDA_CHECK(cudaMemsetAsync(ss, 0, sizeof(double), st));
     SGL_CUDA_CHECK(cudaMemsetAsync(&g->amax, 0, sizeof(unsigned long long), st));
-    k_sumsq_c<<<num_sms() * 4, 256, 0, st>>>(values, p.M, ss);
+    SGL_CUDA_CHECK(cudaMemsetAsync(&g->vmax, 0, sizeof(unsigned long long), st));
+    k_absmax_c<<<256, 256, 0, st>>>(values, p.M, &g->vmax);
+    k_sumsq_c<<<num_sms() * 4, 256, 0, st>>>(values, p.M, &g->vmax, ss);
     SGL_CUDA_CHECK(cudaGetLastError());
     k_absmax_c<<<256, 256, 0, st>>>(coeffs, p.count, &g->amax);
     SGL_CUDA_CHECK(cudaGetLastError());

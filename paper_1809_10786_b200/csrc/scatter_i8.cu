@@ -92,6 +92,18 @@ __device__ __forceinline__ void red_add(double *addr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
 
+// SGL_FLAG_DETERMINISTIC: 64-bit fixed-point reduction (order-independent)
+__device__ __forceinline__ void red_add_s64(double *addr, long long v) {
+    asm volatile("red.global.add.u64 [%0], %1;\n" ::"l"(addr), "l"(v) : "memory");
+}
+
+// x 2^s rounded to an integer (s < 0: round half up by an arithmetic shift)
+__device__ __forceinline__ long long fix_shift(long long x, int s) {
+    if (s >= 0) return x << min(s, 62);
+    if (s < -62) return 0;
+    return (x + (1ll << (-s - 1))) >> (-s);
+}
+
 __device__ __forceinline__ void st_async_v4(void *dst, const uint32_t (&v)[4], uint64_t *bar) {
     asm volatile(
         "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
@@ -125,14 +137,21 @@ __global__ void k_vdigits(const Tile *__restrict__ tiles, const int *__restrict_
         const int64_t ti = ktile[gk];
         const Tile t = tiles[ti];
         const int svt = tsv[ti];
-        const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt);
+        // 2^svt as 2^min(svt, 960) on the digit split and the rest on the value
+        // first: values below ~1e-290 need svt > 1023 (r02 fix: the one-factor
+        // scale overflowed to Inf), and the pre-scaled value keeps w1 v normal
+        const int svt1 = min(svt, 960);
+        const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt1);
+        const double vsc2 = svt == NOSLAB ? 0.0 : ldexp(1.0, svt - svt1);
         const int ks = (int)(gk - voff[ti]);
         const int kn = ks * KST + kl;
         const bool live = kn < t.count;
         const int64_t si = (int64_t)t.start + kn;
         const double u1 = live ? nodes.u1[si] : -1e9;
         SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
-        const double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
+        double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
+        vv.x *= vsc2;
+        vv.y *= vsc2;
         int lo1, hi1;
         window_cells(u1, wp.q, lo1, hi1);
         const int bf = max(0, lo1 - t.o1);   // first window cell, relative to the box
@@ -169,12 +188,16 @@ __device__ __forceinline__ long long tick() {
     else return 0;
 }
 
-template <bool PROF>   // PROF: clock64 wait counters (SGL_FLAG_I8_PROF); compiled out otherwise
+// PROF: clock64 wait counters (SGL_FLAG_I8_PROF); compiled out otherwise.
+// DET: SGL_FLAG_DETERMINISTIC -- the exact per-tile int64 sums are shifted to
+// the call's fixed-point unit 2^-E (*det) and reduced as integers (determ.cu)
+template <bool PROF, bool DET>
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
                  double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
                  const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2,
-                 unsigned long long *__restrict__ prof, const int *__restrict__ skip) {
+                 unsigned long long *__restrict__ prof, const int *__restrict__ skip,
+                 const int *__restrict__ det) {
     if (*skip) return;   // non-finite values (guard.cu)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SSmem &S = *reinterpret_cast<SSmem *>(smem_raw);
@@ -418,6 +441,9 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             const int nmb = mblocks(t);
             const int sv = __ldg(tsv + ti);
             const double unit = sv == NOSLAB ? 0.0 : ldexp(1.0, 8 * DMIN - sA - sv);
+            // DET: this tile's shift to the call's unit (E == kDetOff cannot reach
+            // here: non-finite values skip the kernel)
+            const int dsh = DET ? 8 * DMIN - sA - sv + *det : 0;
             const int kst = kstart2(t, wp);   // padded axis-2 cell of K column 0
             const int c_in0 = t.o2 + wp.pad - kst, c_in1 = c_in0 + t.e2;
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
@@ -457,12 +483,21 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
                 if (inbox) {
                     for (int b = eh * (ROWS / 2 / EPW); b < min(t.e1, (eh + 1) * (ROWS / 2 / EPW)); ++b) {
-                        const double re = (double)S.stage[2 * b][m] * unit, im = (double)S.stage[2 * b + 1][m] * unit;
                         double *q = gp + 2 * (size_t)b * wp.N2p;
                         SGL_DCHECK(wrap1(t.o0 + al, wp.N0) < wp.N0 && t.o1 + wp.pad + b < wp.N1p &&
                                    kst + cl >= 0 && kst + cl < wp.N2p);
-                        if (re != 0.0) red_add(q, re);
-                        if (im != 0.0) red_add(q + 1, im);
+                        if (DET) {
+                            if (sv == NOSLAB) continue;
+                            const long long xr = fix_shift(S.stage[2 * b][m], dsh);
+                            const long long xi = fix_shift(S.stage[2 * b + 1][m], dsh);
+                            if (xr != 0) red_add_s64(q, xr);
+                            if (xi != 0) red_add_s64(q + 1, xi);
+                        } else {
+                            const double re = (double)S.stage[2 * b][m] * unit;
+                            const double im = (double)S.stage[2 * b + 1][m] * unit;
+                            if (re != 0.0) red_add(q, re);
+                            if (im != 0.0) red_add(q + 1, im);
+                        }
                     }
                 }
             }
@@ -501,8 +536,7 @@ __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet
     double m = 0.0;
     for (int i = threadIdx.x; i < t.count; i += blockDim.x) {
         const double2 v = values[nodes.perm[(int64_t)t.start + i]];
-        const double a = fmax(fabs(v.x), fabs(v.y));
-        m = (a != a) ? INFINITY : fmax(m, a);   // NaN counts as +Inf
+        m = fmax(m, cabsmax_naninf(v));   // NaN counts as +Inf
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -596,14 +630,16 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     const size_t sm = sizeof(SSmem);
     unsigned long long *prof = p.prof;   // SGL_FLAG_I8_PROF: per-plan counters on the plan's device
     const bool want = prof != nullptr;
-    auto kern = want ? k_scatter_i8<true> : k_scatter_i8<false>;
+    const int *det = p.det_e();
+    auto kern = want ? (det ? k_scatter_i8<true, true> : k_scatter_i8<true, false>)
+                     : (det ? k_scatter_i8<false, true> : k_scatter_i8<false, false>);
     SGL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
     kern<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
-                                                  reinterpret_cast<double *>(grid), g2, prof, skip);
+                                                  reinterpret_cast<double *>(grid), g2, prof, skip, det);
     SGL_CUDA_CHECK(cudaGetLastError());
     if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)
         std::vector<unsigned long long> h(8 * blocks);

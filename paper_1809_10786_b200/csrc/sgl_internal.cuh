@@ -80,6 +80,23 @@ __host__ __device__ inline void window_cells(double u, int q, int &c_lo, int &c_
     c_hi = lo + q;
 }
 
+// max(|Re|, |Im|) with a NaN in either part as +Inf: fmax alone returns the
+// other operand (r02 fix: NaN + 0i values were seen as 0 by the int8 engines'
+// non-finite checks)
+__device__ __forceinline__ double cabsmax_naninf(double2 v) {
+    const double a = fmax(fabs(v.x), fabs(v.y));
+    return (v.x != v.x || v.y != v.y) ? INFINITY : a;
+}
+
+// SGL_FLAG_DETERMINISTIC (determ.cu): per-call fixed-point exponent E of the
+// spread (grid unit 2^-E; kDetOff = FP64 REDs for non-finite input) and the
+// max |v| it is derived from
+constexpr int kDetOff = -(1 << 20);
+struct DetState {
+    int e, pad_;
+    unsigned long long vmax;
+};
+
 struct StageTimer {
     cudaEvent_t ev[SGL_STAGE_COUNT + 1];
     bool ready = false;
@@ -94,7 +111,8 @@ struct GuardState {
     int adj_redo, pad_;                 // adjoint estimate above the bound: rerun on the FP64 scatter
     unsigned long long fwd_count, adj_count;   // calls that fell back (diagnostics)
     unsigned long long outmax;          // bits of max |Re|, |Im| of the int8 gather output
-    double vsumsq;                      // sum |v|^2 of the adjoint input
+    double vsumsq;                      // sum |v 2^-ev|^2 of the adjoint input (max|v| < 2^ev)
+    unsigned long long vmax;            // bits of max |Re|, |Im| of the adjoint input
     unsigned long long amax;            // bits of max |Re|, |Im| of the adjoint output
     double est_fwd, est_adj;            // last estimates (relative to the output's max)
 };
@@ -210,6 +228,11 @@ struct Plan {
                                    // (2^-46 |v|)^2: (c0 c1 c2)^2 (2q+1)^3 (uniform per-tap error)
     double guard_ap = 0.0;         // adjoint tail's response to the spread noise model (plan time)
     unsigned long long *prof = nullptr;   // SGL_FLAG_I8_PROF: clock64 counters (device, per plan)
+    // SGL_FLAG_DETERMINISTIC (determ.cu): fixed-point spread state (device) and
+    // the window density max_cell sum_n w_n(cell) measured at plan time
+    DetState *det = nullptr;
+    double det_density = 0.0;
+    const int *det_e() const { return det ? &det->e : nullptr; }
     double lap_ms = -1.0;          // SGL_FLAG_I8_PROF: plan-construction stage clock (plan_lap)
 
     // single-process multi-GPU plan (multi.cu): one sub-plan per device over a
@@ -325,5 +348,15 @@ int launch_scatter_tiled_gated(const Plan &p, const double2 *values, double2 *gr
                                cudaStream_t st);
 int setup_i8(Plan &p);
 int num_sms();
+// max(|Re|, |Im|) bits into *out (atomicMax; *out zeroed by the caller; NaN counts as +Inf)
+int launch_absmax(const double2 *v, int64_t n, unsigned long long *out, cudaStream_t st);
+// SGL_FLAG_DETERMINISTIC (determ.cu)
+int setup_det(Plan &p, cudaStream_t st);
+int det_begin(const Plan &p, const double2 *v, cudaStream_t st);
+int det_finish(const Plan &p, double2 *grid, cudaStream_t st);
+// the adjoint's window stage into the zeroed p.grid_buf (int8 scatter with its
+// guard when allow_i8 and live, else the FP64 / per-node scatter), in fixed
+// point under SGL_FLAG_DETERMINISTIC
+int spread_stage(Plan &p, const double2 *v, cudaStream_t st, bool allow_i8);
 
 }  // namespace sgl

@@ -149,7 +149,8 @@ def _stream_ptr(x) -> int | None:
 def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None = None,
          exact_last_stage: bool = False, compact_k1: bool = False, backend: str = "auto",
          precompute: bool = True, device: int | None = None, profile: bool = False,
-         precise_tables: bool | None = None, flags: int = 0, devices=None) -> SglPlan:
+         precise_tables: bool | None = None, flags: int = 0, devices=None,
+         deterministic: bool = False) -> SglPlan:
     """Prepare a fast-transform plan for one scattered point set (transform.py:320-382).
 
     ``backend``: "auto" (q <= 16: the int8 tensor-core gather for the
@@ -167,7 +168,12 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
     evaluation by the direct NDFT on the device (O(M n^3): verification).
     ``devices``: a list of CUDA device ids -- one plan over all of them in
     this process (node shards, one sub-plan per device, sgl_plan_create_multi);
-    the one-process-per-GPU path is `distributed.ShardedPlan`."""
+    the one-process-per-GPU path is `distributed.ShardedPlan`.
+    ``deterministic=True``: bitwise reproducible adjoints (the reference's
+    serial spreading loop, _gridding.py:77-95, is): every window kernel reduces
+    64-bit fixed-point integers into the grid instead of FP64 atomics
+    (SGL_FLAG_DETERMINISTIC, csrc/determ.cu); costs one plan-time spread and a
+    grid conversion per adjoint."""
     if B < 1:
         raise ValueError("bandwidth must be >= 1")
     if backend not in _BACKENDS:
@@ -214,6 +220,8 @@ def plan(B: int, points, sigma: int = 2, q: int | None = 16, rho: float | None =
         flags |= _native.FLAG_FP64_WINDOW
     if profile:
         flags |= _native.FLAG_PROFILE
+    if deterministic:
+        flags |= _native.FLAG_DETERMINISTIC
     # basal matrices in x87 extended precision by default (closer to the
     # truth on ill-conditioned configurations; SGL_FLAG_FP64_TABLES opts out)
     if precise_tables is None:

@@ -151,3 +151,46 @@ def test_guard_off_flag(sgl):
     f = sgl.forward(p, c)
     assert rel(f, sgl.forward(sgl.plan(8, pts, backend="tiled"), c)) <= 1e-11
     assert p.guard["fwd_fallbacks"] == 0 and p.guard["est_fwd"] > 0.0   # estimated, never acted on
+
+
+@pytest.mark.parametrize("scale", [2.0 ** -996, 2.0 ** -830, 2.0 ** 830, 2.0 ** 996])
+def test_int8_engines_over_the_fp64_range(sgl, scale):
+    # r02 fix: the digit scales 2^s of tiles / slabs below ~1e-290 need s > 1023
+    # (applied as two factors now; one factor overflowed to Inf and the int8
+    # scatter returned garbage at 1e-300), and the adjoint estimate's sum of
+    # |v|^2 is taken in units of max|v| (it read 0 at 1e-300, i.e. no check, and
+    # Inf at 1e300, i.e. a fallback on every call).  Raw engines (guard off) and
+    # scale-free estimates; power-of-two scales reproduce the unit-scale result.
+    from paper_1809_10786_b200 import _native
+    rng = np.random.default_rng(5)
+    pts = sgl.gen_points_ball(20000, 4.0, rng)
+    v = rng.uniform(-1, 1, 20000) + 1j * rng.uniform(-1, 1, 20000)
+    c = sgl.gen_coeffs(16, rng)
+    p8 = sgl.plan(16, pts, backend="i8", flags=_native.FLAG_NO_GUARD)
+    p64 = sgl.plan(16, pts, backend="tiled")
+    a1, f1 = sgl.adjoint(p8, v), sgl.forward(p8, c)
+    g1 = p8.guard
+    a8, a64 = sgl.adjoint(p8, v * scale), sgl.adjoint(p64, v * scale)
+    assert np.all(np.isfinite(a8)) and rel(a8, a64) <= TOL, rel(a8, a64)
+    f8, f64 = sgl.forward(p8, c * scale), sgl.forward(p64, c * scale)
+    assert np.all(np.isfinite(f8)) and rel(f8, f64) <= TOL, rel(f8, f64)
+    g = p8.guard
+    assert g["est_adj"] == pytest.approx(g1["est_adj"], rel=1e-6), (g, g1)
+    assert g["est_fwd"] == pytest.approx(g1["est_fwd"], rel=1e-3), (g, g1)
+    assert rel(a8 / scale, a1) <= 1e-14 and rel(f8 / scale, f1) <= 1e-14
+
+
+@pytest.mark.parametrize("bad", [np.nan + 0j, 1j * np.nan, np.inf + 0j])
+def test_nonfinite_in_one_part_without_guard(sgl, bad):
+    # the non-finite check of the int8 scatter runs even with the guard off (and
+    # inside CUDA-graph captures, where the adjoint estimate is skipped): a NaN
+    # in one part of a value must reach the output as it does on FP64
+    from paper_1809_10786_b200 import _native
+    rng = np.random.default_rng(3)
+    pts = sgl.gen_points_ball(4000, 4.0, rng)
+    v = rng.uniform(-1, 1, 4000) + 1j * rng.uniform(-1, 1, 4000)
+    v[321] = bad
+    p8 = sgl.plan(16, pts, backend="i8", flags=_native.FLAG_NO_GUARD)
+    a8, a64 = sgl.adjoint(p8, v), sgl.adjoint(sgl.plan(16, pts, backend="tiled"), v)
+    assert not np.all(np.isfinite(a64))
+    assert _same_nonfinite(a8, a64)
