@@ -77,7 +77,7 @@ void free_plan(Plan *p) {
                     p->snodes.perm, p->tiles, p->stiles, p->Kl, p->Km,
                     p->Kl_off_d, p->Km_off_d, p->dec0, p->dec1, p->dec2, p->grid_buf, p->beta,
                     p->coef_buf, p->val_buf, p->zeta, p->inodes.u0, p->inodes.u1, p->inodes.u2, p->inodes.perm,
-                    p->itiles, p->digits, p->gmax, p->gplist, p->istiles, p->tsv, p->svoff, p->sktile, p->vdig, p->guard, p->prof, p->det};
+                    p->itiles, p->digits, p->gmax, p->gplist, p->istiles, p->tsv, p->vdig, p->guard, p->prof, p->det};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (p->fft_ready) cufftDestroy(p->fft);

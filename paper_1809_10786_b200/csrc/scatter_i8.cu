@@ -13,11 +13,11 @@
 // MMAs per K-step of 32 nodes (W digit p times V digits stacked along N),
 // int32 diagonal accumulators in TMEM (6 x 80 columns).
 //
-// V does not depend on the M-block: its digits are built once per adjoint by
-// k_vdigits into global memory, already in the MN-major UMMA layout of a
-// K-step (15 KB per 32 nodes), and a producer warp streams them into shared
-// memory with 1-D bulk copies (cp.async.bulk, L2-resident across the tile's
-// M-blocks).  Only W is built on the fly, by 16 generator warps (node x
+// V does not depend on the M-block: two value-digit warps build a tile's
+// digits once, one tile ahead, into the CTA's slot of a small ring in global
+// memory (2 x 240 KB per CTA, L2-resident), already in the MN-major UMMA
+// layout of a K-step (15 KB per 32 nodes), and a producer warp streams them
+// into shared memory with 1-D bulk copies (cp.async.bulk) per M-block.  Only W is built on the fly, by 16 generator warps (node x
 // 16-cell group, weights from per-node factors in shared memory), stored with
 // st.async.  The epilogue converts an M-block to FP64 into a per-thread
 // staging column, frees TMEM for the next block's MMAs and only then reduces
@@ -28,7 +28,7 @@
 // CTA (one per SM, persistent, cluster of 1 for st.async): warp 0 MMA
 // issuer, warp 1 value-digit producer, warps 2-17 weight-digit generators (two
 // groups of 8 on alternating K-steps), warps 18-25 epilogue (two per TMEM lane
-// quarter = cells, half the columns each).
+// quarter = cells, half the columns each), warps 26-27 value-digit generators.
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -65,7 +65,10 @@ constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (
 constexpr int NWG = 8 * NGRP;            // weight generator warps (per group: 32 nodes x 8 cell groups)
 constexpr int NEW = 8;                   // epilogue warps: EPW per TMEM lane quarter, 1/EPW of the columns each
 constexpr int EPW = NEW / 4;
-constexpr int ST = (2 + NWG + NEW) * 32;
+constexpr int NVW = 2;                   // value-digit generator warps (warp = K-step, lane = node)
+constexpr int VSLOTS = 2;                // value-digit slots per CTA in global memory (tile parity)
+constexpr int V_SLOT = (SN / KST) * B_STAGE;   // one tile's value digits (16 K-steps, 240 KB)
+constexpr int ST = (2 + NWG + NEW + NVW) * 32;
 
 struct SSmem {
     uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
@@ -78,6 +81,7 @@ struct SSmem {
     int win0[SN];                // axis-0 window in tile slabs: lo | hi << 16 (signed)
     uint64_t fullA[NSTG], emptyA[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
+    uint64_t vready[VSLOTS], vfree[VSLOTS];   // a tile's value digits written / all its MMAs done
     uint32_t tbase;
 };
 
@@ -122,63 +126,52 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 __device__ __forceinline__ int mblocks(const Tile &t) { return (t.e0 * CHUNKS * 16 + MR - 1) / MR; }
 __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1) / KST; }
 
-// value digits of every K-step of every tile (once per adjoint): thread = node
-// of the K-step, walking all 40 axis-1 cells (the Gaussian recurrence runs on
-// across the 5 16-column groups: one exp pair per node; 1.07 ms at config 3
-// against 1.2 ms with a thread per column group); warp = K-step, 4 K-steps
-// per block
-__global__ void k_vdigits(const Tile *__restrict__ tiles, const int *__restrict__ ktile, int64_t nksteps,
-                               NodeSet nodes, WindowParams wp, const double2 *__restrict__ values,
-                               const int *__restrict__ tsv, const int64_t *__restrict__ voff,
-                               uint8_t *__restrict__ vdig, const int *__restrict__ skip) {
-    if (*skip) return;   // non-finite values: the gated FP64 scatter runs instead (guard.cu)
-    const int kl = threadIdx.x & 31, wk = threadIdx.x >> 5;
-    for (int64_t gk = (int64_t)blockIdx.x * 4 + wk; gk < nksteps; gk += (int64_t)gridDim.x * 4) {
-        const int64_t ti = ktile[gk];
-        const Tile t = tiles[ti];
-        const int svt = tsv[ti];
-        // 2^svt as 2^min(svt, 960) on the digit split and the rest on the value
-        // first: values below ~1e-290 need svt > 1023 (r02 fix: the one-factor
-        // scale overflowed to Inf), and the pre-scaled value keeps w1 v normal
-        const int svt1 = min(svt, 960);
-        const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt1);
-        const double vsc2 = svt == NOSLAB ? 0.0 : ldexp(1.0, svt - svt1);
-        const int ks = (int)(gk - voff[ti]);
-        const int kn = ks * KST + kl;
-        const bool live = kn < t.count;
-        const int64_t si = (int64_t)t.start + kn;
-        const double u1 = live ? nodes.u1[si] : -1e9;
-        SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
-        double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
-        vv.x *= vsc2;
-        vv.y *= vsc2;
-        int lo1, hi1;
-        window_cells(u1, wp.q, lo1, hi1);
-        const int bf = max(0, lo1 - t.o1);   // first window cell, relative to the box
-        const double d = u1 - (double)(t.o1 + bf);
-        double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
-        uint8_t *dst = vdig + (voff[ti] + ks) * (int64_t)B_STAGE + (kl >> 3) * B_KBLK + (kl & 7) * 16;
+// value digits of one K-step of a tile: lane = node of the K-step, walking all
+// 40 axis-1 cells (the Gaussian recurrence runs on across the 5 16-column
+// groups: one exp pair per node), written in the K-step's MN-major UMMA layout
+__device__ __forceinline__ void vdigits_kstep(const Tile &t, int svt, int ks, int kl, const NodeSet &nodes,
+                                              const WindowParams &wp, const double2 *__restrict__ values,
+                                              uint8_t *__restrict__ blk) {
+    // 2^svt as 2^min(svt, 960) on the digit split and the rest on the value
+    // first: values below ~1e-290 need svt > 1023 (r02 fix: the one-factor
+    // scale overflowed to Inf), and the pre-scaled value keeps w1 v normal
+    const int svt1 = min(svt, 960);
+    const double vsc = svt == NOSLAB ? 0.0 : ldexp(1.0, svt1);
+    const double vsc2 = svt == NOSLAB ? 0.0 : ldexp(1.0, svt - svt1);
+    const int kn = ks * KST + kl;
+    const bool live = kn < t.count;
+    const int64_t si = (int64_t)t.start + kn;
+    const double u1 = live ? nodes.u1[si] : -1e9;
+    SGL_DCHECK(!live || (si < nodes.n && nodes.perm[si] >= 0 && nodes.perm[si] < nodes.n));
+    double2 vv = live ? values[nodes.perm[si]] : make_double2(0.0, 0.0);
+    vv.x *= vsc2;
+    vv.y *= vsc2;
+    int lo1, hi1;
+    window_cells(u1, wp.q, lo1, hi1);
+    const int bf = max(0, lo1 - t.o1);   // first window cell, relative to the box
+    const double d = u1 - (double)(t.o1 + bf);
+    double w = wp.c1 * exp(-d * d * wp.h1), r = exp(wp.h1 * (2.0 * d - 1.0));
+    uint8_t *dst = blk + (kl >> 3) * B_KBLK + (kl & 7) * 16;
 #pragma unroll 1
-        for (int vg = 0; vg < ROWS / 16; ++vg) {
-            double wv[16];
+    for (int vg = 0; vg < ROWS / 16; ++vg) {
+        double wv[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int b = vg * 8 + j;
-                const double w1 = (live && b >= bf && t.o1 + b <= hi1) ? w : 0.0;
-                if (b >= bf) {
-                    w *= r;
-                    r *= wp.r1_1;
-                }
-                wv[2 * j] = w1 * vv.x;
-                wv[2 * j + 1] = w1 * vv.y;
+        for (int j = 0; j < 8; ++j) {
+            const int b = vg * 8 + j;
+            const double w1 = (live && b >= bf && t.o1 + b <= hi1) ? w : 0.0;
+            if (b >= bf) {
+                w *= r;
+                r *= wp.r1_1;
             }
-            uint32_t dw[ND][4];
-            digits16(vsc, wv, dw);
-#pragma unroll
-            for (int q = 0; q < ND; ++q)
-                *reinterpret_cast<uint4 *>(dst + vg * 128 + q * (ROWS / 16) * 128) =
-                    make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
+            wv[2 * j] = w1 * vv.x;
+            wv[2 * j + 1] = w1 * vv.y;
         }
+        uint32_t dw[ND][4];
+        digits16(vsc, wv, dw);
+#pragma unroll
+        for (int q = 0; q < ND; ++q)
+            *reinterpret_cast<uint4 *>(dst + vg * 128 + q * (ROWS / 16) * 128) =
+                make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
     }
 }
 
@@ -194,8 +187,8 @@ __device__ __forceinline__ long long tick() {
 template <bool PROF, bool DET>
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
-                 double s2, int sA, const int *__restrict__ tsv, const int64_t *__restrict__ voff,
-                 const uint8_t *__restrict__ vdig, double *__restrict__ grid, const G16 g2,
+                 double s2, int sA, const int *__restrict__ tsv, const double2 *__restrict__ values,
+                 uint8_t *__restrict__ vring, double *__restrict__ grid, const G16 g2,
                  unsigned long long *__restrict__ prof, const int *__restrict__ skip,
                  const int *__restrict__ det) {
     if (*skip) return;   // non-finite values (guard.cu)
@@ -214,6 +207,10 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         }
         mbar_init(&S.tfull, 1);
         mbar_init(&S.tempty, NEW);
+        for (int s = 0; s < VSLOTS; ++s) {
+            mbar_init(&S.vready[s], NVW * 32);
+            mbar_init(&S.vfree[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 0) umma::tmem_alloc(&S.tbase, TCOLS);
@@ -231,7 +228,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         int stgb = 0;            // value ring slot and phase, stepped (NSTGB is not a power of 2)
         uint32_t phb = 0;
         long long q0 = tick<PROF>(), qa = 0, qb = 0, qe = 0;
-        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        uint32_t tj = 0;         // this CTA's tile counter (value-digit slot = tj % VSLOTS)
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tj) {
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
@@ -279,6 +277,10 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 if (umma::elect_one()) umma::commit(&S.tfull);
                 __syncwarp();
             }
+            // every bulk copy of the tile's value digits has landed and been read:
+            // its slot may be overwritten (by the tile after next)
+            if (umma::elect_one()) umma::commit(&S.vfree[tj % VSLOTS]);
+            __syncwarp();
         }
         if (PROF && prof && lane == 0) {
             prof[blockIdx.x * 8 + 0] = tick<PROF>() - q0;
@@ -292,10 +294,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             uint32_t g = 0;
             int pstg = 0;        // ring slot and the phase of its current use
             uint32_t pph = 0;
-            for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+            uint32_t tj = 0;
+            for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tj) {
                 const Tile t = tiles[ti];
                 const int nmb = mblocks(t), nks = ksteps(t);
-                const uint8_t *src = vdig + voff[ti] * (int64_t)B_STAGE;
+                const int slot = (int)(tj % VSLOTS);
+                const uint8_t *src = vring + ((size_t)blockIdx.x * VSLOTS + slot) * V_SLOT;
+                mbar_wait(&S.vready[slot], (tj / VSLOTS) & 1);   // written + fenced by the value warps
                 for (int mb = 0; mb < nmb; ++mb)
                     for (int ks = 0; ks < nks; ++ks, ++g) {
                         if (g >= (uint32_t)NSTGB) mbar_wait(&S.emptyB[pstg], pph ^ 1);   // its previous use
@@ -431,6 +436,26 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             prof[blockIdx.x * 8 + 6] = qt;
             prof[blockIdx.x * 8 + 7] = qw;
         }
+    } else if (warp >= 2 + NWG + NEW) {
+        // ---- value-digit generators: V = w1 v does not depend on the M-block, so a
+        // tile's digits are written once, one tile ahead, into this CTA's slot of
+        // an L2-resident ring in global memory (2 x 240 KB per CTA) and re-read
+        // from there per M-block by the producer's bulk copies.  Generic-proxy
+        // writes -> async-proxy reads: fence.proxy.async by every writer before
+        // its arrive on vready.
+        const int vw = warp - (2 + NWG + NEW);
+        uint32_t tj = 0;
+        for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tj) {
+            const Tile t = tiles[ti];
+            const int slot = (int)(tj % VSLOTS);
+            if (tj >= (uint32_t)VSLOTS) mbar_wait(&S.vfree[slot], (tj / VSLOTS - 1) & 1);
+            const int svt = __ldg(tsv + ti);
+            uint8_t *dst = vring + ((size_t)blockIdx.x * VSLOTS + slot) * V_SLOT;
+            for (int ks = vw; ks < ksteps(t); ks += NVW)
+                vdigits_kstep(t, svt, ks, lane, nodes, wp, values, dst + (size_t)ks * B_STAGE);
+            asm volatile("fence.proxy.async;\n" ::: "memory");
+            mbar_arrive(&S.vready[slot]);
+        }
     } else {
         // ---- epilogue: thread = box cell of the M-block = TMEM lane
         const int quarter = warp & 3, m = quarter * 32 + lane, eh = (warp - 2 - NWG) >> 2;
@@ -513,19 +538,6 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     }
 }
 
-// tile index of every K-step (the inverse of voff)
-__global__ void k_ktile(const int64_t *__restrict__ voff, int64_t ntiles, int *__restrict__ ktile) {
-    const int64_t ti = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (ti >= ntiles) return;
-    for (int64_t k = voff[ti]; k < voff[ti + 1]; ++k) ktile[k] = (int)ti;
-}
-
-// K-steps of 32 nodes per tile (0 past the end: the scan's last entry is the total)
-__global__ void k_tile_ksteps(const Tile *__restrict__ tiles, int64_t n, int64_t *ks) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i <= n) ks[i] = i < n ? (tiles[i].count + KST - 1) / KST : 0;
-}
-
 // per tile: value scale from the tile's max |Re v|, |Im v| (|w1 v| 2^sV < 2^46, w1 <= c1)
 __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet nodes,
                               const double2 *__restrict__ values, double c1, int *__restrict__ tsv,
@@ -557,7 +569,6 @@ __global__ void k_tile_vscale(const Tile *__restrict__ tiles, int64_t n, NodeSet
 
 int setup_scatter_i8(Plan &p) {
     const WindowParams &w = p.wp;
-    int64_t total_ks = 0;   // K-steps of all tiles (one 15 KB value-digit block each)
     if (p.n_istiles > 0) {
         TileStats ts;
         const int rc = tile_stats(p.istiles, p.n_istiles, 2, w, nullptr, &ts);
@@ -567,50 +578,23 @@ int setup_scatter_i8(Plan &p) {
             return SGL_ECUDA;
         }
         p.i8_sksteps = ts.work;
-        total_ks = (ts.nodes + KST - 1) / KST + p.n_istiles;   // upper bound of sum ceil(count / 32)
     }
-    // the digit buffer must leave room for the calls' own staging (val_buf2, cuFFT work):
-    // keep 2 GB free, else stay on the FP64 scatter (which needs none)
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    const size_t need = (size_t)std::max<int64_t>(1, total_ks) * B_STAGE;
-    if (need + (size_t(2) << 30) > fr || cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
-        cudaMalloc(&p.svoff, sizeof(int64_t) * (p.n_istiles + 1)) != cudaSuccess ||
+    // value-digit ring: VSLOTS tiles of digits per CTA (73 MB at 148 CTAs, L2-resident),
+    // independent of the node count; on an allocation failure stay on the FP64 scatter
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, num_sms()));
+    const size_t need = (size_t)blocks * VSLOTS * V_SLOT;
+    if (cudaMalloc(&p.tsv, sizeof(int) * (p.n_istiles + 1)) != cudaSuccess ||
         cudaMalloc(&p.vdig, need) != cudaSuccess) {
         cudaGetLastError();
-        for (void *b : {(void *)p.tsv, (void *)p.svoff, (void *)p.vdig, (void *)p.istiles})
+        for (void *b : {(void *)p.tsv, (void *)p.vdig, (void *)p.istiles})
             if (b) cudaFree(b);
         p.tsv = nullptr;
-        p.svoff = nullptr;
         p.vdig = nullptr;
         p.istiles = nullptr;
         p.n_istiles = 0;
         p.i8_sksteps = 0;
         p.i8s = false;   // FP64 scatter (as setup_i8 does for the gather)
         return SGL_OK;
-    }
-    // first value-digit block of every tile: exclusive scan of ceil(count / 32)
-    if (p.n_istiles > 0) {
-        int64_t *ks = nullptr;
-        void *tmp = nullptr;
-        size_t tb = 0;
-        SGL_CUDA_CHECK(cudaMalloc(&ks, sizeof(int64_t) * (p.n_istiles + 1)));
-        k_tile_ksteps<<<(unsigned)((p.n_istiles + 256) / 256), 256>>>(p.istiles, p.n_istiles, ks);
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, ks, p.svoff, (int)(p.n_istiles + 1));
-        SGL_CUDA_CHECK(cudaMalloc(&tmp, tb));
-        cub::DeviceScan::ExclusiveSum(tmp, tb, ks, p.svoff, (int)(p.n_istiles + 1));
-        SGL_CUDA_CHECK(cudaGetLastError());
-        SGL_CUDA_CHECK(cudaMemcpy(&p.n_sksteps, p.svoff + p.n_istiles, sizeof(int64_t), cudaMemcpyDeviceToHost));
-        cudaFree(tmp);
-        cudaFree(ks);
-        if (cudaMalloc(&p.sktile, sizeof(int) * std::max<int64_t>(1, p.n_sksteps)) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("out of device memory for the int8 scatter K-step map");
-            return SGL_ENOMEM;
-        }
-        k_ktile<<<(unsigned)((p.n_istiles + 255) / 256), 256>>>(p.svoff, p.n_istiles, p.sktile);
-        SGL_CUDA_CHECK(cudaGetLastError());
-        SGL_CUDA_CHECK(cudaDeviceSynchronize());
     }
     return SGL_OK;
 }
@@ -622,9 +606,6 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
                                                          skip);
     SGL_CUDA_CHECK(cudaGetLastError());
     const int sms = num_sms();
-    k_vdigits<<<(unsigned)std::min<int64_t>((p.n_sksteps + 3) / 4, (int64_t)sms * 32), 128, 0, st>>>(
-        p.istiles, p.sktile, p.n_sksteps, p.inodes, p.wp, values, p.tsv, p.svoff, p.vdig, skip);
-    SGL_CUDA_CHECK(cudaGetLastError());
     const int e = (int)std::ceil(std::log2(p.wp.c0 * p.wp.c2));
     const int sA = 46 - e, a0 = sA / 2;
     const size_t sm = sizeof(SSmem);
@@ -638,7 +619,7 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
     kern<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
-                                                  std::ldexp(1.0, sA - a0), sA, p.tsv, p.svoff, p.vdig,
+                                                  std::ldexp(1.0, sA - a0), sA, p.tsv, values, p.vdig,
                                                   reinterpret_cast<double *>(grid), g2, prof, skip, det);
     SGL_CUDA_CHECK(cudaGetLastError());
     if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)

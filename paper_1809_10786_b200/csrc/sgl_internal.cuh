@@ -198,10 +198,7 @@ struct Plan {
     int64_t n_istiles = 0;
     int *tsv = nullptr;            // per scatter tile: value fixed-point shift
     int64_t i8_sksteps = 0;        // int8 scatter K-steps per pass
-    int64_t *svoff = nullptr;      // per scatter tile: first value-digit block (K-step)
-    int *sktile = nullptr;         // per value-digit block (K-step): its tile
-    int64_t n_sksteps = 0;         // value-digit blocks of all tiles
-    uint8_t *vdig = nullptr;       // value digits, 15 KB per K-step of every tile
+    uint8_t *vdig = nullptr;       // value-digit ring of the int8 scatter: 2 tiles (2 x 240 KB) per CTA
     uint8_t *digits = nullptr;     // N0 x P2 x 6 x N1p x 2 x 16 signed bytes
     int P2 = 0;                    // 16-cell column blocks of a padded row
     uint64_t *gmax = nullptr;      // device scratch: bits of max |Re G|, |Im G|
