@@ -574,12 +574,12 @@ def main():
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "cpu_port": cpu_port,
             "clocks": clk,
             "gpu_launches": args.steps * ((11 if i8 else 4) * K * (direction != "adj") +
-                                         (11 if stats.get("i8_scatter") else 5) * (direction != "fwd")),
+                                         (10 if stats.get("i8_scatter") else 5) * (direction != "fwd")),
             "gpu_launches_note": ("per forward vector: radial_fwd, sph_fwd, halo_fill, slab_absmax, slab_shift, "
                                   "slice_grid, tile_shift, gather_i8, absmax_c, guard_fwd, gather_tiled (gated: "
                                   "returns at once unless the guard raised its flag)" if i8 else
                                   "per forward vector: radial_fwd, sph_fwd, halo_fill, gather_tiled") +
-                                 ("; per adjoint: tile_vscale, vdigits, scatter_i8, scatter_tiled (gated), "
+                                 ("; per adjoint: tile_vscale, scatter_i8 (builds its value digits itself), scatter_tiled (gated), "
                                   "halo_fold, zeta_crop, sph_adj, radial_adj, sumsq_c, absmax_c, guard_adj"
                                     if stats.get("i8_scatter") else
                                     "; per adjoint: scatter_tiled, halo_fold, zeta_crop, sph_adj, radial_adj") +

@@ -65,9 +65,16 @@ constexpr int B_STAGE = (KST / 8) * B_KBLK;      // one K-step of value digits (
 constexpr int NWG = 8 * NGRP;            // weight generator warps (per group: 32 nodes x 8 cell groups)
 constexpr int NEW = 8;                   // epilogue warps: EPW per TMEM lane quarter, 1/EPW of the columns each
 constexpr int EPW = NEW / 4;
-constexpr int NVW = 2;                   // value-digit generator warps (warp = K-step, lane = node)
+#ifndef SGL_NVW
+#define SGL_NVW 2
+#endif
+constexpr int NVW = SGL_NVW;                   // value-digit generator warps (warp = K-step, lane = node)
 constexpr int VSLOTS = 2;                // value-digit slots per CTA in global memory (tile parity)
 constexpr int V_SLOT = (SN / KST) * B_STAGE;   // one tile's value digits (16 K-steps, 240 KB)
+#ifndef SGL_VAHEAD
+#define SGL_VAHEAD 7
+#endif
+constexpr int VAHEAD = SGL_VAHEAD;       // the next tile's value digits are built during the last VAHEAD M-blocks
 constexpr int ST = (2 + NWG + NEW + NVW) * 32;
 
 struct SSmem {
@@ -82,6 +89,7 @@ struct SSmem {
     uint64_t fullA[NSTG], emptyA[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
     uint64_t vready[VSLOTS], vfree[VSLOTS];   // a tile's value digits written / all its MMAs done
+    uint64_t vgo;                             // the MMA warp is VAHEAD M-blocks from the tile's end
     uint32_t tbase;
 };
 
@@ -95,6 +103,7 @@ __device__ __forceinline__ void gen_sync() { asm volatile("bar.sync 1, %0;\n" ::
 __device__ __forceinline__ void red_add(double *addr, double v) {
     asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
+
 
 // SGL_FLAG_DETERMINISTIC: 64-bit fixed-point reduction (order-independent)
 __device__ __forceinline__ void red_add_s64(double *addr, long long v) {
@@ -116,10 +125,28 @@ __device__ __forceinline__ void st_async_v4(void *dst, const uint32_t (&v)[4], u
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     umma::smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(umma::smem_addr(bar))
+// L2 policy of the value-digit ring (written once per tile, re-read per
+// M-block): evict_last against the grid's RED stream, which otherwise pushes a
+// tile's digits out to DRAM between their write and their reads (config 3:
+// DRAM 3.3 + 4.6 GB per launch without the hint, 2.8 + 2.9 GB with it;
+// evict_first on the REDs as well: no further gain)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::
+            "r"(umma::smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(umma::smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void st_keep_v4(void *dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(dst), "r"(a), "r"(b), "r"(c),
+                 "r"(d), "l"(pol)
                  : "memory");
 }
 
@@ -131,7 +158,7 @@ __device__ __forceinline__ int ksteps(const Tile &t) { return (t.count + KST - 1
 // groups: one exp pair per node), written in the K-step's MN-major UMMA layout
 __device__ __forceinline__ void vdigits_kstep(const Tile &t, int svt, int ks, int kl, const NodeSet &nodes,
                                               const WindowParams &wp, const double2 *__restrict__ values,
-                                              uint8_t *__restrict__ blk) {
+                                              uint8_t *__restrict__ blk, uint64_t pol) {
     // 2^svt as 2^min(svt, 960) on the digit split and the rest on the value
     // first: values below ~1e-290 need svt > 1023 (r02 fix: the one-factor
     // scale overflowed to Inf), and the pre-scaled value keeps w1 v normal
@@ -170,8 +197,7 @@ __device__ __forceinline__ void vdigits_kstep(const Tile &t, int svt, int ks, in
         digits16(vsc, wv, dw);
 #pragma unroll
         for (int q = 0; q < ND; ++q)
-            *reinterpret_cast<uint4 *>(dst + vg * 128 + q * (ROWS / 16) * 128) =
-                make_uint4(dw[q][0], dw[q][1], dw[q][2], dw[q][3]);
+            st_keep_v4(dst + vg * 128 + q * (ROWS / 16) * 128, dw[q][0], dw[q][1], dw[q][2], dw[q][3], pol);
     }
 }
 
@@ -211,6 +237,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             mbar_init(&S.vready[s], NVW * 32);
             mbar_init(&S.vfree[s], 1);
         }
+        mbar_init(&S.vgo, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 0) umma::tmem_alloc(&S.tbase, TCOLS);
@@ -233,6 +260,9 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
+                // start the value warps on the next tile's digits: late enough that
+                // the digits are still in L2 at their first read, early enough to be done
+                if (mb == max(0, nmb - VAHEAD) && lane == 0) mbar_arrive(&S.vgo);
                 long long x0 = tick<PROF>();
                 if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
                 qe += tick<PROF>() - x0;
@@ -291,6 +321,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     } else if (warp == 1) {
         // ---- value-digit producer: one bulk copy per K-step (re-read from L2 per M-block)
         if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
             uint32_t g = 0;
             int pstg = 0;        // ring slot and the phase of its current use
             uint32_t pph = 0;
@@ -305,7 +336,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     for (int ks = 0; ks < nks; ++ks, ++g) {
                         if (g >= (uint32_t)NSTGB) mbar_wait(&S.emptyB[pstg], pph ^ 1);   // its previous use
                         mbar_expect_tx(&S.fullB[pstg], B_STAGE);
-                        bulk_load(S.b[pstg], src + ks * (int64_t)B_STAGE, B_STAGE, &S.fullB[pstg]);
+                        bulk_load(S.b[pstg], src + ks * (int64_t)B_STAGE, B_STAGE, &S.fullB[pstg], pol);
                         if (++pstg == NSTGB) {
                             pstg = 0;
                             pph ^= 1;
@@ -438,23 +469,35 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
         }
     } else if (warp >= 2 + NWG + NEW) {
         // ---- value-digit generators: V = w1 v does not depend on the M-block, so a
-        // tile's digits are written once, one tile ahead, into this CTA's slot of
+        // tile's digits are written once, during the previous tile's last M-blocks, into this CTA's slot of
         // an L2-resident ring in global memory (2 x 240 KB per CTA) and re-read
         // from there per M-block by the producer's bulk copies.  Generic-proxy
         // writes -> async-proxy reads: fence.proxy.async by every writer before
         // its arrive on vready.
         const int vw = warp - (2 + NWG + NEW);
+        const uint64_t pol = policy_evict_last();
         uint32_t tj = 0;
         for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++tj) {
             const Tile t = tiles[ti];
             const int slot = (int)(tj % VSLOTS);
+            if (tj >= 1) mbar_wait(&S.vgo, (tj - 1) & 1);   // one arrive per tile: tile tj - 1 is near its end
             if (tj >= (uint32_t)VSLOTS) mbar_wait(&S.vfree[slot], (tj / VSLOTS - 1) & 1);
             const int svt = __ldg(tsv + ti);
             uint8_t *dst = vring + ((size_t)blockIdx.x * VSLOTS + slot) * V_SLOT;
             for (int ks = vw; ks < ksteps(t); ks += NVW)
-                vdigits_kstep(t, svt, ks, lane, nodes, wp, values, dst + (size_t)ks * B_STAGE);
+                vdigits_kstep(t, svt, ks, lane, nodes, wp, values, dst + (size_t)ks * B_STAGE, pol);
             asm volatile("fence.proxy.async;\n" ::: "memory");
             mbar_arrive(&S.vready[slot]);
+            // the previous tile's digits are dead once all its MMAs are done: drop
+            // their (dirty) L2 lines instead of letting them be written back to DRAM
+            if (tj >= 1) {
+                const int ps = (int)((tj - 1) % VSLOTS);
+                mbar_wait(&S.vfree[ps], ((tj - 1) / VSLOTS) & 1);
+                const Tile pt = tiles[ti - gridDim.x];
+                uint8_t *old = vring + ((size_t)blockIdx.x * VSLOTS + ps) * V_SLOT;
+                for (int o = (vw * 32 + lane) * 128; o < ksteps(pt) * B_STAGE; o += NVW * 32 * 128)
+                    asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(old + o) : "memory");
+            }
         }
     } else {
         // ---- epilogue: thread = box cell of the M-block = TMEM lane
