@@ -260,9 +260,6 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             const Tile t = tiles[ti];
             const int nmb = mblocks(t), nks = ksteps(t);
             for (int mb = 0; mb < nmb; ++mb, ++mc) {
-                // start the value warps on the next tile's digits: late enough that
-                // the digits are still in L2 at their first read, early enough to be done
-                if (mb == max(0, nmb - VAHEAD) && lane == 0) mbar_arrive(&S.vgo);
                 long long x0 = tick<PROF>();
                 if (mc) mbar_wait(&S.tempty, (mc - 1) & 1);
                 qe += tick<PROF>() - x0;
@@ -271,6 +268,13 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     const int stg = (int)(g % NSTG);
                     long long x1 = tick<PROF>();
                     mbar_wait(&S.fullB[stgb], phb);
+                    // start the value warps on the next tile's digits: late enough that
+                    // the digits are still in L2 at their first read, early enough to be
+                    // done.  After this tile's first value digits have arrived, i.e. after
+                    // the value warps consumed the previous tile's vgo phase (short tiles
+                    // trigger at M-block 0: an arrive before that wait could complete two
+                    // phases ahead of the value warps' parity wait)
+                    if (ks == 0 && mb == max(0, nmb - VAHEAD) && lane == 0) mbar_arrive(&S.vgo);
                     long long x2 = tick<PROF>();
                     mbar_wait(&S.fullA[stg], (g / NSTG) & 1);
                     qa += tick<PROF>() - x2;
@@ -497,6 +501,12 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 uint8_t *old = vring + ((size_t)blockIdx.x * VSLOTS + ps) * V_SLOT;
                 for (int o = (vw * 32 + lane) * 128; o < ksteps(pt) * B_STAGE; o += NVW * 32 * 128)
                     asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(old + o) : "memory");
+                // the next tile's digits go to the same slot, and a line is written by
+                // other threads than the one that discards it: order every discard before
+                // every such write (short tiles start them back to back; found by
+                // tools/soak.py as 1e-2 errors on 2e5-node plans with q <= 8)
+                __threadfence_block();
+                asm volatile("bar.sync 2, %0;\n" ::"n"(NVW * 32) : "memory");
             }
         }
     } else {

@@ -231,3 +231,28 @@ def test_fused_call_on_int8_scatter(sgl, name):
     assert np.isnan(sgl.adjoint(p, vn)).any()
     f3, a3 = sgl.forward_adjoint(p, c, v)   # the flag is cleared again
     assert np.all(np.isfinite(a3)) and rel(a3, a0) <= 1e-13
+
+
+@pytest.mark.parametrize("B,q,kind", [(5, 8, "grid"), (5, 8, "lattice"), (8, 3, "lattice"), (27, 2, "ball"),
+                                      (29, 2, "lattice")])
+def test_int8_scatter_short_tiles(sgl, B, q, kind):
+    """2e5 nodes with small cutoffs: tiles of 512 nodes with only a few M-blocks,
+    so the value-digit warps of k_scatter_i8 run back to back (discard of the
+    finished tile's digits, then the next tile's writes to the same slot).  The
+    families tools/soak.py found a discard/write race on (1e-2 errors, run-to-run
+    different); against the FP64 scatter, three calls each."""
+    rng = np.random.default_rng(59)
+    M = 200_000
+    if kind == "grid":
+        pts = sgl.gen_grid(int(round(M ** (1 / 3))), 3.0)
+    elif kind == "ball":
+        pts = sgl.gen_points_ball(M, 2.0, rng)
+    else:   # many nodes on few positions
+        pts = np.column_stack([np.full(M, 1.0), rng.choice([0.0, np.pi / 2, np.pi], M),
+                               rng.choice([0.0, np.pi / 2, np.pi, 1.5 * np.pi], M)])
+    v = rng.uniform(-1, 1, len(pts)) + 1j * rng.uniform(-1, 1, len(pts))
+    p8 = _plan_i8s(sgl, B, pts, q=q)
+    pf = sgl.plan(B, pts, q=q, backend="tiled")
+    ref = sgl.adjoint(pf, v)
+    for _ in range(3):
+        assert rel(sgl.adjoint(p8, v), ref) <= TOL_I8
