@@ -55,7 +55,7 @@ constexpr int SN = kI8SNodes;            // nodes per tile (K)
 constexpr int MR = 128;                  // box cells per M-block (MMA M)
 constexpr int ROWS = 2 * kI8Box1;        // MMA N per digit: (b, re|im) = 80
 constexpr int NGRP = 2;                  // generator groups, alternating K-steps (group = ring stage)
-constexpr int NSTG = NGRP < 2 ? 2 : NGRP;              // weight-digit ring (one stage per generator group) (K-steps of 32 nodes)
+constexpr int NSTG = 3;                  // weight-digit ring (K-steps of 32 nodes): 1.5 stages per generator group
 constexpr int NSTGB = 3;                 // value-digit ring
 constexpr int KST = 32;                  // nodes per K-step
 constexpr int A_DIGIT = (KST / 8) * 8 * 128;   // 4 node blocks x 8 cell blocks x 128 B (MN-major)
@@ -80,17 +80,20 @@ constexpr int ST = (2 + NWG + NEW + NVW) * 32;
 struct SSmem {
     uint8_t a[NSTG][A_STAGE];    // weight digits [digit][node/8][cell/16][node%8][cell%16]
     uint8_t b[NSTGB][B_STAGE];   // value digits  [node/8][digit][col/16][node%8][col%16]
-    long long stage[ROWS][MR];   // epilogue: one M-block as exact int64 sums, [column][cell]
-    double e2[CHUNKS][SN], f2[CHUNKS][SN];   // W2 of chunk cc: w(cb + j) = e2 f2^j exp(-h2 j^2)
+    long long stage[ROWS - 4 * EPW][MR];   // epilogue: one M-block as exact int64 sums, [column][cell]; each
+                                 // warp's last 4 columns stay in its registers
+    double e2[CHUNKS][SN], f2[SN];   // W2 of chunk cc: w(cb + j) = e2[cc] (f2 kf[cc])^j exp(-h2 j^2)
     int win2[SN];                // axis-2 window relative to K column 0: lo | hi << 16 (signed)
     double w0t[4][SN];           // W0 of the current M-block's (<= 4) slabs, row = slab & 3
-    double w0s[SN], r0s[SN];     // axis-0 Gaussian walk per node: W0 of its next slab, ratio
-    int win0[SN];                // axis-0 window in tile slabs: lo | hi << 16 (signed)
     uint64_t fullA[NSTG], emptyA[NSTG], fullB[NSTGB], emptyB[NSTGB];
     uint64_t tfull, tempty;
     uint64_t vready[VSLOTS], vfree[VSLOTS];   // a tile's value digits written / all its MMAs done
     uint64_t vgo;                             // the MMA warp is VAHEAD M-blocks from the tile's end
     uint32_t tbase;
+};
+
+struct K3 {
+    double v[CHUNKS];   // exp(-32 h2 cc): chunk cc's ratio f2 of chunk 0's
 };
 
 struct G16 {
@@ -214,7 +217,7 @@ template <bool PROF, bool DET>
 __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
     k_scatter_i8(const Tile *__restrict__ tiles, int64_t ntiles, NodeSet nodes, WindowParams wp, double s0,
                  double s2, int sA, const int *__restrict__ tsv, const double2 *__restrict__ values,
-                 uint8_t *__restrict__ vring, double *__restrict__ grid, const G16 g2,
+                 uint8_t *__restrict__ vring, double *__restrict__ grid, const G16 g2, const K3 kf,
                  unsigned long long *__restrict__ prof, const int *__restrict__ skip,
                  const int *__restrict__ det) {
     if (*skip) return;   // non-finite values (guard.cu)
@@ -362,6 +365,11 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
             gen_sync();   // the previous tile's readers of the node tables are done
             const int kst = kstart2(t, wp) - wp.pad;   // cell of K-range column 0 (axis 2)
             const int kcount = ksteps(t) * KST;
+            // axis-0 Gaussian walk of this thread's node (thread gt owns node gt: SN == NWG * 32):
+            // W0 of its next slab, the ratio, its window in tile slabs (lo | hi << 16, signed)
+            static_assert(SN <= NWG * 32, "one generator thread per node of the tile");
+            double w0s = 0.0, r0s = 0.0;
+            int win0 = 0x7fff | (-1 << 16);
             for (int i = gt; i < kcount; i += NWG * 32) {
                 // per node: axis-0 coordinate, axis-2 window and the W2 factors of
                 // the three 16-cell chunks (2 exps per chunk here, none per K-step);
@@ -378,15 +386,15 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 window_cells(u0, wp.q, lo0, hi0);
                 lo0 = max(lo0, t.o0);   // (the box covers the window; kept for safety)
                 const double d0 = u0 - (double)lo0;
-                S.w0s[i] = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
-                S.r0s[i] = exp(wp.h0 * (2.0 * d0 - 1.0));
-                S.win0[i] = live ? ((lo0 - t.o0) & 0xffff) | ((hi0 - t.o0) << 16) : (0x7fff | (-1 << 16));
+                w0s = s0 * (wp.c0 * exp(-d0 * d0 * wp.h0));
+                r0s = exp(wp.h0 * (2.0 * d0 - 1.0));
+                if (live) win0 = ((lo0 - t.o0) & 0xffff) | ((hi0 - t.o0) << 16);
 #pragma unroll
                 for (int cc = 0; cc < CHUNKS; ++cc) {
                     const double d = u2 - (double)(kst + 16 * cc);
                     S.e2[cc][i] = live ? s2 * (wp.c2 * exp(-d * d * wp.h2)) : 0.0;
-                    S.f2[cc][i] = exp(2.0 * wp.h2 * d);
                 }
+                S.f2[i] = exp(2.0 * wp.h2 * (u2 - (double)kst));
             }
             gen_sync();
             qt += tick<PROF>() - x0;
@@ -400,8 +408,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 if (nxt <= a_mb + 3) {
                     gen_sync();   // the readers of the rows being replaced are done
                     for (int n = gt; n < kcount; n += NWG * 32) {
-                        const int wn = S.win0[n], lo = (int)(short)(wn & 0xffff), hi = wn >> 16;
-                        double w = S.w0s[n], r = S.r0s[n];
+                        const int lo = (int)(short)(win0 & 0xffff), hi = win0 >> 16;
+                        double w = w0s, r = r0s;
                         for (int x = nxt; x <= a_mb + 3; ++x) {
                             double v = 0.0;
                             if (x >= lo && x <= hi && x < t.e0) {
@@ -411,8 +419,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                             }
                             S.w0t[x & 3][n] = v;
                         }
-                        S.w0s[n] = w;
-                        S.r0s[n] = r;
+                        w0s = w;
+                        r0s = r;
                     }
                     nxt = a_mb + 4;
                     gen_sync();
@@ -420,7 +428,8 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 qw += tick<PROF>() - x1;
                 const int cid = mb * 8 + grp, al = cid / CHUNKS, cc = cid - CHUNKS * al;
                 // this thread's node tables for the M-block (padding nodes have e = 0)
-                const double *w0p = S.w0t[al & 3] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2[cc] + kl;
+                const double *w0p = S.w0t[al & 3] + kl, *e2p = S.e2[cc] + kl, *f2p = S.f2 + kl;
+                const double kfc = kf.v[cc];
                 const int *win2p = S.win2 + kl;
                 // this group's K-steps of the M-block only (global K-step g0 + ks; a
                 // strided loop instead of skipping the other group's: 29.19 -> 29.08 ms)
@@ -434,7 +443,7 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     // W0 folded into the chunk factor: w0 w2(cb + j) = (w0 e) f^j g_j, so
                     // the g_j product is the digit FMA itself (one DMUL per entry fewer;
                     // scatter 29.67 -> 29.56 ms at config 3)
-                    const double e = w0p[kn] * e2p[kn], f = f2p[kn];
+                    const double e = w0p[kn] * e2p[kn], f = f2p[kn] * kfc;
                     const int wn = win2p[kn], jlo = (int)(short)(wn & 0xffff) - 16 * cc, jhi = (wn >> 16) - 16 * cc;
                     // the node's window [jlo, jhi] inside this 16-cell chunk as an entry mask
                     const uint32_t mask = (jhi < 0 || jlo > 15)
@@ -535,7 +544,9 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                 // the TMEM loads of step i+1 are in flight while step i converts
                 constexpr int CB4 = ROWS / 4 / EPW;   // 4-column steps of this warp
                 const int c0 = eh * CB4;
+                constexpr int SROWS = (CB4 - 1) * 4;   // staged columns of this warp
                 int32_t D[2][NBLK][4];
+                long long keep[4];
                 __syncwarp();   // tcgen05.ld is .sync.aligned
 #pragma unroll
                 for (int k = 0; k < NBLK; ++k) umma::tmem_ld4(tl + (uint32_t)(k * ROWS + c0 * 4), D[0][k]);
@@ -551,32 +562,42 @@ __global__ void __cluster_dims__(1, 1, 1) __launch_bounds__(ST, 1)
                     // the exact int64 only: its conversion to FP64 waits until after
                     // the TMEM release (scatter 29.73 -> 29.29 ms at config 3)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        S.stage[(c0 + i) * 4 + j][m] = combine6_i64(D[cur][0][j], D[cur][1][j], D[cur][2][j],
-                                                                    D[cur][3][j], D[cur][4][j], D[cur][5][j]);
+                    for (int j = 0; j < 4; ++j) {
+                        const long long x = combine6_i64(D[cur][0][j], D[cur][1][j], D[cur][2][j], D[cur][3][j],
+                                                         D[cur][4][j], D[cur][5][j]);
+                        if (i + 1 < CB4) S.stage[eh * SROWS + i * 4 + j][m] = x;
+                        else keep[j] = x;   // the last step stays in registers (8 KB of staging less)
+                    }
                     umma::tmem_ld_wait();
                 }
                 umma::fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.tempty);   // TMEM free: the next block's MMAs overlap the REDs
                 if (inbox) {
-                    for (int b = eh * (ROWS / 2 / EPW); b < min(t.e1, (eh + 1) * (ROWS / 2 / EPW)); ++b) {
+                    // one axis-1 cell (re, im) of this thread's grid column
+                    auto emit = [&](int b, long long sre, long long sim) {
                         double *q = gp + 2 * (size_t)b * wp.N2p;
                         SGL_DCHECK(wrap1(t.o0 + al, wp.N0) < wp.N0 && t.o1 + wp.pad + b < wp.N1p &&
                                    kst + cl >= 0 && kst + cl < wp.N2p);
                         if (DET) {
-                            if (sv == NOSLAB) continue;
-                            const long long xr = fix_shift(S.stage[2 * b][m], dsh);
-                            const long long xi = fix_shift(S.stage[2 * b + 1][m], dsh);
+                            if (sv == NOSLAB) return;
+                            const long long xr = fix_shift(sre, dsh);
+                            const long long xi = fix_shift(sim, dsh);
                             if (xr != 0) red_add_s64(q, xr);
                             if (xi != 0) red_add_s64(q + 1, xi);
                         } else {
-                            const double re = (double)S.stage[2 * b][m] * unit;
-                            const double im = (double)S.stage[2 * b + 1][m] * unit;
+                            const double re = (double)sre * unit;
+                            const double im = (double)sim * unit;
                             if (re != 0.0) red_add(q, re);
                             if (im != 0.0) red_add(q + 1, im);
                         }
-                    }
+                    };
+                    constexpr int BW = ROWS / 2 / EPW;   // axis-1 cells of this warp: BW - 2 staged, 2 in registers
+                    const int b0 = eh * BW;
+                    for (int lb = 0; lb < min(t.e1 - b0, BW - 2); ++lb)
+                        emit(b0 + lb, S.stage[eh * SROWS + 2 * lb][m], S.stage[eh * SROWS + 2 * lb + 1][m]);
+                    if (b0 + BW - 2 < t.e1) emit(b0 + BW - 2, keep[0], keep[1]);
+                    if (b0 + BW - 1 < t.e1) emit(b0 + BW - 1, keep[2], keep[3]);
                 }
             }
         }
@@ -671,9 +692,11 @@ int launch_scatter_i8(const Plan &p, const double2 *values, double2 *grid, cudaS
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(p.n_istiles, sms));
     G16 g2;
     for (int j = 0; j < 16; ++j) g2.v[j] = std::exp(-p.wp.h2 * (double)(j * j));
+    K3 kf;
+    for (int cc = 0; cc < CHUNKS; ++cc) kf.v[cc] = std::exp(-32.0 * p.wp.h2 * (double)cc);
     kern<<<(unsigned)blocks, ST, sm, st>>>(p.istiles, p.n_istiles, p.inodes, p.wp, std::ldexp(1.0, a0),
                                                   std::ldexp(1.0, sA - a0), sA, p.tsv, values, p.vdig,
-                                                  reinterpret_cast<double *>(grid), g2, prof, skip, det);
+                                                  reinterpret_cast<double *>(grid), g2, kf, prof, skip, det);
     SGL_CUDA_CHECK(cudaGetLastError());
     if (want) {   // SGL_I8_PROF=1: where the MMA warp waits (debug)
         std::vector<unsigned long long> h(8 * blocks);
