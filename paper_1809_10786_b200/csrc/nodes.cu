@@ -656,7 +656,7 @@ int build_nodes(Plan &p, const double *pts, cudaStream_t st) {
                 // per node (config-3 subsamples, i.e. the node shards of a
                 // strong-scaling run: 1.2-1.7x, profiles/r02/scatter_crossover.txt;
                 // config 3: 29.7 vs 50 ms); below ~1e5 nodes its per-plan setup
-                // (value-digit buffers, guard calibration) is not worth it.  Inputs
+                // (value-digit ring, guard calibration) is not worth it.  Inputs
                 // the accuracy guard keeps rejecting switch the plan to FP64 at run
                 // time (Plan::i8s_off, capi.cu)
                 TileStats ts;
